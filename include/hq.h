@@ -1,0 +1,150 @@
+/*
+ * hq.h — C ABI of the B200 batched variational-circuit simulator.
+ *
+ * This is the drop-in boundary for the reference's hot path (VQNet 2.0 /
+ * `hyqnet`, pure Python + NumPy).  Each entry point replaces one piece of it:
+ *
+ *   hq_plan_create   replaces the per-evaluation circuit rebuild + validation:
+ *                    QuantumLayer._build (pkg/src/hyqnet/qnn.py:95-105),
+ *                    GateOp.__post_init__ / Circuit.add (qsim.py:54-71,109-113).
+ *                    The tape is traced once per batch (tracer.py), not per
+ *                    evaluation.
+ *   hq_forward       replaces the serial batch loop of QuantumLayer.forward
+ *                    (qnn.py:123-133): simulate (qsim.py:179-191) + apply_gate
+ *                    (qsim.py:150-176) + probabilities (qsim.py:194-211) + the
+ *                    EXACT_PROB readout E = Σ_j j·P(j) (qnn.py:107-116).  With
+ *                    HQ_WANT_JAC it also produces, per sample, the row the
+ *                    reference's df_x / df_p closures compute with
+ *                    parameter_shift_grad (qnn.py:35-52,136-153) at upstream 1.
+ *   hq_vjp           replaces the upstream scaling + sequential batch sum of
+ *                    df_x / df_p (qnn.py:137-152).
+ *   hq_state         replaces simulate() returning the amplitudes
+ *                    (qsim.py:179-191), for StateVector-level parity tests.
+ *
+ * Conventions (all pinned by the reference tests): qubit k is
+ * bit k of the amplitude index; rotations are half-angle; CR(θ) multiplies
+ * |11⟩ by e^{iθ}; the readout weights are w(idx) = Σ_i 2^i·bit(idx, measured[i]).
+ *
+ * All pointers passed to hq_forward / hq_vjp / hq_state are DEVICE pointers
+ * (caller-owned, e.g. torch tensors); `stream` is a cudaStream_t.  Plans are
+ * immutable after creation and may be used concurrently on distinct streams
+ * with distinct workspaces.  Errors: a non-zero hq_status plus a thread-local
+ * message from hq_last_error(); the Python layer maps HQ_E_CIRCUIT ->
+ * CircuitError, HQ_E_CONFIG -> ConfigError, HQ_E_DIMENSION -> DimensionError,
+ * HQ_E_ENCODING -> EncodingError (errors.py:8-26), anything else -> NativeError.
+ */
+#ifndef HQ_H
+#define HQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HQ_ABI_VERSION 1
+
+typedef struct hq_plan_s* hq_plan;
+
+typedef enum {
+  HQ_OK = 0,
+  HQ_E_CIRCUIT = 1,
+  HQ_E_CONFIG = 2,
+  HQ_E_DIMENSION = 3,
+  HQ_E_CUDA = 4,
+  HQ_E_OOM = 5,
+  HQ_E_ENCODING = 6
+} hq_status;
+
+/* amplitude precision: complex64 (fast mode, 1e-5) or complex128 (reference, 1e-10) */
+enum { HQ_C64 = 0, HQ_C128 = 1 };
+
+/* gate kinds: qsim.py:19-22 plus the native state load */
+enum {
+  HQ_GATE_H = 0, HQ_GATE_X = 1, HQ_GATE_Y = 2, HQ_GATE_Z = 3,
+  HQ_GATE_RX = 4, HQ_GATE_RY = 5, HQ_GATE_RZ = 6,
+  HQ_GATE_CNOT = 7, HQ_GATE_CZ = 8, HQ_GATE_CR = 9, HQ_GATE_SWAP = 10,
+  HQ_GATE_STATEPREP = 11
+};
+
+/* gradient mode per variable (inputs first, then params) */
+enum { HQ_GRAD_ZERO = 0, HQ_GRAD_ADJOINT = 1, HQ_GRAD_TWOPOINT = 2 };
+
+/* hq_forward flags */
+enum { HQ_WANT_JAC = 1 };
+
+/* One tape entry.  q0 is the control of CNOT/CZ/CR (GateOp targets order).
+ * slot indexes the affine slot table for RX/RY/RZ/CR, else -1.
+ * STATEPREP: q0 = index into the prep table, q1 = slot = -1. */
+typedef struct {
+  int32_t kind, q0, q1, slot;
+} hq_op;
+
+typedef struct {
+  int32_t n_qubits;
+  int32_t precision;                 /* HQ_C64 | HQ_C128 */
+  int32_t n_ops;
+  const hq_op* ops;
+  /* affine slots: value[s] = slot_const[s] + Σ_{k in [slot_ptr[s], slot_ptr[s+1])}
+   *               slot_coef[k] * var[slot_var[k]],  var = [inputs | params] */
+  int32_t n_slots;
+  const double* slot_const;
+  const int32_t* slot_ptr;           /* n_slots + 1 */
+  const int32_t* slot_var;
+  const double* slot_coef;
+  int32_t n_inputs, n_params;
+  int32_t n_measured;                /* 0 => all qubits (qnn.py:108) */
+  const int32_t* measured;
+  /* state loads (amplitude_embedding): prep p covers qubits
+   * prep_qubits[prep_ptr[p] .. prep_ptr[p+1]) (value bit i -> qubit i of that
+   * list) with values = slots [prep_slot0[p], prep_slot0[p] + prep_len[p]) */
+  int32_t n_preps;
+  const int32_t* prep_ptr;
+  const int32_t* prep_qubits;
+  const int32_t* prep_slot0;
+  const int32_t* prep_len;
+  /* gradient spec, length n_inputs + n_params (NULL => no gradient) */
+  const int32_t* grad_mode;
+  const int32_t* grad_slot;          /* ADJOINT: the single slot the variable enters */
+  const double* grad_factor;         /* ADJOINT: 2*grad_scale*sin(coef*shift) */
+  double shift;                      /* qnn.py:64, default pi/2 */
+  double grad_scale;                 /* qnn.py:64, default 0.5 */
+} hq_plan_desc;
+
+int hq_abi_version(void);
+const char* hq_last_error(void);
+
+hq_status hq_plan_create(const hq_plan_desc* desc, hq_plan* out);
+void hq_plan_destroy(hq_plan plan);
+
+/* human-readable execution plan (kernel choice, passes) — valid until the plan dies */
+const char* hq_plan_describe(hq_plan plan);
+
+/* bytes of device workspace hq_forward / hq_state need for `batch` samples */
+size_t hq_workspace_bytes(hq_plan plan, int64_t batch, int32_t flags);
+
+/* out[b] = E(x[b], theta); with HQ_WANT_JAC, jac[b, v] (row stride
+ * n_inputs + n_params) = the reference's per-sample shift-rule gradient at
+ * upstream 1 for every variable with a non-ZERO mode, 0 otherwise.
+ * x: [batch, ldx] f64, theta: [n_params] f64, out: [batch] f64. */
+hq_status hq_forward(hq_plan plan, const double* x, int64_t ldx, const double* theta,
+                     int64_t batch, int32_t flags, double* out, double* jac,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* grad_x[b, i] = upstream[b] * jac[b, i];
+ * grad_theta[j] = Σ_b upstream[b] * jac[b, n_inputs + j], summed in sample
+ * order (qnn.py:147-152).  Either output may be NULL. */
+hq_status hq_vjp(hq_plan plan, const double* jac, const double* upstream, int64_t batch,
+                 double* grad_x, double* grad_theta, void* stream);
+
+/* final amplitudes, interleaved complex128 [batch, 2^n, 2]; `init` (optional,
+ * same layout, batch rows or 1 row broadcast) replaces |0...0>. */
+hq_status hq_state(hq_plan plan, const double* x, int64_t ldx, const double* theta,
+                   int64_t batch, const double* init, int64_t init_rows, double* state,
+                   void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HQ_H */

@@ -1,0 +1,601 @@
+// C ABI + host planner of the batched circuit simulator (see include/hq.h).
+//
+// Plan creation validates the tape the way the reference validates circuits
+// (GateOp.__post_init__ qsim.py:54-71, Circuit.add qsim.py:109-113,
+// Circuit.measure qsim.py:132-140), decides the execution path, and for the
+// HBM path schedules gates into passes:
+//
+//   * a pass = one read + one write of the state, tile = 2^q amplitudes over q
+//     "local" qubits, the low f qubits always local (contiguous 64 B runs);
+//   * a gate joins the current pass when no earlier unscheduled gate shares a
+//     qubit with it and its exchange qubits (targets of non-diagonal kinds) are
+//     local; diagonal kinds and controls may sit on non-local qubits because
+//     their bit is constant over a tile.
+//
+// Everything device-side of a plan lives in one cudaMalloc.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "hq_internal.h"
+#include "hq_launch.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+hq_status fail(hq_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+constexpr int kMaxQubits = 34;
+constexpr int kMaxPreps = 32;
+constexpr size_t kMaxPassOps = 2048;   // bounds the per-pass trig cache in shared memory
+
+bool takes_angle(int k) {
+  return k == HQ_GATE_RX || k == HQ_GATE_RY || k == HQ_GATE_RZ || k == HQ_GATE_CR;
+}
+bool two_qubit(int k) {
+  return k == HQ_GATE_CNOT || k == HQ_GATE_CZ || k == HQ_GATE_CR || k == HQ_GATE_SWAP;
+}
+const char* kind_name(int k) {
+  static const char* names[] = {"H", "X", "Y", "Z", "RX", "RY", "RZ", "CNOT", "CZ", "CR", "SWAP", "STATEPREP"};
+  return (k >= 0 && k <= 11) ? names[k] : "?";
+}
+
+uint64_t op_mask(const hq_op& op) {
+  uint64_t m = 1ull << op.q0;
+  if (two_qubit(op.kind)) m |= 1ull << op.q1;
+  return m;
+}
+// qubits that must be resident in a tile (pairs are exchanged along them)
+uint64_t exch_mask(const hq_op& op) {
+  switch (op.kind) {
+    case HQ_GATE_H: case HQ_GATE_X: case HQ_GATE_Y: case HQ_GATE_RX: case HQ_GATE_RY:
+      return 1ull << op.q0;
+    case HQ_GATE_CNOT:
+      return 1ull << op.q1;
+    case HQ_GATE_SWAP:
+      return (1ull << op.q0) | (1ull << op.q1);
+    default:
+      return 0;
+  }
+}
+int popc(uint64_t m) { return __builtin_popcountll(m); }
+
+size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
+
+int onchip_max_qubits(int precision) { return precision == HQ_C64 ? 13 : 12; }
+int tile_bits_for(int precision) { return precision == HQ_C64 ? 12 : 11; }
+int fixed_bits_for(int precision) { return precision == HQ_C64 ? 3 : 2; }
+
+int64_t ws_budget() {
+  const char* e = std::getenv("HQ_WS_BUDGET_MB");
+  int64_t mb = e ? std::atoll(e) : 24 * 1024;
+  if (mb < 64) mb = 64;
+  return mb << 20;
+}
+
+struct Layout {
+  int64_t V = 0;
+  size_t tp = 0, dpart = 0, psi = 0, lam = 0, rpart = 0, scratch = 0, total = 0;
+  int32_t n_parts = 1;
+  hq::StreamWs sws;
+};
+
+Layout layout_for(const hq_plan_s* pl, int64_t B, int32_t flags, bool need_state_only = false) {
+  Layout L;
+  const bool jac = (flags & HQ_WANT_JAC) != 0;
+  L.V = B + (jac ? B * 2 * pl->n_tp : 0);
+  const size_t amp = pl->precision == HQ_C64 ? 8 : 16;
+  size_t off = 0;
+  if (pl->onchip) {
+    L.n_parts = hq::onchip_parts(pl);
+  } else {
+    const int64_t n_tiles = 1ll << (pl->n_qubits - pl->tile_bits);
+    const bool adj = jac && pl->n_adj > 0;
+    const int64_t per = (int64_t)amp << pl->n_qubits;
+    int64_t cs = ws_budget() / (per * (adj ? 2 : 1));
+    if (cs < 1) cs = 1;
+    if (cs > L.V) cs = L.V;
+    if (cs < 1) cs = 1;
+    int64_t want = (1184 + cs - 1) / cs;  // >= ~8 CTAs per SM per launch
+    int64_t nc = 16;
+    while (nc < want) nc <<= 1;
+    if (nc > n_tiles) nc = n_tiles;
+    L.sws.chunk_samples = cs;
+    L.sws.n_chunks = (int32_t)nc;
+    L.n_parts = (int32_t)nc;
+    L.psi = off; off = align_up(off + (size_t)cs * per);
+    if (adj) { L.lam = off; off = align_up(off + (size_t)cs * per); }
+    L.rpart = off; off = align_up(off + (size_t)cs * nc * 8);
+  }
+  (void)need_state_only;
+  L.scratch = off; off = align_up(off + (size_t)B * 8 + 8);   // readout sink for hq_state
+  if (jac) {
+    L.tp = off; off = align_up(off + (size_t)B * 2 * pl->n_tp * 8 + 8);
+    L.dpart = off; off = align_up(off + (size_t)B * pl->n_adj * L.n_parts * 8 + 8);
+  }
+  L.total = off + 256;
+  return L;
+}
+
+}  // namespace
+
+extern "C" int hq_abi_version(void) { return HQ_ABI_VERSION; }
+extern "C" const char* hq_last_error(void) { return g_err.c_str(); }
+
+// ---------------------------------------------------------------------------
+static hq_status validate(const hq_plan_desc* d) {
+  if (!d) return fail(HQ_E_CONFIG, "null plan descriptor");
+  if (d->n_qubits < 1 || d->n_qubits > kMaxQubits)
+    return fail(HQ_E_CIRCUIT, "n_qubits must be in 1.." + std::to_string(kMaxQubits) + ", got " +
+                                  std::to_string(d->n_qubits));
+  if (d->precision != HQ_C64 && d->precision != HQ_C128) return fail(HQ_E_CONFIG, "unknown precision");
+  if (d->n_ops < 0 || (d->n_ops > 0 && !d->ops)) return fail(HQ_E_CONFIG, "bad op array");
+  if (d->n_slots < 0 || (d->n_slots > 0 && (!d->slot_const || !d->slot_ptr)))
+    return fail(HQ_E_CONFIG, "bad slot table");
+  if (d->n_inputs < 0 || d->n_params < 0) return fail(HQ_E_CONFIG, "negative variable count");
+  const int nvars = d->n_inputs + d->n_params;
+  if (d->n_slots > 0) {
+    if (d->slot_ptr[0] != 0) return fail(HQ_E_CONFIG, "slot_ptr[0] must be 0");
+    for (int s = 0; s < d->n_slots; ++s) {
+      if (d->slot_ptr[s + 1] < d->slot_ptr[s]) return fail(HQ_E_CONFIG, "slot_ptr not monotone");
+      for (int k = d->slot_ptr[s]; k < d->slot_ptr[s + 1]; ++k)
+        if (d->slot_var[k] < 0 || d->slot_var[k] >= nvars) return fail(HQ_E_CONFIG, "slot variable out of range");
+    }
+  }
+  if (d->n_preps < 0 || d->n_preps > kMaxPreps) return fail(HQ_E_CONFIG, "too many state loads");
+  for (int p = 0; p < d->n_preps; ++p) {
+    const int q0 = d->prep_ptr[p], q1 = d->prep_ptr[p + 1];
+    if (q1 <= q0) return fail(HQ_E_CIRCUIT, "empty state load");
+    uint64_t m = 0;
+    for (int k = q0; k < q1; ++k) {
+      const int q = d->prep_qubits[k];
+      if (q < 0 || q >= d->n_qubits) return fail(HQ_E_CIRCUIT, "state-load qubit out of range");
+      if (m & (1ull << q)) return fail(HQ_E_CIRCUIT, "duplicate qubit in state load");
+      m |= 1ull << q;
+    }
+    if (d->prep_len[p] < 1 || (int64_t)d->prep_len[p] > (1ll << (q1 - q0)))
+      return fail(HQ_E_ENCODING, "state-load vector exceeds its qubits");
+    if (d->prep_slot0[p] < 0 || d->prep_slot0[p] + d->prep_len[p] > d->n_slots)
+      return fail(HQ_E_CONFIG, "state-load slots out of range");
+  }
+  for (int i = 0; i < d->n_ops; ++i) {
+    const hq_op& op = d->ops[i];
+    if (op.kind < 0 || op.kind > HQ_GATE_STATEPREP)
+      return fail(HQ_E_CIRCUIT, "unknown gate kind " + std::to_string(op.kind));
+    if (op.kind == HQ_GATE_STATEPREP) {
+      if (op.q0 < 0 || op.q0 >= d->n_preps) return fail(HQ_E_CONFIG, "bad state-load index");
+      continue;
+    }
+    if (op.q0 < 0 || op.q0 >= d->n_qubits)
+      return fail(HQ_E_CIRCUIT, std::string(kind_name(op.kind)) + " targets exceed " +
+                                    std::to_string(d->n_qubits) + " qubits");
+    if (two_qubit(op.kind)) {
+      if (op.q1 < 0 || op.q1 >= d->n_qubits)
+        return fail(HQ_E_CIRCUIT, std::string(kind_name(op.kind)) + " targets exceed " +
+                                      std::to_string(d->n_qubits) + " qubits");
+      if (op.q1 == op.q0) return fail(HQ_E_CIRCUIT, std::string("duplicate targets in ") + kind_name(op.kind));
+    }
+    if (takes_angle(op.kind)) {
+      if (op.slot < 0 || op.slot >= d->n_slots) return fail(HQ_E_CIRCUIT, std::string(kind_name(op.kind)) + " requires one finite angle");
+    } else if (op.slot >= 0) {
+      return fail(HQ_E_CIRCUIT, std::string(kind_name(op.kind)) + " takes no angle");
+    }
+  }
+  if (d->n_measured < 0 || (d->n_measured > 0 && !d->measured)) return fail(HQ_E_CONFIG, "bad measured list");
+  uint64_t mm = 0;
+  for (int i = 0; i < d->n_measured; ++i) {
+    const int q = d->measured[i];
+    if (q < 0 || q >= d->n_qubits) return fail(HQ_E_CIRCUIT, "measured qubit " + std::to_string(q) + " out of range");
+    if (mm & (1ull << q)) return fail(HQ_E_CIRCUIT, "qubit " + std::to_string(q) + " measured twice");
+    mm |= 1ull << q;
+  }
+  if (d->grad_mode) {
+    for (int v = 0; v < nvars; ++v) {
+      const int m = d->grad_mode[v];
+      if (m < HQ_GRAD_ZERO || m > HQ_GRAD_TWOPOINT) return fail(HQ_E_CONFIG, "bad gradient mode");
+      if (m == HQ_GRAD_ADJOINT && (d->grad_slot[v] < 0 || d->grad_slot[v] >= d->n_slots))
+        return fail(HQ_E_CONFIG, "adjoint variable without a slot");
+    }
+  }
+  if (!(d->shift > 0.0)) return fail(HQ_E_CONFIG, "shift must be positive");
+  return HQ_OK;
+}
+
+namespace {
+
+// Greedy pass scheduler (see file comment).
+std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int q, int f) {
+  std::vector<hq::Pass> passes;
+  std::vector<char> done(ops.size(), 0);
+  size_t left = ops.size();
+  const uint64_t fixed = (f >= 64) ? ~0ull : ((1ull << f) - 1);
+  while (left > 0) {
+    uint64_t L = fixed;
+    hq::Pass ps;
+    bool progress = true;
+    bool first_scan = true;
+    while (progress) {
+      progress = false;
+      uint64_t blocked = 0;
+      for (size_t k = 0; k < ops.size(); ++k) {
+        if (done[k]) continue;
+        const uint64_t qs = op_mask(ops[k]);
+        if (qs & blocked) { blocked |= qs; continue; }
+        const uint64_t ex = exch_mask(ops[k]);
+        if (ps.op_ids.size() >= kMaxPassOps) { blocked |= qs; continue; }
+        if ((ex & ~L) == 0 || popc(L | ex) <= q) {
+          L |= ex;
+          done[k] = 1;
+          --left;
+          ps.op_ids.push_back((int32_t)k);
+          progress = true;
+        } else {
+          blocked |= qs;
+        }
+      }
+      if (first_scan) {
+        // top up the tile with the lowest remaining qubits, then rescan
+        for (int b = 0; b < n && popc(L) < q; ++b) L |= 1ull << b;
+        first_scan = false;
+        progress = true;
+      }
+    }
+    for (int b = 0; b < n; ++b)
+      if (L & (1ull << b)) ps.local.push_back(b);
+    passes.push_back(std::move(ps));
+  }
+  if (passes.empty()) {
+    hq::Pass ps;
+    for (int b = 0; b < q; ++b) ps.local.push_back(b);
+    passes.push_back(std::move(ps));
+  }
+  return passes;
+}
+
+template <typename T>
+void put(std::vector<char>& blob, size_t& off, const T* src, size_t count, const T*& dst_dev_rel) {
+  off = align_up(off, 16);
+  if (blob.size() < off + count * sizeof(T)) blob.resize(off + count * sizeof(T));
+  if (count) std::memcpy(blob.data() + off, src, count * sizeof(T));
+  dst_dev_rel = reinterpret_cast<const T*>(off);
+  off += count * sizeof(T);
+}
+
+template <typename T>
+const T* rebase(const T* rel, char* base) {
+  return reinterpret_cast<const T*>(base + reinterpret_cast<size_t>(rel));
+}
+
+}  // namespace
+
+extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
+  if (!out) return fail(HQ_E_CONFIG, "null output");
+  *out = nullptr;
+  hq_status st = validate(d);
+  if (st != HQ_OK) return st;
+  auto pl = new hq_plan_s();
+  const int n = d->n_qubits;
+  const int nvars = d->n_inputs + d->n_params;
+  pl->n_qubits = n;
+  pl->precision = d->precision;
+  pl->n_inputs = d->n_inputs;
+  pl->n_params = d->n_params;
+  pl->n_slots = d->n_slots;
+
+  // ---- state loads must precede every gate on their qubits ----------------
+  std::vector<hq_op> gates;
+  uint64_t touched = 0, prep_mask = 0;
+  for (int i = 0; i < d->n_ops; ++i) {
+    const hq_op& op = d->ops[i];
+    if (op.kind == HQ_GATE_STATEPREP) {
+      uint64_t m = 0;
+      for (int k = d->prep_ptr[op.q0]; k < d->prep_ptr[op.q0 + 1]; ++k) m |= 1ull << d->prep_qubits[k];
+      if ((m & touched) || (m & prep_mask)) {
+        delete pl;
+        return fail(HQ_E_CIRCUIT, "state load after gates on its qubits has no native lowering");
+      }
+      prep_mask |= m;
+      continue;
+    }
+    touched |= op_mask(op);
+    gates.push_back(op);
+  }
+  pl->has_preps = d->n_preps > 0;
+  std::vector<int32_t> prep_off(d->n_preps);
+  for (int p = 0; p < d->n_preps; ++p) { prep_off[p] = pl->prep_total; pl->prep_total += d->prep_len[p]; }
+
+  // ---- gradient bookkeeping -------------------------------------------------
+  std::vector<int32_t> var_mode(nvars, HQ_GRAD_ZERO), var_dsl(nvars, -1), var_tp(nvars, -1), tp_var;
+  std::vector<double> var_factor(nvars, 0.0);
+  std::map<int, int> dsl_of_slot;
+  if (d->grad_mode) {
+    for (int v = 0; v < nvars; ++v) {
+      var_mode[v] = d->grad_mode[v];
+      if (var_mode[v] == HQ_GRAD_ADJOINT) {
+        const int s = d->grad_slot[v];
+        auto it = dsl_of_slot.find(s);
+        if (it == dsl_of_slot.end()) it = dsl_of_slot.emplace(s, (int)dsl_of_slot.size()).first;
+        var_dsl[v] = it->second;
+        var_factor[v] = d->grad_factor[v];
+      } else if (var_mode[v] == HQ_GRAD_TWOPOINT) {
+        var_tp[v] = (int32_t)tp_var.size();
+        tp_var.push_back(v);
+      }
+    }
+  }
+  pl->n_adj = (int32_t)dsl_of_slot.size();
+  pl->n_tp = (int32_t)tp_var.size();
+  pl->host_var_mode = var_mode;
+  std::vector<int> slot_users(d->n_slots, 0);
+  for (const auto& g : gates) if (g.slot >= 0) slot_users[g.slot]++;
+  for (const auto& kv : dsl_of_slot) {
+    if (slot_users[kv.first] != 1) {
+      delete pl;
+      return fail(HQ_E_CONFIG, "adjoint slot must feed exactly one gate");
+    }
+  }
+  auto dslot_of = [&](const hq_op& g) -> int {
+    if (g.slot < 0) return -1;
+    auto it = dsl_of_slot.find(g.slot);
+    return it == dsl_of_slot.end() ? -1 : it->second;
+  };
+
+  // ---- execution path ---------------------------------------------------------
+  // HQ_FORCE_STREAM / HQ_TILE_BITS: test hooks that push small circuits through
+  // the multi-pass HBM path (parity of the pass planner against the oracle)
+  const char* force = std::getenv("HQ_FORCE_STREAM");
+  const char* tb_env = std::getenv("HQ_TILE_BITS");
+  pl->onchip = n <= onchip_max_qubits(d->precision) && !(force && force[0] == '1');
+  std::vector<int32_t> pass_slots, pass_dlist, pass_local;
+  if (pl->onchip) {
+    pl->tile_bits = n;
+    for (const auto& g : gates) {
+      hq::DOp o{};
+      o.kind = g.kind;
+      o.a = g.q0;
+      o.b = two_qubit(g.kind) ? g.q1 : -1;
+      o.slot = g.slot;
+      o.dslot = dslot_of(g);
+      pl->dops.push_back(o);
+    }
+    if (hq::onchip_smem_bytes(pl) > 220 * 1024) pl->onchip = false;
+  }
+  if (!pl->onchip) {
+    pl->dops.clear();
+    pl->tile_bits = tile_bits_for(d->precision);
+    if (tb_env) pl->tile_bits = std::max(3, std::min(pl->tile_bits, std::atoi(tb_env)));
+    if (n <= pl->tile_bits) pl->tile_bits = n - 1;
+    if (pl->tile_bits < 2) {
+      delete pl;
+      return fail(HQ_E_CONFIG, "circuit too small for the streaming path");
+    }
+    const int f = std::min(fixed_bits_for(d->precision), pl->tile_bits - 2);
+    pl->passes = schedule_passes(gates, n, pl->tile_bits, f);
+    for (auto& ps : pl->passes) {
+      int pos[kMaxQubits];
+      for (int b = 0; b < n; ++b) pos[b] = ~b;
+      for (int i = 0; i < (int)ps.local.size(); ++i) pos[ps.local[i]] = i;
+      std::map<int, int> local_slot;
+      ps.first_dop = (int32_t)pl->dops.size();
+      ps.first_dlist = (int32_t)pass_dlist.size();
+      for (int k : ps.op_ids) {
+        const hq_op& g = gates[k];
+        hq::DOp o{};
+        o.kind = g.kind;
+        o.a = pos[g.q0];
+        o.b = two_qubit(g.kind) ? pos[g.q1] : -1;
+        o.slot = -1;
+        if (g.slot >= 0) {
+          auto it = local_slot.find(g.slot);
+          if (it == local_slot.end()) {
+            it = local_slot.emplace(g.slot, (int)ps.slots.size()).first;
+            ps.slots.push_back(g.slot);
+          }
+          o.slot = it->second;
+        }
+        o.dslot = dslot_of(g);
+        if (o.dslot >= 0) pass_dlist.push_back(o.dslot);
+        pl->dops.push_back(o);
+      }
+      ps.n_dops = (int32_t)ps.op_ids.size();
+      ps.n_dslots_pass = (int32_t)pass_dlist.size() - ps.first_dlist;
+      ps.first_slotlist = (int32_t)pass_slots.size();
+      pass_slots.insert(pass_slots.end(), ps.slots.begin(), ps.slots.end());
+      // local qubits then non-local, in increasing order
+      std::vector<int32_t> row(ps.local.begin(), ps.local.end());
+      for (int b = 0; b < n; ++b)
+        if (pos[b] < 0) row.push_back(b);
+      pass_local.insert(pass_local.end(), row.begin(), row.end());
+      pl->max_pass_slots = std::max(pl->max_pass_slots, (int32_t)ps.slots.size());
+      pl->max_pass_dl = std::max(pl->max_pass_dl, ps.n_dslots_pass);
+    }
+  }
+
+  // ---- upload -------------------------------------------------------------
+  std::vector<char> blob;
+  size_t off = 0;
+  hq::DevPlan dv{};
+  const hq::DOp* r_ops;
+  const int32_t *r_sptr, *r_svar, *r_meas, *r_pptr, *r_pq, *r_ps0, *r_plen, *r_tp, *r_vm, *r_vd, *r_vt;
+  const int32_t *r_pslots, *r_pdl, *r_ploc, *r_poff;
+  const double *r_sconst, *r_scoef, *r_vf;
+  std::vector<int32_t> sptr(d->slot_ptr, d->slot_ptr + (d->n_slots ? d->n_slots + 1 : 0));
+  const int nnz = d->n_slots ? d->slot_ptr[d->n_slots] : 0;
+  std::vector<int32_t> meas(d->measured, d->measured + d->n_measured);
+  if (meas.empty())
+    for (int qb = 0; qb < n; ++qb) meas.push_back(qb);
+  put(blob, off, pl->dops.data(), pl->dops.size(), r_ops);
+  put(blob, off, d->slot_const, (size_t)d->n_slots, r_sconst);
+  put(blob, off, sptr.data(), sptr.size(), r_sptr);
+  put(blob, off, d->slot_var, (size_t)nnz, r_svar);
+  put(blob, off, d->slot_coef, (size_t)nnz, r_scoef);
+  put(blob, off, meas.data(), meas.size(), r_meas);
+  std::vector<int32_t> pptr(d->prep_ptr, d->prep_ptr + (d->n_preps ? d->n_preps + 1 : 0));
+  const int npq = d->n_preps ? d->prep_ptr[d->n_preps] : 0;
+  put(blob, off, pptr.data(), pptr.size(), r_pptr);
+  put(blob, off, d->prep_qubits, (size_t)npq, r_pq);
+  put(blob, off, d->prep_slot0, (size_t)d->n_preps, r_ps0);
+  put(blob, off, d->prep_len, (size_t)d->n_preps, r_plen);
+  put(blob, off, prep_off.data(), prep_off.size(), r_poff);
+  put(blob, off, tp_var.data(), tp_var.size(), r_tp);
+  put(blob, off, var_mode.data(), var_mode.size(), r_vm);
+  put(blob, off, var_dsl.data(), var_dsl.size(), r_vd);
+  put(blob, off, var_tp.data(), var_tp.size(), r_vt);
+  put(blob, off, var_factor.data(), var_factor.size(), r_vf);
+  put(blob, off, pass_slots.data(), pass_slots.size(), r_pslots);
+  put(blob, off, pass_dlist.data(), pass_dlist.size(), r_pdl);
+  put(blob, off, pass_local.data(), pass_local.size(), r_ploc);
+  blob.resize(align_up(std::max<size_t>(blob.size(), 16)));
+  cudaError_t ce = cudaMalloc(&pl->dmem, blob.size());
+  if (ce != cudaSuccess) {
+    delete pl;
+    return fail(ce == cudaErrorMemoryAllocation ? HQ_E_OOM : HQ_E_CUDA,
+                std::string("plan upload: ") + cudaGetErrorString(ce));
+  }
+  ce = cudaMemcpy(pl->dmem, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+  if (ce != cudaSuccess) {
+    cudaFree(pl->dmem);
+    delete pl;
+    return fail(HQ_E_CUDA, std::string("plan upload: ") + cudaGetErrorString(ce));
+  }
+  char* base = static_cast<char*>(pl->dmem);
+  dv.n_qubits = n;
+  dv.n_slots = d->n_slots;
+  dv.n_inputs = d->n_inputs;
+  dv.n_params = d->n_params;
+  dv.n_vars = nvars;
+  dv.n_measured = (int32_t)meas.size();
+  dv.n_preps = d->n_preps;
+  dv.n_tp = pl->n_tp;
+  dv.n_adj = pl->n_adj;
+  dv.shift = d->shift;
+  dv.grad_scale = d->grad_scale;
+  dv.slot_const = rebase(r_sconst, base);
+  dv.slot_ptr = rebase(r_sptr, base);
+  dv.slot_var = rebase(r_svar, base);
+  dv.slot_coef = rebase(r_scoef, base);
+  dv.measured = rebase(r_meas, base);
+  dv.prep_ptr = rebase(r_pptr, base);
+  dv.prep_qubits = rebase(r_pq, base);
+  dv.prep_slot0 = rebase(r_ps0, base);
+  dv.prep_len = rebase(r_plen, base);
+  dv.tp_var = rebase(r_tp, base);
+  dv.var_mode = rebase(r_vm, base);
+  dv.var_dsl = rebase(r_vd, base);
+  dv.var_tp = rebase(r_vt, base);
+  dv.var_factor = rebase(r_vf, base);
+  pl->dev = dv;
+  pl->d_ops = rebase(r_ops, base);
+  pl->d_pass_slots = rebase(r_pslots, base);
+  pl->d_pass_dlist = rebase(r_pdl, base);
+  pl->d_pass_local = rebase(r_ploc, base);
+  pl->d_prep_off = rebase(r_poff, base);
+
+  std::ostringstream os;
+  os << "n=" << n << " " << (d->precision == HQ_C64 ? "c64" : "c128") << " gates=" << gates.size()
+     << " slots=" << d->n_slots << " preps=" << d->n_preps << " adjoint_slots=" << pl->n_adj
+     << " twopoint_vars=" << pl->n_tp;
+  if (pl->onchip) {
+    os << " path=onchip smem=" << hq::onchip_smem_bytes(pl);
+  } else {
+    os << " path=stream tile_bits=" << pl->tile_bits << " passes=" << pl->passes.size() << " [";
+    for (size_t i = 0; i < pl->passes.size(); ++i) os << (i ? "," : "") << pl->passes[i].n_dops;
+    os << "]";
+  }
+  pl->description = os.str();
+  *out = pl;
+  return HQ_OK;
+}
+
+extern "C" void hq_plan_destroy(hq_plan pl) {
+  if (!pl) return;
+  if (pl->dmem) cudaFree(pl->dmem);
+  delete pl;
+}
+
+extern "C" const char* hq_plan_describe(hq_plan pl) { return pl ? pl->description.c_str() : ""; }
+
+extern "C" size_t hq_workspace_bytes(hq_plan pl, int64_t batch, int32_t flags) {
+  if (!pl || batch < 0) return 0;
+  return layout_for(pl, batch, flags).total;
+}
+
+static hq_status run(hq_plan pl, const double* x, int64_t ldx, const double* theta, int64_t batch,
+                     int32_t flags, double* out, double* jac, double* state, const double* init,
+                     int64_t init_rows, void* ws, size_t ws_bytes, void* stream) {
+  if (!pl) return fail(HQ_E_CONFIG, "null plan");
+  if (batch < 0) return fail(HQ_E_DIMENSION, "negative batch");
+  if (batch == 0) return HQ_OK;
+  if (pl->n_inputs > 0 && (!x || ldx < pl->n_inputs))
+    return fail(HQ_E_DIMENSION, "input rows narrower than the circuit's inputs");
+  if (pl->n_params > 0 && !theta) return fail(HQ_E_DIMENSION, "missing parameters");
+  if (init && pl->has_preps) return fail(HQ_E_CIRCUIT, "initial state and state loads are exclusive");
+  const Layout L = layout_for(pl, batch, flags);
+  if (ws_bytes < L.total || (!ws && L.total > 256)) return fail(HQ_E_CONFIG, "workspace too small");
+  char* w = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+  hq::LaunchIn in;
+  in.x = x;
+  in.ldx = ldx;
+  in.theta = theta;
+  in.B = batch;
+  in.V = L.V;
+  in.out = out;
+  in.jac = (flags & HQ_WANT_JAC) ? jac : nullptr;
+  in.tp = reinterpret_cast<double*>(w + L.tp);
+  in.dpart = reinterpret_cast<double*>(w + L.dpart);
+  in.n_parts = L.n_parts;
+  in.want_adj = (flags & HQ_WANT_JAC) ? 1 : 0;
+  in.state = state;
+  in.init = init;
+  in.init_rows = init_rows;
+  in.sws = L.sws;
+  if (!pl->onchip) {
+    in.sws.psi = w + L.psi;
+    in.sws.lam = L.lam ? w + L.lam : nullptr;
+    in.sws.rpart = reinterpret_cast<double*>(w + L.rpart);
+  }
+  cudaError_t e = hq::launch_forward(pl, in, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(HQ_E_CUDA, std::string("forward launch: ") + cudaGetErrorString(e));
+  return HQ_OK;
+}
+
+extern "C" hq_status hq_forward(hq_plan pl, const double* x, int64_t ldx, const double* theta,
+                                int64_t batch, int32_t flags, double* out, double* jac, void* ws,
+                                size_t ws_bytes, void* stream) {
+  if (!out && batch > 0) return fail(HQ_E_CONFIG, "null output");
+  if ((flags & HQ_WANT_JAC) && !jac && batch > 0) return fail(HQ_E_CONFIG, "null jacobian output");
+  return run(pl, x, ldx, theta, batch, flags, out, jac, nullptr, nullptr, 0, ws, ws_bytes, stream);
+}
+
+extern "C" hq_status hq_state(hq_plan pl, const double* x, int64_t ldx, const double* theta,
+                              int64_t batch, const double* init, int64_t init_rows, double* state,
+                              void* ws, size_t ws_bytes, void* stream) {
+  if (!state && batch > 0) return fail(HQ_E_CONFIG, "null state output");
+  if (init && init_rows != 1 && init_rows != batch) return fail(HQ_E_DIMENSION, "init rows must be 1 or batch");
+  // the readout still runs; route it into the workspace's scratch row
+  const Layout L = layout_for(pl, batch, 0);
+  if (!pl || ws_bytes < L.total) return fail(HQ_E_CONFIG, "workspace too small");
+  char* w = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+  double* out = reinterpret_cast<double*>(w + L.scratch);
+  return run(pl, x, ldx, theta, batch, 0, out, nullptr, state, init, init_rows, ws, ws_bytes, stream);
+}
+
+extern "C" hq_status hq_vjp(hq_plan pl, const double* jac, const double* upstream, int64_t batch,
+                            double* grad_x, double* grad_theta, void* stream) {
+  if (!pl) return fail(HQ_E_CONFIG, "null plan");
+  if (batch <= 0) return HQ_OK;
+  if (!jac || !upstream) return fail(HQ_E_CONFIG, "null jacobian / upstream");
+  cudaError_t e = hq::launch_vjp(pl, jac, upstream, batch, grad_x, grad_theta, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(HQ_E_CUDA, std::string("vjp launch: ") + cudaGetErrorString(e));
+  return HQ_OK;
+}

@@ -1,0 +1,104 @@
+// Internal structures shared by the host planner (hq_api.cpp) and the sm_100a
+// kernels (hq_kernels.cu).  Nothing here crosses the C ABI.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/hq.h"
+
+namespace hq {
+
+// One op as a kernel sees it.  Qubit operands are TILE bit positions when >= 0;
+// a negative value ~g (= -1-g) names a global qubit g that is not resident in
+// the tile, whose bit is constant over the tile (only legal as a control or as
+// the qubit of a diagonal gate — the planner guarantees it).
+struct DOp {
+  int32_t kind;
+  int32_t a;      // target for 1q kinds; control for CNOT/CZ/CR; first qubit of SWAP
+  int32_t b;      // target of CNOT/CZ/CR, second qubit of SWAP, unused otherwise
+  int32_t slot;   // angle slot or -1
+  int32_t dslot;  // index among the adjoint variables whose derivative this op yields, or -1
+  int32_t pad[3];
+};
+
+// Device-resident, immutable plan constants (all pointers are device memory).
+struct DevPlan {
+  int32_t n_qubits;
+  int32_t n_slots;
+  int32_t n_inputs, n_params, n_vars;
+  int32_t n_measured;
+  int32_t n_preps;
+  int32_t n_tp;     // two-point variables
+  int32_t n_adj;    // derivative slots (distinct angle slots the adjoint sweep differentiates)
+  double shift, grad_scale;
+  const double* slot_const;
+  const int32_t* slot_ptr;
+  const int32_t* slot_var;
+  const double* slot_coef;
+  const int32_t* measured;
+  const int32_t* prep_ptr;
+  const int32_t* prep_qubits;
+  const int32_t* prep_slot0;
+  const int32_t* prep_len;
+  const int32_t* tp_var;       // [n_tp] variable ids
+  const int32_t* var_mode;     // [n_vars] HQ_GRAD_*
+  const int32_t* var_dsl;      // [n_vars] ADJOINT: derivative slot
+  const int32_t* var_tp;       // [n_vars] TWOPOINT: index into tp_var
+  const double* var_factor;    // [n_vars] ADJOINT: 2*grad_scale*sin(coef*shift)
+};
+
+// One HBM pass of the streaming path: tile = 2^q amplitudes gathered from the
+// global qubits local[0..q).
+struct Pass {
+  std::vector<int32_t> local;      // tile bit i <-> global qubit local[i]
+  std::vector<int32_t> op_ids;     // tape ops applied in this pass, in order
+  std::vector<int32_t> slots;      // distinct angle slots those ops read
+  int32_t first_dop = 0;           // offset of this pass's DOps in the device array
+  int32_t n_dops = 0;
+  int32_t first_slotlist = 0;      // offset into the device slot-list array
+  int32_t n_dslots_pass = 0;       // ops in this pass that yield a derivative
+  int32_t first_dlist = 0;         // offset into device list of dslot ids of this pass
+};
+
+struct PassDev {
+  int32_t q;                 // tile bits
+  int32_t n_ops;
+  const DOp* ops;
+  int32_t n_slots;           // slots used by this pass (trig cached per CTA)
+  const int32_t* slots;
+  int32_t n_dl;              // derivative-bearing ops in this pass
+  const int32_t* dlist;      // their dslot ids, in pass op order
+  const int32_t* local;      // [q] global qubit of each tile bit
+  const int32_t* nonlocal;   // [n-q] global qubit of each tile-id bit
+  int32_t first, last;       // first pass (initialise state) / last pass (readout, λ init)
+};
+
+}  // namespace hq
+
+struct hq_plan_s {
+  int32_t n_qubits = 0;
+  int32_t precision = HQ_C128;
+  int32_t n_inputs = 0, n_params = 0;
+  bool onchip = true;
+  int32_t tile_bits = 0;                  // streaming path
+  int32_t n_adj = 0, n_tp = 0;
+  std::vector<hq::DOp> dops;              // on-chip: the whole tape; streaming: per pass
+  std::vector<hq::Pass> passes;
+  std::vector<int32_t> host_var_mode;
+  int32_t n_slots = 0;
+  int32_t max_pass_slots = 0;
+  int32_t max_pass_dl = 0;
+  bool has_preps = false;
+  int32_t prep_total = 0;                 // Σ prep_len
+  std::string description;
+  // device memory (one allocation, carved)
+  void* dmem = nullptr;
+  hq::DevPlan dev{};
+  const hq::DOp* d_ops = nullptr;
+  const int32_t* d_pass_slots = nullptr;
+  const int32_t* d_pass_dlist = nullptr;
+  const int32_t* d_pass_local = nullptr;  // [n_passes][n] (local then nonlocal)
+  const int32_t* d_prep_off = nullptr;    // [n_preps]
+};

@@ -1,0 +1,366 @@
+"""Execution engine: tape -> ``hq_plan`` -> sm_100a kernels.
+
+``Plan`` owns one C-ABI plan handle (``include/hq.h``) and runs it on torch
+CUDA tensors (PyTorch is used for device memory and the current stream only).
+``run_batch`` is what ``QuantumLayer.forward`` calls: it traces the builder
+(``tracer.py``), picks or builds the plan, and returns per-sample expectations
+and, when gradients are wanted, the per-sample jacobian rows the reference's
+``df_x`` / ``df_p`` closures would produce at upstream 1 (``qnn.py:136-153``).
+
+Builders that are not provably affine / batch-invariant run through
+``run_per_sample``: the builder is called per sample and per shifted value,
+exactly like the reference (``qnn.py:35-52``), and the resulting circuits are
+simulated in batches grouped by structure — still on the GPU, with every angle
+carried as a per-circuit input.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from collections import OrderedDict
+
+import numpy as np
+
+from . import _native as nat
+from . import tracer as tr
+from .errors import CircuitError, ConfigError, EncodingError, NativeError
+
+_PREC = {"c64": nat.HQ_C64, "c128": nat.HQ_C128, "complex64": nat.HQ_C64,
+         "complex128": nat.HQ_C128}
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise NativeError("no CUDA device: this package has no CPU execution path")
+    return torch
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _arr(a, dt):
+    a = np.ascontiguousarray(np.asarray(a, dtype=dt))
+    return a, (a.ctypes.data if a.size else None)
+
+
+class Plan:
+    """One immutable device plan for a tape + gradient spec + precision."""
+
+    def __init__(self, tape: tr.Tape, n_inputs: int, n_params: int, precision: str = "c128",
+                 grad=None, shift: float = math.pi / 2, grad_scale: float = 0.5):
+        if precision not in _PREC:
+            raise ConfigError(f"precision must be c64 or c128, got {precision!r}")
+        L = nat.lib()
+        torch = _torch()
+        self.device = torch.cuda.current_device()
+        self.n_qubits = tape.n_qubits
+        self.n_inputs, self.n_params = int(n_inputs), int(n_params)
+        self.n_vars = self.n_inputs + self.n_params
+        self.precision = precision
+        ops = (nat.HqOp * max(1, len(tape.ops)))()
+        for i, (kind, targets, slot) in enumerate(tape.ops):
+            if kind == "STATEPREP":
+                ops[i] = nat.HqOp(11, slot, -1, -1)
+            elif len(targets) == 2:
+                ops[i] = nat.HqOp(nat.KIND_CODE[kind], targets[0], targets[1], slot)
+            else:
+                ops[i] = nat.HqOp(nat.KIND_CODE[kind], targets[0], -1, slot)
+        nnz_ptr = [0]
+        var, coef = [], []
+        for terms in tape.slot_terms:
+            for v in sorted(terms):
+                var.append(v)
+                coef.append(terms[v])
+            nnz_ptr.append(len(var))
+        keep = []
+
+        def a(x, dt):
+            arr, p = _arr(x, dt)
+            keep.append(arr)
+            return p
+
+        d = nat.HqPlanDesc()
+        d.n_qubits = tape.n_qubits
+        d.precision = _PREC[precision]
+        d.n_ops = len(tape.ops)
+        d.ops = ctypes.cast(ops, ctypes.c_void_p)
+        d.n_slots = len(tape.slot_const)
+        d.slot_const = a(tape.slot_const, np.float64)
+        d.slot_ptr = a(nnz_ptr, np.int32)
+        d.slot_var = a(var, np.int32)
+        d.slot_coef = a(coef, np.float64)
+        d.n_inputs, d.n_params = self.n_inputs, self.n_params
+        d.n_measured = len(tape.measured)
+        d.measured = a(tape.measured, np.int32)
+        d.n_preps = len(tape.preps)
+        pq, pp, ps0, pl = [], [0], [], []
+        for qubits, first, count in tape.preps:
+            pq.extend(qubits)
+            pp.append(len(pq))
+            ps0.append(first)
+            pl.append(count)
+        d.prep_ptr = a(pp, np.int32)
+        d.prep_qubits = a(pq, np.int32)
+        d.prep_slot0 = a(ps0, np.int32)
+        d.prep_len = a(pl, np.int32)
+        if grad is not None:
+            mode, vslot, factor = grad
+            d.grad_mode = a(mode, np.int32)
+            d.grad_slot = a(vslot, np.int32)
+            d.grad_factor = a(factor, np.float64)
+            self.grad_mode = np.asarray(mode)
+        else:
+            self.grad_mode = np.zeros(self.n_vars, np.int32)
+        d.shift, d.grad_scale = float(shift), float(grad_scale)
+        h = ctypes.c_void_p()
+        nat.check(L.hq_plan_create(ctypes.byref(d), ctypes.byref(h)), "plan")
+        self._h = h
+        self._lib = L
+        self.description = L.hq_plan_describe(h).decode()
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self._lib.hq_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def _ws(self, B, flags):
+        torch = _torch()
+        n = int(self._lib.hq_workspace_bytes(self._h, int(B), int(flags)))
+        return torch.empty(max(n, 256), dtype=torch.uint8, device=f"cuda:{self.device}"), n
+
+    def forward(self, x, theta, want_jac: bool):
+        """x: cuda f64 [B, ldx]; theta: cuda f64 [P] -> (out [B], jac [B, nv] | None)."""
+        torch = _torch()
+        B = int(x.shape[0])
+        dev = f"cuda:{self.device}"
+        out = torch.empty(B, dtype=torch.float64, device=dev)
+        jac = torch.empty((B, self.n_vars), dtype=torch.float64, device=dev) if want_jac else None
+        flags = nat.HQ_WANT_JAC if want_jac else 0
+        ws, nbytes = self._ws(B, flags)
+        st = torch.cuda.current_stream().cuda_stream
+        nat.check(self._lib.hq_forward(self._h, _ptr(x), int(x.stride(0)) if x.dim() == 2 else 0,
+                                       _ptr(theta), B, flags, _ptr(out), _ptr(jac), _ptr(ws),
+                                       ws.numel(), st), "forward")
+        return out, jac
+
+    def vjp(self, jac, upstream, want_x=True, want_theta=True):
+        torch = _torch()
+        B = int(jac.shape[0])
+        dev = jac.device
+        gx = torch.empty((B, self.n_inputs), dtype=torch.float64, device=dev) if want_x else None
+        gt = torch.empty(self.n_params, dtype=torch.float64, device=dev) if want_theta else None
+        st = torch.cuda.current_stream().cuda_stream
+        nat.check(self._lib.hq_vjp(self._h, _ptr(jac), _ptr(upstream), B, _ptr(gx), _ptr(gt), st),
+                  "vjp")
+        return gx, gt
+
+    def state(self, x, theta, init=None):
+        torch = _torch()
+        B = int(x.shape[0]) if x is not None else 1
+        dev = f"cuda:{self.device}"
+        st_out = torch.empty((B, 1 << self.n_qubits, 2), dtype=torch.float64, device=dev)
+        ws, _ = self._ws(B, 0)
+        rows = 0 if init is None else int(init.shape[0])
+        st = torch.cuda.current_stream().cuda_stream
+        nat.check(self._lib.hq_state(self._h, _ptr(x), int(x.stride(0)) if x is not None else 0,
+                                     _ptr(theta), B, _ptr(init), rows, _ptr(st_out), _ptr(ws),
+                                     ws.numel(), st), "state")
+        return st_out
+
+
+# ------------------------------------------------------------------------------
+def tape_key(tape: tr.Tape):
+    return (tape.structure_key(), tuple(tape.slot_const),
+            tuple(tuple(sorted(t.items())) for t in tape.slot_terms))
+
+
+class PlanCache:
+    """Small LRU of plans keyed by tape + gradient spec + precision + device."""
+
+    def __init__(self, size: int = 8):
+        self.size = size
+        self._d: OrderedDict = OrderedDict()
+
+    def get(self, tape, n_inputs, n_params, precision, grad, shift, grad_scale):
+        torch = _torch()
+        gkey = None if grad is None else (tuple(grad[0]), tuple(grad[1]), tuple(grad[2]))
+        key = (tape_key(tape), n_inputs, n_params, precision, gkey, shift, grad_scale,
+               torch.cuda.current_device())
+        plan = self._d.get(key)
+        if plan is None:
+            plan = Plan(tape, n_inputs, n_params, precision, grad, shift, grad_scale)
+            self._d[key] = plan
+            while len(self._d) > self.size:
+                self._d.popitem(last=False)
+        else:
+            self._d.move_to_end(key)
+        return plan
+
+
+_global_cache = PlanCache(32)
+
+
+def _check_preps(tape: tr.Tape, x: np.ndarray, theta: np.ndarray):
+    """Host check of the reference's per-sample embedding errors (templates.py:71-75)."""
+    for _, first, count in tape.preps:
+        vals = np.zeros((x.shape[0], count))
+        for k in range(count):
+            s = first + k
+            col = np.full(x.shape[0], tape.slot_const[s])
+            for v, c in tape.slot_terms[s].items():
+                col = col + c * (x[:, v] if v < x.shape[1] else theta[v - x.shape[1]])
+            vals[:, k] = col
+        if not np.all(np.isfinite(vals)):
+            raise EncodingError("amplitude embedding needs a finite nonzero vector")
+        if np.any(np.linalg.norm(vals, axis=1) == 0.0):
+            raise EncodingError("cannot embed the zero vector")
+
+
+def run_batch(builder, xd: np.ndarray, pd: np.ndarray, want_x: bool, want_p: bool,
+              precision: str = "c128", shift: float = math.pi / 2, grad_scale: float = 0.5,
+              cache: PlanCache | None = None):
+    """Host-boundary entry: numpy in, numpy out.
+
+    Returns ``(out [B], jac [B, d+P] | None, info)``.
+    """
+    torch = _torch()
+    B, d = xd.shape
+    P = pd.shape[0]
+    tape, ok = tr.trace(builder, xd, pd)
+    if not ok:
+        return run_per_sample(builder, xd, pd, want_x, want_p, precision, shift, grad_scale)
+    if tape.preps:
+        _check_preps(tape, xd, pd)
+    wanted = [want_x] * d + [want_p] * P
+    grad = tr.classify(tape, d + P, wanted, shift, grad_scale) if (want_x or want_p) else None
+    cache = cache or _global_cache
+    try:
+        plan = cache.get(tape, d, P, precision, grad, shift, grad_scale)
+    except CircuitError as exc:
+        if "no native lowering" in str(exc):
+            return run_per_sample(builder, xd, pd, want_x, want_p, precision, shift, grad_scale)
+        raise
+    dev = f"cuda:{plan.device}"
+    x_t = torch.from_numpy(np.ascontiguousarray(xd)).to(dev)
+    p_t = torch.from_numpy(np.ascontiguousarray(pd)).to(dev)
+    out, jac = plan.forward(x_t, p_t, grad is not None)
+    out_h = out.cpu().numpy()
+    return out_h, jac, {"plan": plan, "path": "traced"}
+
+
+# ------------------------------------------------------------------------------
+def _circuit_rows(circuits):
+    """Group plain-float circuits by structure -> {key: (tape, [(idx, angles)])}."""
+    groups = {}
+    for idx, c in enumerate(circuits):
+        tr.check_circuit(c)
+        measured = [int(q) for q in c.measured_qubits] or list(range(c.n_qubits))
+        ops, angles = [], []
+        for op in c.ops:
+            if op.kind == "STATEPREP":
+                raise CircuitError("state loads only exist in traced builders")
+            if op.angle is None:
+                ops.append((op.kind, tuple(op.targets), -1))
+            else:
+                ops.append((op.kind, tuple(op.targets), len(angles)))
+                angles.append(float(op.angle))
+        key = (int(c.n_qubits), tuple(measured), tuple(ops))
+        if key not in groups:
+            tape = tr.Tape(int(c.n_qubits), measured, ops, [])
+            tape.slot_const = [0.0] * len(angles)
+            tape.slot_terms = [{s: 1.0} for s in range(len(angles))]
+            groups[key] = (tape, [])
+        groups[key][1].append((idx, angles))
+    return groups
+
+
+def evaluate_circuits(circuits, precision: str = "c128") -> np.ndarray:
+    """EXACT_PROB readout of each circuit (angles carried as per-circuit inputs)."""
+    torch = _torch()
+    out = np.empty(len(circuits), dtype=np.float64)
+    for tape, rows in _circuit_rows(circuits).values():
+        A = len(tape.slot_const)
+        plan = _global_cache.get(tape, A, 0, precision, None, math.pi / 2, 0.5)
+        x = np.array([r[1] for r in rows], dtype=np.float64).reshape(len(rows), A)
+        dev = f"cuda:{plan.device}"
+        xt = torch.from_numpy(x).to(dev) if A else torch.zeros((len(rows), 1), dtype=torch.float64, device=dev)
+        pt = torch.zeros(1, dtype=torch.float64, device=dev)
+        e, _ = plan.forward(xt, pt, False)
+        out[[r[0] for r in rows]] = e.cpu().numpy()
+    return out
+
+
+def final_states(circuits, precision: str = "c128", init=None) -> list:
+    """Final amplitudes (complex128 numpy) of each circuit."""
+    torch = _torch()
+    res = [None] * len(circuits)
+    for tape, rows in _circuit_rows(circuits).values():
+        A = len(tape.slot_const)
+        plan = _global_cache.get(tape, A, 0, precision, None, math.pi / 2, 0.5)
+        dev = f"cuda:{plan.device}"
+        x = np.array([r[1] for r in rows], dtype=np.float64).reshape(len(rows), A)
+        xt = torch.from_numpy(x).to(dev) if A else torch.zeros((len(rows), 1), dtype=torch.float64, device=dev)
+        pt = torch.zeros(1, dtype=torch.float64, device=dev)
+        it = None
+        if init is not None:
+            z = np.ascontiguousarray(np.asarray(init, np.complex128).reshape(1, -1))
+            it = torch.from_numpy(z.view(np.float64).reshape(1, -1, 2)).to(dev)
+        s = plan.state(xt, pt, it).cpu().numpy()
+        for k, (idx, _) in enumerate(rows):
+            res[idx] = s[k, :, 0] + 1j * s[k, :, 1]
+    return res
+
+
+def simulate_circuit(circuit, init=None, precision: str = "c128") -> np.ndarray:
+    return final_states([circuit], precision, init)[0]
+
+
+def run_per_sample(builder, xd, pd, want_x, want_p, precision, shift, grad_scale):
+    """The reference's own evaluation pattern, with the simulations batched on GPU.
+
+    One builder call per sample and per shifted value (qnn.py:35-52,131-153);
+    all resulting circuits are simulated together.
+    """
+    from .qnn import build_circuit
+    B, d = xd.shape
+    P = pd.shape[0]
+    circuits, index = [], []
+    for i in range(B):
+        circuits.append(build_circuit(builder, xd[i], pd))
+        index.append(("out", i, -1, 0))
+    for i in range(B):
+        if want_x:
+            for j in range(d):
+                for sgn in (1, -1):
+                    v = xd[i].copy()
+                    v[j] = xd[i, j] + sgn * shift
+                    circuits.append(build_circuit(builder, v, pd))
+                    index.append(("x", i, j, sgn))
+        if want_p:
+            for j in range(P):
+                for sgn in (1, -1):
+                    v = pd.copy()
+                    v[j] = pd[j] + sgn * shift
+                    circuits.append(build_circuit(builder, xd[i], v))
+                    index.append(("p", i, j, sgn))
+    e = evaluate_circuits(circuits, precision)
+    out = e[:B].copy()
+    jac = None
+    if want_x or want_p:
+        jac = np.zeros((B, d + P))
+        k = B
+        while k < len(index):
+            kind, i, j, _ = index[k]
+            col = j if kind == "x" else d + j
+            jac[i, col] = (e[k] - e[k + 1]) * grad_scale
+            k += 2
+        torch = _torch()
+        jac = torch.from_numpy(jac).to(f"cuda:{torch.cuda.current_device()}")
+    return out, jac, {"plan": None, "path": "per_sample"}

@@ -1,0 +1,176 @@
+"""Generate golden vectors by running the REFERENCE implementation (hyqnet).
+
+Run in the build container (the reference is not present on the GPU box):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+It imports ``hyqnet`` from /root/reference/pkg/src, drives it through its own
+public API (``QuantumLayer``, ``backward``, ``simulate``, ``QAELayer``) with the
+same builders the product and oracle use (``workloads.make_builder``), and
+writes ``tests/golden/*.npz``.  Nothing else in the repo reads /root/reference.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+import hyqnet.qsim as rq  # noqa: E402
+import hyqnet.templates as rt  # noqa: E402
+from hyqnet.qnn import QAELayer, QuantumLayer  # noqa: E402
+from hyqnet.tensor import Tensor, backward, tsum  # noqa: E402
+
+from paper_2301_03251_b200 import workloads as wl  # noqa: E402
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, f"{name}.npz")
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({', '.join(arrays)})")
+
+
+def layer_case(name, cfg, batch, want_x, seed_g=7):
+    builder = wl.make_builder(cfg, rq, rt)
+    x = wl.inputs_for(cfg, batch)
+    theta = wl.params_for(cfg)
+    layer = QuantumLayer(builder, n_params=theta.size, param_init=theta)
+    xt = Tensor(x, requires_grad=want_x, dtype=np.float64)
+    g = np.random.default_rng(seed_g).uniform(0.5, 1.5, (batch, 1))
+    t0 = time.perf_counter()
+    out = layer(xt)
+    backward(tsum(out * Tensor(g, dtype=np.float64)))
+    dt = time.perf_counter() - t0
+    save(name, x=x, theta=theta, upstream=g[:, 0], out=out.numpy()[:, 0],
+         grad_x=xt.grad if want_x else np.zeros_like(x), grad_p=layer.params.grad,
+         seconds=np.array(dt))
+
+
+def cfg4_case():
+    builder = wl.make_builder("cfg4", rq, rt)
+    x = wl.inputs_for("cfg4", 2)
+    theta = wl.params_for("cfg4")
+    layer = QuantumLayer(builder, n_params=theta.size, param_init=theta)
+    out = layer(Tensor(x, dtype=np.float64)).numpy()[:, 0]
+    idx = np.array([0, 1, 57, 200, 311, 399])
+    s = layer.shift
+    jac = []
+    for j in idx:
+        tp = theta.copy(); tp[j] += s
+        tm = theta.copy(); tm[j] -= s
+        jac.append((layer._run(x[0], tp) - layer._run(x[0], tm)) * layer.grad_scale)
+    save("cfg4", x=x, theta=theta, out=out, jac_idx=idx, jac0=np.array(jac))
+
+
+def random_circuits_case():
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from conftest import random_circuit
+    rng = np.random.default_rng(1234)
+    kinds, q0, q1, ang, starts, nq, states, exps = [], [], [], [], [0], [], [], []
+    for k in range(40):
+        n = int(rng.integers(1, 6))
+        c = random_circuit(rng, n, int(rng.integers(0, 24)))
+        for op in c.ops:
+            kinds.append(op.kind)
+            q0.append(op.targets[0])
+            q1.append(op.targets[1] if len(op.targets) > 1 else -1)
+            ang.append(np.nan if op.angle is None else op.angle)
+        starts.append(len(kinds))
+        nq.append(n)
+        st = rq.simulate(c).amplitudes
+        states.append(np.pad(st, (0, 32 - st.size)))
+        probs = rq.probabilities(rq.simulate(c), list(range(n)))
+        exps.append(float(np.arange(probs.size) @ probs))
+    save("random_circuits", kinds=np.array(kinds), q0=np.array(q0), q1=np.array(q1),
+         angle=np.array(ang), starts=np.array(starts), n_qubits=np.array(nq),
+         states=np.array(states), expectation=np.array(exps))
+
+
+def reupload_case():
+    # not shift-exact: input used twice, shared parameter, scaled parameter
+    def builder(inputs, params):
+        c = rq.Circuit(3)
+        c.ry(0, inputs[0])
+        c.rx(1, inputs[1])
+        c.cnot(0, 1)
+        c.ry(0, inputs[0])            # re-upload
+        c.rz(1, params[0])
+        c.rx(2, params[0])            # shared
+        c.ry(2, 2.0 * params[1])      # scaled
+        c.cr(1, 2, params[2] - 0.3)   # CR, affine
+        c.h(2)
+        c.cz(0, 2)
+        c.swap(0, 2)
+        c.ry(1, 0.5 * params[3] + inputs[1])
+        c.measure(0, 2)
+        return c
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-np.pi, np.pi, (5, 2))
+    theta = rng.uniform(0, 2 * np.pi, 4)
+    layer = QuantumLayer(builder, n_params=4, param_init=theta)
+    xt = Tensor(x, requires_grad=True, dtype=np.float64)
+    g = rng.uniform(0.5, 1.5, (5, 1))
+    out = layer(xt)
+    backward(tsum(out * Tensor(g, dtype=np.float64)))
+    save("reupload", x=x, theta=theta, upstream=g[:, 0], out=out.numpy()[:, 0], grad_x=xt.grad,
+         grad_p=layer.params.grad)
+
+
+def qae_cases():
+    layer = QAELayer(1, 4, machine_type="exact_prob", param_init=np.linspace(0.1, 1.1, 18))
+    x = np.array([[0.6, 0.8, 0.0, 0.0]])
+    out = layer(Tensor(x, dtype=np.float64))
+    backward(tsum(out))
+    save("qae_1_4", x=x, theta=np.linspace(0.1, 1.1, 18), out=out.numpy()[:, 0],
+         grad_p=layer.params.grad)
+    rng = np.random.default_rng(1234)
+    theta = rng.uniform(0, 2 * np.pi, 60)
+    layer = QAELayer(2, 7, machine_type="exact_prob", param_init=theta)
+    x = rng.standard_normal((3, 16))
+    g = rng.uniform(0.5, 1.5, (3, 1))
+    out = layer(Tensor(x, dtype=np.float64))
+    backward(tsum(out * Tensor(g, dtype=np.float64)))
+    save("qae_2_7", x=x, theta=theta, upstream=g[:, 0], out=out.numpy()[:, 0],
+         grad_p=layer.params.grad)
+
+
+def embedding_case():
+    rng = np.random.default_rng(5)
+    vecs = [np.array([0.2, -0.4, 0.4, -0.8]), np.array([3, 1, -4, 1, -5, 9, -2, 6], float),
+            np.array([0.6, 0.8]), rng.standard_normal(16), rng.standard_normal(5),
+            np.array([0.0, 0.0, 1.0, 0.0])]
+    out = []
+    for v in vecs:
+        n = max(1, int(np.ceil(np.log2(v.size))))
+        c = rq.Circuit(n + 1)
+        c.extend(rt.amplitude_embedding(v, qubits=list(range(1, n + 1))))
+        out.append(np.pad(rq.simulate(c).amplitudes, (0, 32 - 2 ** (n + 1))))
+    save("embedding", vecs=np.array([np.pad(v, (0, 16 - v.size)) for v in vecs]),
+         sizes=np.array([v.size for v in vecs]), states=np.array(out))
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "cfg4", "random", "reupload", "qae", "embed"]
+    if "cfg1" in which:
+        layer_case("cfg1", "cfg1", 16, True)
+    if "cfg2" in which:
+        layer_case("cfg2", "cfg2", 3, True)
+    if "cfg3" in which:
+        layer_case("cfg3", "cfg3", 2, False)
+    if "cfg4" in which:
+        cfg4_case()
+    if "random" in which:
+        random_circuits_case()
+    if "reupload" in which:
+        reupload_case()
+    if "qae" in which:
+        qae_cases()
+    if "embed" in which:
+        embedding_case()

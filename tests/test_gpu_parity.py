@@ -1,0 +1,313 @@
+"""GPU parity: the sm_100a path against golden vectors (produced by the
+reference itself) and against the CPU oracle on seeded inputs.
+
+Tolerances (north_star): complex128 1e-10 relative (absolute floor 1e-4 for
+near-zero entries); complex64 1e-5 relative on expectations/amplitudes and
+1e-5 normwise (‖Δ‖∞/‖ref‖∞) on gradient vectors.
+"""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import golden, normwise_error, relative_error
+from oracle import hq_oracle as O
+from paper_2301_03251_b200 import (Circuit, QAELayer, QuantumLayer, Tensor, backward, no_grad,
+                                   qsim, tsum, workloads as wl)
+from paper_2301_03251_b200 import templates as T
+from paper_2301_03251_b200 import engine
+
+pytestmark = pytest.mark.gpu
+
+PRECS = ["c128", "c64"]
+
+
+def check_vals(got, want, prec, grad=False):
+    if prec == "c128":
+        assert relative_error(got, want, floor=1e-4) < 1e-10
+    elif grad:
+        assert normwise_error(got, want) < 1e-5
+    else:
+        assert relative_error(got, want, floor=1e-3) < 1e-5
+
+
+def layer_run(builder, x, theta, prec, upstream=None, want_x=True):
+    layer = QuantumLayer(builder, n_params=len(theta), param_init=theta, precision=prec)
+    xt = Tensor(x, requires_grad=want_x, dtype=np.float64)
+    out = layer(xt)
+    g = np.ones((len(x), 1)) if upstream is None else np.asarray(upstream).reshape(-1, 1)
+    backward(tsum(out * Tensor(g, dtype=np.float64)))
+    return out.numpy()[:, 0], (xt.grad if want_x else None), layer.params.grad, layer
+
+
+def _golden_circuits(g):
+    out = []
+    for k in range(len(g["n_qubits"])):
+        c = Circuit(int(g["n_qubits"][k]))
+        for i in range(g["starts"][k], g["starts"][k + 1]):
+            tg = (int(g["q0"][i]),) if g["q1"][i] < 0 else (int(g["q0"][i]), int(g["q1"][i]))
+            a = None if np.isnan(g["angle"][i]) else float(g["angle"][i])
+            c.add(qsim.GateOp(str(g["kinds"][i]), tg, a))
+        c.measure(*range(c.n_qubits))
+        out.append(c)
+    return out
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_random_circuits_states(prec):
+    g = golden("random_circuits")
+    circuits = _golden_circuits(g)
+    states = engine.final_states(circuits, prec)
+    exps = engine.evaluate_circuits(circuits, prec)
+    tol = 1e-12 if prec == "c128" else 2e-6
+    for k, st in enumerate(states):
+        np.testing.assert_allclose(st, g["states"][k][:st.size], atol=tol)
+    np.testing.assert_allclose(exps, g["expectation"], atol=tol * 10)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_cfg1_golden(prec):
+    g = golden("cfg1")
+    b = wl.make_builder("cfg1", qsim, T)
+    out, gx, gp, layer = layer_run(b, g["x"], g["theta"], prec, g["upstream"])
+    assert "onchip" in layer.last_info["plan"].description
+    check_vals(out, g["out"], prec)
+    check_vals(gx, g["grad_x"], prec, grad=True)
+    check_vals(gp, g["grad_p"], prec, grad=True)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_cfg2_golden(prec):
+    g = golden("cfg2")
+    b = wl.make_builder("cfg2", qsim, T)
+    out, gx, gp, _ = layer_run(b, g["x"], g["theta"], prec, g["upstream"])
+    check_vals(out, g["out"], prec)
+    check_vals(gx, g["grad_x"], prec, grad=True)
+    check_vals(gp, g["grad_p"], prec, grad=True)
+
+
+def test_cfg3_golden_state_load_and_adjoint():
+    g = golden("cfg3")
+    b = wl.make_builder("cfg3", qsim, T)
+    out, _, gp, layer = layer_run(b, g["x"], g["theta"], "c128", g["upstream"], want_x=False)
+    assert "preps=1" in layer.last_info["plan"].description
+    check_vals(out, g["out"], "c128")
+    check_vals(gp, g["grad_p"], "c128", grad=True)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_cfg4_golden_streaming(prec):
+    g = golden("cfg4")
+    b = wl.make_builder("cfg4", qsim, T)
+    layer = QuantumLayer(b, n_params=400, param_init=g["theta"], precision=prec)
+    res, jac, info = engine.run_batch(b, g["x"], g["theta"], False, True, prec, cache=layer._plans)
+    assert "stream" in info["plan"].description
+    check_vals(res, g["out"], prec)
+    j = jac.cpu().numpy()[0, 20:][g["jac_idx"]]
+    if prec == "c128":
+        assert relative_error(j, g["jac0"], floor=1e-4) < 1e-10
+    else:
+        assert np.max(np.abs(j - g["jac0"])) < 1e-5 * max(np.max(np.abs(g["jac0"])), 1e-2)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_reupload_two_point_path(prec):
+    g = golden("reupload")
+
+    def b(inputs, params):
+        c = Circuit(3)
+        c.ry(0, inputs[0]); c.rx(1, inputs[1]); c.cnot(0, 1); c.ry(0, inputs[0])
+        c.rz(1, params[0]); c.rx(2, params[0]); c.ry(2, 2.0 * params[1])
+        c.cr(1, 2, params[2] - 0.3); c.h(2); c.cz(0, 2); c.swap(0, 2)
+        c.ry(1, 0.5 * params[3] + inputs[1]); c.measure(0, 2)
+        return c
+    out, gx, gp, layer = layer_run(b, g["x"], g["theta"], prec, g["upstream"])
+    assert "twopoint_vars=3" in layer.last_info["plan"].description  # x0, x1, θ0 enter twice
+    check_vals(out, g["out"], prec)
+    check_vals(gx, g["grad_x"], prec, grad=True)
+    check_vals(gp, g["grad_p"], prec, grad=True)
+
+
+@pytest.mark.parametrize("name,trash,total", [("qae_1_4", 1, 4), ("qae_2_7", 2, 7)])
+def test_qae_layer_golden(name, trash, total):
+    g = golden(name)
+    layer = QAELayer(trash, total, machine_type="exact_prob", param_init=g["theta"])
+    out = layer(Tensor(g["x"], dtype=np.float64))
+    up = g.get("upstream", np.ones(len(g["x"])))
+    backward(tsum(out * Tensor(up.reshape(-1, 1), dtype=np.float64)))
+    assert relative_error(out.numpy()[:, 0], g["out"], floor=1e-4) < 1e-10
+    assert relative_error(layer.params.grad, g["grad_p"], floor=1e-4) < 1e-10
+
+
+def test_embedding_states_golden():
+    g = golden("embedding")
+    for k, size in enumerate(g["sizes"]):
+        v = [float(a) for a in g["vecs"][k][:size]]
+        n = max(1, int(np.ceil(np.log2(size))))
+
+        def b(inputs, params, n=n):
+            c = Circuit(n + 1)
+            c.extend(T.amplitude_embedding(inputs, qubits=list(range(1, n + 1))))
+            return c
+        # traced path: one native state load
+        tape, ok = engine.tr.trace(b, np.array([v]), np.zeros(0))
+        assert ok and tape.preps
+        plan = engine.Plan(tape, size, 0, "c128")
+        import torch
+        st = plan.state(torch.tensor([v], dtype=torch.float64, device="cuda"),
+                        torch.zeros(1, dtype=torch.float64, device="cuda")).cpu().numpy()[0]
+        z = st[:, 0] + 1j * st[:, 1]
+        np.testing.assert_allclose(z, g["states"][k][:z.size], atol=1e-13)
+
+
+# ---------------------------------------------------------------------------
+# oracle comparisons on seeded random inputs, including the multi-pass path
+def _random_layer_builder(n, depth, seed):
+    rng = np.random.default_rng(seed)
+    kinds = ["H", "X", "Y", "Z", "RX", "RY", "RZ", "CNOT", "CZ", "CR", "SWAP"]
+    plan = []
+    for _ in range(depth):
+        k = kinds[rng.integers(len(kinds))]
+        if k in ("CNOT", "CZ", "CR", "SWAP"):
+            a, b = rng.choice(n, 2, replace=False)
+            plan.append((k, (int(a), int(b)), int(rng.integers(0, 6))))
+        else:
+            plan.append((k, (int(rng.integers(n)),), int(rng.integers(0, 6))))
+    meas = [int(q) for q in rng.choice(n, min(n, 3), replace=False)]
+
+    def builder(inputs, params, Circ=Circuit):
+        c = Circ(n)
+        for k, tg, v in plan:
+            ang = (inputs[v] if v < 2 else params[v - 2]) if k in ("RX", "RY", "RZ", "CR") else None
+            if k in ("CNOT", "CZ", "SWAP"):
+                getattr(c, k.lower())(*tg)
+            elif k == "CR":
+                c.cr(tg[0], tg[1], ang)
+            elif ang is None:
+                getattr(c, k.lower())(tg[0])
+            else:
+                getattr(c, k.lower())(tg[0], ang)
+        c.measure(*meas)
+        return c
+    return builder
+
+
+@pytest.mark.parametrize("n,tile_bits", [(5, None), (9, None), (9, 4), (14, None), (15, 6)])
+@pytest.mark.parametrize("prec", PRECS)
+def test_random_layers_vs_oracle(n, tile_bits, prec, monkeypatch):
+    if tile_bits is not None:
+        monkeypatch.setenv("HQ_FORCE_STREAM", "1")
+        monkeypatch.setenv("HQ_TILE_BITS", str(tile_bits))
+    b = _random_layer_builder(n, 60, seed=n * 7 + (tile_bits or 0))
+    rng = np.random.default_rng(n)
+    x = rng.uniform(-3, 3, (3, 2))
+    th = rng.uniform(0, 6, 4)
+    res, jac, info = engine.run_batch(b, x, th, True, True, prec, cache=engine.PlanCache(2))
+    ob = lambda i, p: b(i, p, Circ=O.Circuit)
+    out, jx, jp, _, _ = O.layer(ob, x, th)
+    check_vals(res, out, prec)
+    j = jac.cpu().numpy()
+    check_vals(j[:, :2], jx, prec, grad=True)
+    check_vals(j[:, 2:], jp, prec, grad=True)
+    if tile_bits is not None:
+        assert "stream" in info["plan"].description
+
+
+def test_non_affine_builder_uses_per_sample_path():
+    def b(inputs, params):
+        c = Circuit(2)
+        c.ry(0, float(np.arctan(inputs[0])))
+        c.rx(1, params[0] * params[0])
+        c.cnot(0, 1)
+        c.measure(1)
+        return c
+    x = np.array([[0.3], [1.2]])
+    th = np.array([0.7])
+    out, gx, gp, layer = layer_run(b, x, th, "c128")
+    assert layer.last_info["path"] == "per_sample"
+
+    def _ob(i, p):
+        c = O.Circuit(2)
+        c.ry(0, float(np.arctan(i[0]))); c.rx(1, p[0] * p[0]); c.cnot(0, 1); c.measure(1)
+        return c
+    o, jx, jp, gxo, gpo = O.layer(_ob, x, th)
+    assert relative_error(out, o) < 1e-10
+    assert relative_error(gx, gxo, floor=1e-4) < 1e-10
+    assert relative_error(gp, gpo, floor=1e-4) < 1e-10
+
+
+# ---------------------------------------------------------------------------
+# reference behaviours pinned by hyqnet's own tests (test_qnn.py)
+def h_ry(inputs, params):
+    c = Circuit(1)
+    c.h(0)
+    c.ry(0, inputs[0])
+    c.measure(0)
+    return c
+
+
+def test_h_ry_closed_forms():
+    layer = QuantumLayer(h_ry, n_params=0)
+    th = np.linspace(-2 * np.pi, 2 * np.pi, 50)
+    x = Tensor(th.reshape(-1, 1), requires_grad=True, dtype=np.float64)
+    out = layer(x)
+    np.testing.assert_allclose(out.numpy()[:, 0], (1 + np.sin(th)) / 2, atol=1e-12)
+    backward(tsum(out))
+    np.testing.assert_allclose(x.grad[:, 0], np.cos(th) / 2, atol=1e-10)
+
+
+@pytest.mark.parametrize("scale", [0.5, 1.0])
+@pytest.mark.parametrize("shift", [np.pi / 2, 0.3])
+def test_grad_scale_and_shift(scale, shift):
+    layer = QuantumLayer(h_ry, 0, grad_scale=scale, shift=shift)
+    x = Tensor(np.array([[0.4]]), requires_grad=True, dtype=np.float64)
+    backward(tsum(layer(x)))
+    want = ((1 + np.sin(0.4 + shift)) / 2 - (1 + np.sin(0.4 - shift)) / 2) * scale
+    assert x.grad[0, 0] == pytest.approx(want, abs=1e-12)
+
+
+def test_batch_rows_independent_and_dtype():
+    layer = QuantumLayer(h_ry, n_params=0)
+    x = np.array([[0.1], [0.7], [-1.3]])
+    together = layer(Tensor(x, dtype=np.float64)).numpy()
+    single = np.vstack([layer(Tensor(r.reshape(1, -1), dtype=np.float64)).numpy() for r in x])
+    np.testing.assert_allclose(together, single, atol=1e-14)
+    assert layer(Tensor(np.zeros((1, 1), dtype=np.float32))).dtype == np.float32
+    assert layer(Tensor(np.zeros((1, 1), dtype=np.float64))).dtype == np.float64
+    assert layer(Tensor(np.zeros((0, 1)))).shape == (0, 1)
+
+
+def test_param_grads_sum_over_batch():
+    def ry_param(inputs, params):
+        c = Circuit(1)
+        c.ry(0, params[0])
+        c.measure(0)
+        return c
+    layer = QuantumLayer(ry_param, n_params=1, param_init=[0.5])
+    backward(tsum(layer(Tensor(np.zeros((3, 1))))))
+    assert layer.params.grad[0] == pytest.approx(3 * np.sin(0.5) / 2, abs=1e-10)
+
+
+def test_no_grad_skips_jacobian():
+    b = wl.make_builder("cfg1", qsim, T)
+    layer = QuantumLayer(b, n_params=24, param_init=wl.params_for("cfg1"))
+    with no_grad():
+        out = layer(Tensor(wl.inputs_for("cfg1", 8), dtype=np.float64))
+    assert not out.requires_grad
+    assert "adjoint_slots=0" in layer.last_info["plan"].description
+
+
+def test_cfg4_full_size_norm_and_round_trip():
+    """Size-independent properties at the bench's full circuit (n = 20)."""
+    b = wl.make_builder("cfg4", qsim, T)
+    x = wl.inputs_for("cfg4", 2)
+    th = wl.params_for("cfg4")
+    tape, ok = engine.tr.trace(b, x, th)
+    import torch
+    for prec, tol in (("c128", 1e-12), ("c64", 1e-5)):
+        plan = engine.Plan(tape, 20, 400, prec)
+        st = plan.state(torch.tensor(x, device="cuda"), torch.tensor(th, device="cuda"))
+        z = st[..., 0].double() ** 2 + st[..., 1].double() ** 2
+        np.testing.assert_allclose(z.sum(dim=1).cpu().numpy(), 1.0, atol=tol)

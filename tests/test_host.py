@@ -1,0 +1,192 @@
+"""Host-side logic (CPU): circuit API + validation, tracer, gradient classifier,
+templates vs the oracle's restatement, autograd boundary."""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import hq_oracle as O
+from paper_2301_03251_b200 import (Circuit, CircuitError, ConfigError, EncodingError, FormatError,
+                                   GateOp, StatePrepOp, Tensor, backward, tsum, workloads as wl)
+from paper_2301_03251_b200 import templates as T
+from paper_2301_03251_b200 import qsim
+from paper_2301_03251_b200 import tracer as tr
+from paper_2301_03251_b200.qnn import QuantumLayer
+
+
+class TestCircuitApi:
+    def test_gateop_validation(self):
+        for args in [("T", (0,)), ("RX", (0,)), ("H", (0,), 0.5), ("CNOT", (0,)), ("X", (0, 1)),
+                     ("CNOT", (1, 1)), ("X", (-1,)), ("RY", (0,), float("nan"))]:
+            with pytest.raises(CircuitError):
+                GateOp(*args)
+
+    def test_circuit_range_and_measure(self):
+        c = Circuit(2)
+        with pytest.raises(CircuitError):
+            c.x(2)
+        c.measure(0, 1)
+        with pytest.raises(CircuitError):
+            c.measure(0)
+        with pytest.raises(CircuitError):
+            Circuit(0)
+        with pytest.raises(CircuitError):
+            Circuit(qsim.MAX_QUBITS + 1)
+
+    def test_text_round_trip(self):
+        c = Circuit(3)
+        c.h(0); c.cnot(0, 2); c.ry(1, 0.25); c.cr(1, 2, -0.5); c.measure(0, 2)
+        p = qsim.parse_circuit_text(qsim.format_circuit_text(c))
+        assert p.ops == c.ops and p.measured_qubits == c.measured_qubits
+        for bad in ("FOO 0\n", "H zero\n", "RX 0\n"):
+            with pytest.raises(FormatError):
+                qsim.parse_circuit_text(bad)
+
+    def test_probabilities_order(self):
+        sv = qsim.StateVector(3)
+        sv.amplitudes[:] = 0
+        sv.amplitudes[0b110] = 1.0  # q1 = 1, q2 = 1
+        p = qsim.probabilities(sv, [2, 0])
+        assert p[0b01] == 1.0  # bit 0 of outcome = qubit 2
+
+
+class TestTemplates:
+    def test_gate_lists_match_oracle(self, rng):
+        pairs = [
+            (T.cry(0, 1, 0.83), O.cry(0, 1, 0.83)),
+            (T.crz(1, 0, -1.37), O.crz(1, 0, -1.37)),
+            (T.ccz(0, 1, 2), O.ccz(0, 1, 2)),
+            (T.toffoli(3, 1, 0), O.toffoli(3, 1, 0)),
+            (T.cswap(0, 1, 2), O.cswap(0, 1, 2)),
+            (T.angle_embedding([0.1, 0.2], "X"), O.angle_embedding([0.1, 0.2], "X")),
+        ]
+        for v in (rng.standard_normal(16), [0.6, 0.8], [0.0, 0.0, 1.0, 0.0], [3, 1, -4, 1, -5]):
+            pairs.append((T.amplitude_embedding(v), O.amplitude_embedding(v)))
+        for mine, ref in pairs:
+            assert [(o.kind, o.targets) for o in mine] == [(o.kind, o.targets) for o in ref]
+            for a, b in zip(mine, ref):
+                assert (a.angle is None) == (b.angle is None)
+                if a.angle is not None:
+                    assert a.angle == pytest.approx(b.angle, abs=1e-15)
+
+    def test_embedding_errors(self):
+        for bad in ([0, 0, 0, 0], [1.0, np.nan]):
+            with pytest.raises(EncodingError):
+                T.amplitude_embedding(bad)
+        with pytest.raises(EncodingError):
+            T.amplitude_embedding([1, 2, 3], qubits=[0])
+        with pytest.raises(EncodingError):
+            T.angle_embedding([0.1], axis="W")
+        with pytest.raises(EncodingError):
+            T.basis_embedding([2])
+
+
+class TestTracer:
+    def test_cfg1_is_affine_and_adjoint(self):
+        b = wl.make_builder("cfg1", qsim, T)
+        x = wl.inputs_for("cfg1", 4)
+        th = wl.params_for("cfg1")
+        tape, ok = tr.trace(b, x, th)
+        assert ok and len(tape.ops) == 36 and len(tape.slot_const) == 28
+        mode, slot, factor = tr.classify(tape, 28, [True] * 28, math.pi / 2, 0.5)
+        assert (mode == tr.MODE_ADJOINT).all()
+        np.testing.assert_allclose(factor, 1.0)   # 2 * 0.5 * sin(pi/2)
+
+    def test_affine_forms(self):
+        def b(inputs, params):
+            c = Circuit(2)
+            c.ry(0, 2.0 * inputs[0] - params[1] / 4 + 0.5)
+            c.rz(1, -(params[0] + 1.0))
+            c.cr(0, 1, math.pi * params[1])
+            return c
+        tape, ok = tr.trace(b, np.array([[0.3]]), np.array([0.1, 0.2]))
+        assert ok
+        assert tape.slot_terms[0] == {0: 2.0, 2: -0.25} and tape.slot_const[0] == 0.5
+        assert tape.slot_terms[1] == {1: -1.0} and tape.slot_const[1] == -1.0
+        assert tape.slot_terms[2] == {2: math.pi}
+        mode, slot, factor = tr.classify(tape, 3, [True] * 3, math.pi / 2, 0.5)
+        # x0 and theta0 once each; theta1 twice -> two-point
+        assert list(mode) == [tr.MODE_ADJOINT, tr.MODE_ADJOINT, tr.MODE_TWOPOINT]
+        assert factor[0] == pytest.approx(math.sin(2.0 * math.pi / 2))
+        assert factor[1] == pytest.approx(math.sin(-math.pi / 2))
+
+    def test_hidden_nonlinearity_detected(self):
+        def b(inputs, params):
+            c = Circuit(1)
+            c.ry(0, float(np.sin(inputs[0])))
+            return c
+        _, ok = tr.trace(b, np.array([[0.3], [0.9]]), np.zeros(0))
+        assert not ok
+
+    def test_product_of_traced_values_is_non_affine(self):
+        def b(inputs, params):
+            c = Circuit(1)
+            c.ry(0, inputs[0] * params[0])
+            return c
+        _, ok = tr.trace(b, np.array([[0.3]]), np.array([0.2]))
+        assert not ok
+
+    def test_data_dependent_structure_detected(self):
+        def b(inputs, params):
+            c = Circuit(2)
+            if inputs[0] > 0:
+                c.x(1)
+            c.ry(0, inputs[0])
+            return c
+        _, ok = tr.trace(b, np.array([[0.3], [-0.2]]), np.zeros(0))
+        assert not ok
+
+    def test_amplitude_embedding_lowers_to_state_load(self):
+        b = wl.make_builder("cfg3", qsim, T)
+        x = wl.inputs_for("cfg3", 3)
+        tape, ok = tr.trace(b, x, wl.params_for("cfg3"))
+        assert ok
+        assert tape.ops[0][0] == "STATEPREP" and len(tape.preps) == 1
+        assert tape.preps[0][2] == 512
+        mode, _, _ = tr.classify(tape, 512 + 108, [True] * 620, math.pi / 2, 0.5)
+        assert (mode[:512] == tr.MODE_TWOPOINT).all()
+        assert (mode[512:] == tr.MODE_ADJOINT).all()
+
+    def test_builder_error_wrapped(self):
+        def b(inputs, params):
+            raise ValueError("boom")
+        with pytest.raises(CircuitError):
+            tr.trace(b, np.zeros((1, 1)), np.zeros(0))
+
+    def test_unused_variable_is_zero(self):
+        def b(inputs, params):
+            c = Circuit(1)
+            c.ry(0, params[0])
+            return c
+        tape, ok = tr.trace(b, np.zeros((1, 2)), np.array([0.1]))
+        mode, _, _ = tr.classify(tape, 3, [True] * 3, math.pi / 2, 0.5)
+        assert list(mode) == [tr.MODE_ZERO, tr.MODE_ZERO, tr.MODE_ADJOINT]
+
+
+class TestLayerConfig:
+    def test_config_validation(self):
+        b = wl.make_builder("cfg1", qsim, T)
+        for kw in (dict(machine_type="analog"), dict(n_params=-1), dict(shots=0),
+                   dict(shift=0.0), dict(n_params=2, param_init=[1.0]),
+                   dict(machine_type="noisy"), dict(precision="c32")):
+            args = dict(n_params=0)
+            args.update(kw)
+            with pytest.raises(ConfigError):
+                QuantumLayer(b, **args)
+
+    def test_default_init_draws_from_package_generator(self):
+        from paper_2301_03251_b200 import manual_seed
+        manual_seed(0)
+        a = QuantumLayer(lambda i, p: None, n_params=5).params.data.copy()
+        manual_seed(0)
+        want = np.random.default_rng(0).uniform(0, 2 * np.pi, 5)
+        np.testing.assert_array_equal(a, want)
+
+
+class TestAutogradBoundary:
+    def test_sum_backward(self):
+        x = Tensor(np.array([[1.0, 2.0]]), requires_grad=True)
+        y = tsum(x * 3.0 - 1.0)
+        backward(y)
+        np.testing.assert_array_equal(x.grad, [[3.0, 3.0]])
