@@ -144,6 +144,36 @@ hq_status hq_state(hq_plan plan, const double* x, int64_t ldx, const double* the
                    int64_t batch, const double* init, int64_t init_rows, double* state,
                    void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- introspection / measurement ---------------------------------------- */
+
+typedef struct {
+  int32_t path;              /* 0 = on-chip (state in shared memory), 1 = HBM streaming */
+  int32_t n_passes;          /* streaming: HBM passes per direction */
+  int32_t tile_bits;         /* amplitudes per tile = 2^tile_bits */
+  int32_t n_adjoint_slots;   /* derivatives produced by the adjoint sweep */
+  int32_t n_twopoint_vars;   /* variables evaluated by the batched two-point rule */
+  int64_t launches;          /* kernel launches one hq_forward(batch, flags) makes */
+  int64_t chunk_samples;     /* streaming: samples resident per launch */
+  double state_bytes;        /* bytes of one sample's state vector */
+} hq_plan_stats;
+
+hq_status hq_stats(hq_plan plan, int64_t batch, int32_t flags, hq_plan_stats* out);
+
+/* Kernel classes of the live profile. */
+enum { HQ_K_ONCHIP = 0, HQ_K_PASS_FWD = 1, HQ_K_PASS_BWD = 2, HQ_K_OTHER = 3, HQ_K_CLASSES = 4 };
+
+typedef struct {
+  double ms[HQ_K_CLASSES];       /* summed device time per class (CUDA events) */
+  int64_t launches[HQ_K_CLASSES];
+  double bytes[HQ_K_CLASSES];    /* state bytes each class reads + writes (traffic model) */
+} hq_profile_result;
+
+/* While enabled, every launch of this plan is bracketed by CUDA events on its
+ * stream.  hq_profile_read synchronises those events, sums them and resets.
+ * Not thread-safe while enabled. */
+hq_status hq_profile_enable(hq_plan plan, int32_t enable);
+hq_status hq_profile_read(hq_plan plan, hq_profile_result* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -139,10 +139,10 @@ def apply_gate(psi, n, op):
     if op.kind in _KINDS1:
         m = gate_matrix(op.kind, op.angle)
         v = _pair_view(psi, n, op.targets[0])
-        a0 = v[:, 0, :].copy()
-        a1 = v[:, 1, :].copy()
-        v[:, 0, :] = m[0, 0] * a0 + m[0, 1] * a1
-        v[:, 1, :] = m[1, 0] * a0 + m[1, 1] * a1
+        n0 = m[0, 0] * v[:, 0, :] + m[0, 1] * v[:, 1, :]
+        n1 = m[1, 0] * v[:, 0, :] + m[1, 1] * v[:, 1, :]
+        v[:, 0, :] = n0
+        v[:, 1, :] = n1
         return psi
     a, b = op.targets
     v, axa, axb = _quad_view(psi, n, a, b)

@@ -20,7 +20,9 @@ KIND_CODE = {"H": 0, "X": 1, "Y": 2, "Z": 3, "RX": 4, "RY": 5, "RZ": 6, "CNOT": 
              "CR": 9, "SWAP": 10, "STATEPREP": 11}
 
 EXPORTS = ("hq_abi_version", "hq_last_error", "hq_plan_create", "hq_plan_destroy",
-           "hq_plan_describe", "hq_workspace_bytes", "hq_forward", "hq_vjp", "hq_state")
+           "hq_plan_describe", "hq_workspace_bytes", "hq_forward", "hq_vjp", "hq_state",
+           "hq_stats", "hq_profile_enable", "hq_profile_read")
+K_CLASSES = ("onchip", "pass_fwd", "pass_bwd", "other")
 
 
 class HqOp(ctypes.Structure):
@@ -44,6 +46,18 @@ class HqPlanDesc(ctypes.Structure):
         ("grad_mode", _P), ("grad_slot", _P), ("grad_factor", _P),
         ("shift", ctypes.c_double), ("grad_scale", ctypes.c_double),
     ]
+
+
+class HqStats(ctypes.Structure):
+    _fields_ = [("path", ctypes.c_int32), ("n_passes", ctypes.c_int32),
+                ("tile_bits", ctypes.c_int32), ("n_adjoint_slots", ctypes.c_int32),
+                ("n_twopoint_vars", ctypes.c_int32), ("launches", ctypes.c_int64),
+                ("chunk_samples", ctypes.c_int64), ("state_bytes", ctypes.c_double)]
+
+
+class HqProfile(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_double * 4), ("launches", ctypes.c_int64 * 4),
+                ("bytes", ctypes.c_double * 4)]
 
 
 _lib = None
@@ -75,6 +89,12 @@ def lib():
     h.hq_state.argtypes = [_P, _P, ctypes.c_int64, _P, ctypes.c_int64, _P, ctypes.c_int64, _P, _P,
                            ctypes.c_size_t, _P]
     h.hq_state.restype = ctypes.c_int
+    h.hq_stats.argtypes = [_P, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(HqStats)]
+    h.hq_stats.restype = ctypes.c_int
+    h.hq_profile_enable.argtypes = [_P, ctypes.c_int32]
+    h.hq_profile_enable.restype = ctypes.c_int
+    h.hq_profile_read.argtypes = [_P, ctypes.POINTER(HqProfile)]
+    h.hq_profile_read.restype = ctypes.c_int
     if h.hq_abi_version() != 1:
         raise NativeError(f"libhq ABI {h.hq_abi_version()} != 1")
     _lib = h

@@ -519,6 +519,8 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
 
 extern "C" void hq_plan_destroy(hq_plan pl) {
   if (!pl) return;
+  for (auto& r : pl->prof.recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : pl->prof.pool) cudaEventDestroy(e);
   if (pl->dmem) cudaFree(pl->dmem);
   delete pl;
 }
@@ -597,5 +599,62 @@ extern "C" hq_status hq_vjp(hq_plan pl, const double* jac, const double* upstrea
   if (!jac || !upstream) return fail(HQ_E_CONFIG, "null jacobian / upstream");
   cudaError_t e = hq::launch_vjp(pl, jac, upstream, batch, grad_x, grad_theta, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(HQ_E_CUDA, std::string("vjp launch: ") + cudaGetErrorString(e));
+  return HQ_OK;
+}
+
+extern "C" hq_status hq_stats(hq_plan pl, int64_t batch, int32_t flags, hq_plan_stats* out) {
+  if (!pl || !out) return fail(HQ_E_CONFIG, "null plan / output");
+  const Layout L = layout_for(pl, batch, flags);
+  hq_plan_stats s{};
+  s.path = pl->onchip ? 0 : 1;
+  s.n_passes = pl->onchip ? 1 : (int32_t)pl->passes.size();
+  s.tile_bits = pl->tile_bits;
+  s.n_adjoint_slots = pl->n_adj;
+  s.n_twopoint_vars = pl->n_tp;
+  s.state_bytes = (double)(pl->precision == HQ_C64 ? 8 : 16) * (double)(1ll << pl->n_qubits);
+  const bool jac = (flags & HQ_WANT_JAC) != 0;
+  int64_t launches = 0;
+  if (batch > 0) {
+    if (pl->onchip) {
+      launches = 1;
+    } else {
+      const int64_t np = (int64_t)pl->passes.size();
+      const int64_t cs = L.sws.chunk_samples;
+      const int64_t real_chunks = (batch + cs - 1) / cs;
+      const int64_t shifted = L.V - batch;
+      const int64_t sh_chunks = (shifted + cs - 1) / cs;
+      const bool adj = jac && pl->n_adj > 0;
+      launches = real_chunks * (np + 1 + (adj ? np : 0)) + sh_chunks * (np + 1);
+      s.chunk_samples = cs;
+    }
+    if (jac && (int64_t)batch * (pl->n_inputs + pl->n_params) > 0) launches += 1;
+  }
+  s.launches = launches;
+  *out = s;
+  return HQ_OK;
+}
+
+extern "C" hq_status hq_profile_enable(hq_plan pl, int32_t enable) {
+  if (!pl) return fail(HQ_E_CONFIG, "null plan");
+  pl->prof.on = enable != 0;
+  return HQ_OK;
+}
+
+extern "C" hq_status hq_profile_read(hq_plan pl, hq_profile_result* out) {
+  if (!pl || !out) return fail(HQ_E_CONFIG, "null plan / output");
+  hq_profile_result r{};
+  for (auto& rec : pl->prof.recs) {
+    cudaError_t e = cudaEventSynchronize(rec.b);
+    if (e != cudaSuccess) return fail(HQ_E_CUDA, std::string("profile: ") + cudaGetErrorString(e));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, rec.a, rec.b);
+    r.ms[rec.cls] += ms;
+    r.launches[rec.cls] += 1;
+    r.bytes[rec.cls] += rec.bytes;
+    pl->prof.pool.push_back(rec.a);
+    pl->prof.pool.push_back(rec.b);
+  }
+  pl->prof.recs.clear();
+  *out = r;
   return HQ_OK;
 }

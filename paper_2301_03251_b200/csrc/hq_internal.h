@@ -2,6 +2,8 @@
 // kernels (hq_kernels.cu).  Nothing here crosses the C ABI.
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -75,6 +77,24 @@ struct PassDev {
   int32_t first, last;       // first pass (initialise state) / last pass (readout, λ init)
 };
 
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+  double bytes;
+};
+
+struct Prof {
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    cudaEvent_t e;
+    if (!pool.empty()) { e = pool.back(); pool.pop_back(); return e; }
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
 }  // namespace hq
 
 struct hq_plan_s {
@@ -101,4 +121,5 @@ struct hq_plan_s {
   const int32_t* d_pass_dlist = nullptr;
   const int32_t* d_pass_local = nullptr;  // [n_passes][n] (local then nonlocal)
   const int32_t* d_prep_off = nullptr;    // [n_preps]
+  mutable hq::Prof prof;                  // live per-launch timing (bench / profiling)
 };

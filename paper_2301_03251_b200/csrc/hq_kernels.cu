@@ -14,6 +14,7 @@
 //   k_vjp         upstream scaling + sequential batch sum (qnn.py:137-152).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 
 #include "hq_internal.h"
@@ -450,6 +451,26 @@ __global__ void k_vjp_theta(const double* __restrict__ jac, const double* __rest
 
 namespace hq {
 
+// Bracket one launch with events when the plan is being profiled.
+struct ProfScope {
+  const hq_plan_s* pl;
+  cudaStream_t st;
+  ProfRec r;
+  ProfScope(const hq_plan_s* p, cudaStream_t s, int cls, double bytes) : pl(p), st(s) {
+    if (!pl->prof.on) return;
+    r.cls = cls;
+    r.bytes = bytes;
+    r.a = pl->prof.get();
+    r.b = pl->prof.get();
+    cudaEventRecord(r.a, st);
+  }
+  ~ProfScope() {
+    if (!pl->prof.on) return;
+    cudaEventRecord(r.b, st);
+    pl->prof.recs.push_back(r);
+  }
+};
+
 static size_t onchip_smem(const hq_plan_s* pl, bool c64) {
   const size_t amp = c64 ? 8 : 16;
   const size_t prep = ((size_t)pl->dev.n_preps ? (size_t)pl->prep_total + 1 : 0) & ~(size_t)1;
@@ -489,7 +510,10 @@ static cudaError_t run_onchip(const hq_plan_s* pl, const KArgs& a, cudaStream_t 
   int64_t grid = a.V;
   if (grid > (1ll << 30)) grid = 1ll << 30;
   if (grid == 0) return cudaSuccess;
-  k_onchip<R><<<(unsigned)grid, T, smem, st>>>(a, pl->d_ops, (int)pl->dops.size());
+  {
+    ProfScope ps(pl, st, HQ_K_ONCHIP, (double)a.B * (pl->n_inputs + 1) * 8.0);
+    k_onchip<R><<<(unsigned)grid, T, smem, st>>>(a, pl->d_ops, (int)pl->dops.size());
+  }
   return cudaGetLastError();
 }
 
@@ -518,12 +542,15 @@ static cudaError_t run_stream(const hq_plan_s* pl, KArgs a, const StreamWs& ws, 
   const int n_chunks = ws.n_chunks;
   const int tpc = (int)(n_tiles / n_chunks);
   const int np = (int)pl->passes.size();
+  size_t sf = 0, sb = 0;
   for (int i = 0; i < np; ++i) {
-    const size_t sf = pass_smem(pl, pl->passes[i], sizeof(R) == 4, false, T);
-    const size_t sb = pass_smem(pl, pl->passes[i], sizeof(R) == 4, true, T);
-    cudaFuncSetAttribute(k_pass_fwd<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sf);
-    cudaFuncSetAttribute(k_pass_bwd<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+    sf = std::max(sf, pass_smem(pl, pl->passes[i], sizeof(R) == 4, false, T));
+    sb = std::max(sb, pass_smem(pl, pl->passes[i], sizeof(R) == 4, true, T));
   }
+  cudaError_t e0 = cudaFuncSetAttribute(k_pass_fwd<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sf);
+  if (e0 == cudaSuccess)
+    e0 = cudaFuncSetAttribute(k_pass_bwd<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+  if (e0 != cudaSuccess) return e0;
   // real rows [0, B) then shifted rows [B, V): a launch never mixes them, so
   // only real-row launches run the adjoint sweep
   const int64_t ranges[2][2] = {{0, a.B}, {a.B, a.V}};
@@ -539,17 +566,24 @@ static cudaError_t run_stream(const hq_plan_s* pl, KArgs a, const StreamWs& ws, 
       pa.psi = ws.psi;
       pa.lam = adj ? ws.lam : nullptr;
       pa.rpart = ws.rpart;
+      const double vec = (double)nv * (double)sizeof(typename Cx<R>::T) * (double)(1ll << n);
       for (int i = 0; i < np; ++i) {
         pa.ps = pass_dev(pl, i);
         const size_t sm = pass_smem(pl, pl->passes[i], sizeof(R) == 4, false, T);
+        const double moved = vec * ((i == 0 ? 0 : 1) + 1 + ((i == np - 1 && adj) ? 1 : 0));
+        ProfScope ps(pl, st, HQ_K_PASS_FWD, moved);
         k_pass_fwd<R><<<(unsigned)(nv * n_chunks), T, sm, st>>>(a, pa);
       }
-      k_readout_fold<<<(unsigned)((nv + 255) / 256), 256, 0, st>>>(ws.rpart, v0, nv, n_chunks, a.B,
-                                                                  a.out, a.tp);
+      {
+        ProfScope ps(pl, st, HQ_K_OTHER, (double)nv * n_chunks * 8.0);
+        k_readout_fold<<<(unsigned)((nv + 255) / 256), 256, 0, st>>>(ws.rpart, v0, nv, n_chunks, a.B,
+                                                                    a.out, a.tp);
+      }
       if (adj) {
         for (int i = np - 1; i >= 0; --i) {
           pa.ps = pass_dev(pl, i);
           const size_t sm = pass_smem(pl, pl->passes[i], sizeof(R) == 4, true, T);
+          ProfScope ps(pl, st, HQ_K_PASS_BWD, vec * (2 + (i == 0 ? 0 : 2)));
           k_pass_bwd<R><<<(unsigned)(nv * n_chunks), T, sm, st>>>(a, pa);
         }
       }
@@ -586,6 +620,7 @@ cudaError_t launch_forward(const hq_plan_s* pl, const LaunchIn& in, cudaStream_t
   if (in.jac) {
     const int64_t tot = in.B * pl->dev.n_vars;
     if (tot > 0) {
+      ProfScope ps(pl, st, HQ_K_OTHER, (double)tot * 8.0);
       k_jac<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->dev, in.B, in.dpart, in.n_parts, in.tp,
                                                          in.jac);
     }

@@ -130,6 +130,21 @@ class Plan:
                 pass
             self._h = None
 
+    def stats(self, B, want_jac=True) -> dict:
+        st = nat.HqStats()
+        nat.check(self._lib.hq_stats(self._h, int(B), nat.HQ_WANT_JAC if want_jac else 0,
+                                     ctypes.byref(st)), "stats")
+        return {f: getattr(st, f) for f, _ in nat.HqStats._fields_}
+
+    def profile(self, enable: bool) -> None:
+        nat.check(self._lib.hq_profile_enable(self._h, 1 if enable else 0), "profile")
+
+    def profile_read(self) -> dict:
+        r = nat.HqProfile()
+        nat.check(self._lib.hq_profile_read(self._h, ctypes.byref(r)), "profile")
+        return {k: {"ms": r.ms[i], "launches": r.launches[i], "bytes": r.bytes[i]}
+                for i, k in enumerate(nat.K_CLASSES)}
+
     def _ws(self, B, flags):
         torch = _torch()
         n = int(self._lib.hq_workspace_bytes(self._h, int(B), int(flags)))

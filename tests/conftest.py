@@ -34,14 +34,14 @@ def relative_error(a, b, floor=1e-8):
     return float(np.max(np.abs(a - b) / scale))
 
 
-def normwise_error(a, b):
-    """‖a − b‖∞ / ‖b‖∞ — the c64 gradient criterion (elementwise relative error
-    of near-zero gradient entries is ill-conditioned in float32)."""
+def normwise_error(a, b, floor=1e-300):
+    """‖a − b‖∞ / max(‖b‖∞, floor) — the c64 gradient criterion (elementwise
+    relative error of near-zero gradient entries is ill-conditioned in float32)."""
     a = np.asarray(a, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
     if a.size == 0:
         return 0.0
-    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), floor))
 
 
 def golden(name):
