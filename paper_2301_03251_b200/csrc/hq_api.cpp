@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -25,6 +26,7 @@
 
 #include "hq_internal.h"
 #include "hq_launch.h"
+#include "hq_jit.h"
 
 namespace {
 
@@ -262,6 +264,102 @@ std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int 
   return passes;
 }
 
+// register bits per thread in the streaming kernels (must match hq_stream.cu RBits)
+int reg_bits_for(int precision) { return precision == HQ_C64 ? 4 : 3; }
+
+uint16_t swz_host(uint32_t j) { return (uint16_t)(j ^ (((j >> 4) ^ (j >> 8)) & 15u)); }
+
+// Split one pass's ops (tile-bit operands) into register windows (see
+// hq_window.cuh): same greedy as the pass scheduler, capacity kRegBits, over
+// the exchange qubits; controls / diagonal qubits may be thread bits.
+void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB) {
+  auto exch = [](const hq::DOp& o) -> uint32_t {
+    switch (o.kind) {
+      case HQ_GATE_H: case HQ_GATE_X: case HQ_GATE_Y: case HQ_GATE_RX: case HQ_GATE_RY:
+        return 1u << o.a;
+      case HQ_GATE_CNOT:
+        return 1u << o.b;
+      default:
+        return 0u;
+    }
+  };
+  auto qmask = [](const hq::DOp& o) -> uint32_t {
+    uint32_t m = 0;
+    if (o.a >= 0) m |= 1u << o.a;
+    if (o.b >= 0) m |= 1u << o.b;
+    return m;
+  };
+  std::vector<int> dl(ops.size(), -1);
+  int ndl = 0;
+  for (size_t k = 0; k < ops.size(); ++k)
+    if (ops[k].dslot >= 0) dl[k] = ndl++;
+  std::vector<char> done(ops.size(), 0);
+  size_t left = ops.size();
+  const uint32_t all = (q >= 32) ? ~0u : ((1u << q) - 1);
+  do {
+    uint32_t Rm = 0;
+    std::vector<size_t> exec;
+    bool progress = true, first_scan = true;
+    while (progress) {
+      progress = false;
+      uint32_t blocked = 0;
+      for (size_t k = 0; k < ops.size(); ++k) {
+        if (done[k]) continue;
+        const uint32_t qs = qmask(ops[k]);
+        if (qs & blocked) { blocked |= qs; continue; }
+        const uint32_t ex = exch(ops[k]);
+        if ((ex & ~Rm) == 0 || popc(Rm | ex) <= RB) {
+          Rm |= ex;
+          done[k] = 1;
+          --left;
+          exec.push_back(k);
+          progress = true;
+        } else {
+          blocked |= qs;
+        }
+      }
+      if (first_scan) {
+        for (int b = q - 1; b >= 0 && popc(Rm) < RB; --b) Rm |= 1u << b;
+        first_scan = false;
+        progress = true;
+      }
+    }
+    // register bits, then thread bits: lanes first, covering all 4 bank classes
+    std::vector<int> R, S, rest;
+    for (int b = 0; b < q; ++b) (Rm >> b & 1u ? R : rest).push_back(b);
+    std::vector<char> used(rest.size(), 0);
+    for (int cls = 0; cls < 4 && (int)S.size() < 5; ++cls)
+      for (size_t i = 0; i < rest.size(); ++i)
+        if (!used[i] && (rest[i] & 3) == cls) { S.push_back(rest[i]); used[i] = 1; break; }
+    for (size_t i = 0; i < rest.size(); ++i)
+      if (!used[i]) S.push_back(rest[i]);
+    (void)all;
+    hq::WinDev w{};
+    w.op0 = (int16_t)ps.wops.size();
+    for (int i = 0; i < RB; ++i) w.pr[i] = swz_host(1u << R[i]);
+    for (size_t s2 = 0; s2 < S.size() && s2 < 10; ++s2) w.ps[s2] = swz_host(1u << S[s2]);
+    auto code = [&](int x) -> int8_t {
+      if (x < 0) return (int8_t)(64 + ~x);
+      for (int i = 0; i < RB; ++i) if (R[i] == x) return (int8_t)i;
+      for (size_t i = 0; i < S.size(); ++i) if (S[i] == x) return (int8_t)(16 + i);
+      return (int8_t)-1;
+    };
+    for (size_t k : exec) {
+      const hq::DOp& o = ops[k];
+      hq::WOp wo{};
+      wo.kind = (int8_t)o.kind;
+      wo.a = code(o.a);
+      wo.b = o.b == -1 && o.kind != HQ_GATE_CNOT && o.kind != HQ_GATE_CZ && o.kind != HQ_GATE_CR
+                 ? (int8_t)-1 : code(o.b);
+      wo.slot = (int16_t)o.slot;
+      wo.dl = (int16_t)dl[k];
+      ps.wops.push_back(wo);
+    }
+    w.op1 = (int16_t)ps.wops.size();
+    ps.wins.push_back(w);
+  } while (left > 0);
+}
+
 template <typename T>
 void put(std::vector<char>& blob, size_t& off, const T* src, size_t count, const T*& dst_dev_rel) {
   off = align_up(off, 16);
@@ -380,6 +478,23 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
       return fail(HQ_E_CONFIG, "circuit too small for the streaming path");
     }
     const int f = std::min(fixed_bits_for(d->precision), pl->tile_bits - 2);
+    // SWAP(a,b) = CNOT(a,b) CNOT(b,a) CNOT(a,b): register windows only permute along one bit
+    std::vector<hq_op> g2;
+    for (const auto& g : gates) {
+      if (g.kind == HQ_GATE_SWAP) {
+        g2.push_back(hq_op{HQ_GATE_CNOT, g.q0, g.q1, -1});
+        g2.push_back(hq_op{HQ_GATE_CNOT, g.q1, g.q0, -1});
+        g2.push_back(hq_op{HQ_GATE_CNOT, g.q0, g.q1, -1});
+      } else {
+        g2.push_back(g);
+      }
+    }
+    gates.swap(g2);
+    const int RB = reg_bits_for(d->precision);
+    if (pl->tile_bits - RB < 5 || pl->tile_bits - RB > 10) {
+      delete pl;
+      return fail(HQ_E_CONFIG, "tile must hold 2^9..2^14 amplitudes");
+    }
     pl->passes = schedule_passes(gates, n, pl->tile_bits, f);
     for (auto& ps : pl->passes) {
       int pos[kMaxQubits];
@@ -388,6 +503,7 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
       std::map<int, int> local_slot;
       ps.first_dop = (int32_t)pl->dops.size();
       ps.first_dlist = (int32_t)pass_dlist.size();
+      std::vector<hq::DOp> pops;
       for (int k : ps.op_ids) {
         const hq_op& g = gates[k];
         hq::DOp o{};
@@ -406,7 +522,9 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
         o.dslot = dslot_of(g);
         if (o.dslot >= 0) pass_dlist.push_back(o.dslot);
         pl->dops.push_back(o);
+        pops.push_back(o);
       }
+      plan_windows(ps, pops, pl->tile_bits, RB);
       ps.n_dops = (int32_t)ps.op_ids.size();
       ps.n_dslots_pass = (int32_t)pass_dlist.size() - ps.first_dlist;
       ps.first_slotlist = (int32_t)pass_slots.size();
@@ -418,6 +536,21 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
       pass_local.insert(pass_local.end(), row.begin(), row.end());
       pl->max_pass_slots = std::max(pl->max_pass_slots, (int32_t)ps.slots.size());
       pl->max_pass_dl = std::max(pl->max_pass_dl, ps.n_dslots_pass);
+    }
+  }
+
+  std::vector<int32_t> rz_slots;
+  for (int i = 0; i < d->n_ops; ++i)
+    if (d->ops[i].kind == HQ_GATE_RZ) rz_slots.push_back(d->ops[i].slot);
+
+  if (!pl->onchip) {
+    std::string why;
+    if (hq::jit_build(pl, why) != HQ_OK) {
+      pl->jit.ok = false;
+      pl->jit.why = why;
+      if (!(std::getenv("HQ_JIT") && std::getenv("HQ_JIT")[0] == '0'))
+        std::fprintf(stderr, "hq: pass specialisation unavailable (%s); using the generic window kernels\n",
+                     why.c_str());
     }
   }
 
@@ -455,6 +588,20 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
   put(blob, off, pass_slots.data(), pass_slots.size(), r_pslots);
   put(blob, off, pass_dlist.data(), pass_dlist.size(), r_pdl);
   put(blob, off, pass_local.data(), pass_local.size(), r_ploc);
+  std::vector<hq::WinDev> all_wins;
+  std::vector<hq::WOp> all_wops;
+  for (auto& ps : pl->passes) {
+    ps.first_win = (int32_t)all_wins.size();
+    ps.first_wop = (int32_t)all_wops.size();
+    all_wins.insert(all_wins.end(), ps.wins.begin(), ps.wins.end());
+    all_wops.insert(all_wops.end(), ps.wops.begin(), ps.wops.end());
+  }
+  const hq::WinDev* r_wins;
+  const hq::WOp* r_wops;
+  put(blob, off, all_wins.data(), all_wins.size(), r_wins);
+  put(blob, off, all_wops.data(), all_wops.size(), r_wops);
+  const int32_t* r_rz;
+  put(blob, off, rz_slots.data(), rz_slots.size(), r_rz);
   blob.resize(align_up(std::max<size_t>(blob.size(), 16)));
   cudaError_t ce = cudaMalloc(&pl->dmem, blob.size());
   if (ce != cudaSuccess) {
@@ -494,12 +641,16 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
   dv.var_dsl = rebase(r_vd, base);
   dv.var_tp = rebase(r_vt, base);
   dv.var_factor = rebase(r_vf, base);
-  pl->dev = dv;
   pl->d_ops = rebase(r_ops, base);
   pl->d_pass_slots = rebase(r_pslots, base);
   pl->d_pass_dlist = rebase(r_pdl, base);
   pl->d_pass_local = rebase(r_ploc, base);
   pl->d_prep_off = rebase(r_poff, base);
+  pl->d_wins = rebase(r_wins, base);
+  dv.n_rz = (int32_t)rz_slots.size();
+  dv.rz_slots = rebase(r_rz, base);
+  pl->dev = dv;
+  pl->d_wops = rebase(r_wops, base);
 
   std::ostringstream os;
   os << "n=" << n << " " << (d->precision == HQ_C64 ? "c64" : "c128") << " gates=" << gates.size()
@@ -508,8 +659,9 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
   if (pl->onchip) {
     os << " path=onchip smem=" << hq::onchip_smem_bytes(pl);
   } else {
-    os << " path=stream tile_bits=" << pl->tile_bits << " passes=" << pl->passes.size() << " [";
-    for (size_t i = 0; i < pl->passes.size(); ++i) os << (i ? "," : "") << pl->passes[i].n_dops;
+    os << " path=stream kernels=" << (pl->jit.ok ? "jit" : "generic") << " tile_bits=" << pl->tile_bits << " passes=" << pl->passes.size() << " [";
+    for (size_t i = 0; i < pl->passes.size(); ++i)
+      os << (i ? "," : "") << pl->passes[i].n_dops << "/" << pl->passes[i].wins.size() << "w";
     os << "]";
   }
   pl->description = os.str();
@@ -643,6 +795,8 @@ extern "C" hq_status hq_profile_enable(hq_plan pl, int32_t enable) {
 extern "C" hq_status hq_profile_read(hq_plan pl, hq_profile_result* out) {
   if (!pl || !out) return fail(HQ_E_CONFIG, "null plan / output");
   hq_profile_result r{};
+  const char* dump = std::getenv("HQ_PROFILE_DUMP");
+  int idx = 0;
   for (auto& rec : pl->prof.recs) {
     cudaError_t e = cudaEventSynchronize(rec.b);
     if (e != cudaSuccess) return fail(HQ_E_CUDA, std::string("profile: ") + cudaGetErrorString(e));
@@ -651,6 +805,10 @@ extern "C" hq_status hq_profile_read(hq_plan pl, hq_profile_result* out) {
     r.ms[rec.cls] += ms;
     r.launches[rec.cls] += 1;
     r.bytes[rec.cls] += rec.bytes;
+    if (dump && dump[0] == '1')
+      std::fprintf(stderr, "hq_prof %d cls=%d ms=%.4f bytes=%.0f GBps=%.1f\n", idx, rec.cls, ms, rec.bytes,
+                   ms > 0 ? rec.bytes / (ms * 1e6) : 0.0);
+    ++idx;
     pl->prof.pool.push_back(rec.a);
     pl->prof.pool.push_back(rec.b);
   }

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../../include/hq.h"
+#include "hq_pod.h"
 
 namespace hq {
 
@@ -25,30 +26,24 @@ struct DOp {
   int32_t pad[3];
 };
 
-// Device-resident, immutable plan constants (all pointers are device memory).
-struct DevPlan {
-  int32_t n_qubits;
-  int32_t n_slots;
-  int32_t n_inputs, n_params, n_vars;
-  int32_t n_measured;
-  int32_t n_preps;
-  int32_t n_tp;     // two-point variables
-  int32_t n_adj;    // derivative slots (distinct angle slots the adjoint sweep differentiates)
-  double shift, grad_scale;
-  const double* slot_const;
-  const int32_t* slot_ptr;
-  const int32_t* slot_var;
-  const double* slot_coef;
-  const int32_t* measured;
-  const int32_t* prep_ptr;
-  const int32_t* prep_qubits;
-  const int32_t* prep_slot0;
-  const int32_t* prep_len;
-  const int32_t* tp_var;       // [n_tp] variable ids
-  const int32_t* var_mode;     // [n_vars] HQ_GRAD_*
-  const int32_t* var_dsl;      // [n_vars] ADJOINT: derivative slot
-  const int32_t* var_tp;       // [n_vars] TWOPOINT: index into tp_var
-  const double* var_factor;    // [n_vars] ADJOINT: 2*grad_scale*sin(coef*shift)
+// One op of a register window (streaming path).  Operand codes:
+//   0..15 register bit, 16 + s thread-index bit s, 64 + g global qubit g
+//   outside the tile (constant over the tile).
+struct WOp {
+  int8_t kind;
+  int8_t a;        // target / control / first qubit
+  int8_t b;        // second operand or -1
+  int8_t pad0;
+  int16_t slot;    // pass-local trig slot or -1
+  int16_t dl;      // pass-local derivative index or -1
+};
+
+// A register window: which tile qubits are register bits (pr, swizzled masks)
+// and thread bits (ps), and its op range in the pass's WOp list.
+struct WinDev {
+  int16_t op0, op1;
+  uint16_t pr[4];   // swz(1 << R[i])
+  uint16_t ps[10];  // swz(1 << S[s]); thread-index bit s <-> tile qubit S[s]
 };
 
 // One HBM pass of the streaming path: tile = 2^q amplitudes gathered from the
@@ -62,19 +57,9 @@ struct Pass {
   int32_t first_slotlist = 0;      // offset into the device slot-list array
   int32_t n_dslots_pass = 0;       // ops in this pass that yield a derivative
   int32_t first_dlist = 0;         // offset into device list of dslot ids of this pass
-};
-
-struct PassDev {
-  int32_t q;                 // tile bits
-  int32_t n_ops;
-  const DOp* ops;
-  int32_t n_slots;           // slots used by this pass (trig cached per CTA)
-  const int32_t* slots;
-  int32_t n_dl;              // derivative-bearing ops in this pass
-  const int32_t* dlist;      // their dslot ids, in pass op order
-  const int32_t* local;      // [q] global qubit of each tile bit
-  const int32_t* nonlocal;   // [n-q] global qubit of each tile-id bit
-  int32_t first, last;       // first pass (initialise state) / last pass (readout, λ init)
+  std::vector<WinDev> wins;        // register windows of this pass
+  std::vector<WOp> wops;           // ops in window order
+  int32_t first_win = 0, first_wop = 0;
 };
 
 struct ProfRec {
@@ -121,5 +106,12 @@ struct hq_plan_s {
   const int32_t* d_pass_dlist = nullptr;
   const int32_t* d_pass_local = nullptr;  // [n_passes][n] (local then nonlocal)
   const int32_t* d_prep_off = nullptr;    // [n_preps]
+  const hq::WinDev* d_wins = nullptr;
+  const hq::WOp* d_wops = nullptr;
   mutable hq::Prof prof;                  // live per-launch timing (bench / profiling)
+  struct Jit {
+    bool ok = false;
+    std::string why;                      // why the static kernels run instead
+    std::vector<cudaKernel_t> fwd, bwd;   // per pass
+  } jit;
 };

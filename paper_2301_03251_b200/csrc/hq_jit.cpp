@@ -1,0 +1,758 @@
+// Per-plan specialisation of the HBM-streaming passes (NVRTC, sm_100a).
+//
+// The static window kernels (hq_stream.cu) interpret each gate at run time:
+// a switch on the register bit, runtime masks, operand decode — and every
+// switch merge forces register moves.  ncu showed ~8 instructions of overhead
+// per useful FP instruction.  Here the planner's windows are turned into
+// straight-line CUDA C++ instead, one kernel per pass and direction:
+//
+//   * register bits, slot offsets and swizzle masks are literals;
+//   * CNOT / X / SWAP between register bits are compile-time renamings of the
+//     register variables (no instructions at all);
+//   * diagonal gates on thread- or tile-constant bits fold into one pending
+//     per-thread phase, applied once per window;
+//   * RZ drops its global phase (multiplies only the |1> half), except when
+//     the caller asked for amplitudes (hq_state).
+//
+// The generated source = typedefs + hq_pod.h + hq_dev.cuh (embedded verbatim)
+// + the kernels.  Cubins are cached in-process and on disk
+// ($HQ_JIT_CACHE, default ~/.cache/hq_jit), keyed by a hash of the source.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <thread>
+#include <atomic>
+#include <sstream>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "hq_internal.h"
+#include "hq_jit.h"
+#include "hq_jit_src.inc"  // kJitPod, kJitDev: hq_pod.h / hq_dev.cuh as strings
+
+namespace hq {
+namespace {
+
+// ---------------------------------------------------------------------------
+// NVRTC, loaded lazily (no link-time dependency)
+typedef int nvrtcResult;
+typedef struct _nvrtcProgram* nvrtcProgram;
+
+struct Nvrtc {
+  bool ok = false;
+  std::string why;
+  nvrtcResult (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*, const char* const*) = nullptr;
+  nvrtcResult (*compile)(nvrtcProgram, int, const char* const*) = nullptr;
+  nvrtcResult (*cubin_size)(nvrtcProgram, size_t*) = nullptr;
+  nvrtcResult (*cubin)(nvrtcProgram, char*) = nullptr;
+  nvrtcResult (*log_size)(nvrtcProgram, size_t*) = nullptr;
+  nvrtcResult (*log)(nvrtcProgram, char*) = nullptr;
+  nvrtcResult (*destroy)(nvrtcProgram*) = nullptr;
+  nvrtcResult (*version)(int*, int*) = nullptr;
+};
+
+Nvrtc load_nvrtc() {
+  Nvrtc n;
+  const char* cands[] = {"libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"};
+  void* h = nullptr;
+  for (const char* c : cands)
+    if ((h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
+  if (!h) { n.why = "libnvrtc.so.12 not found"; return n; }
+  n.create = (decltype(n.create))dlsym(h, "nvrtcCreateProgram");
+  n.compile = (decltype(n.compile))dlsym(h, "nvrtcCompileProgram");
+  n.cubin_size = (decltype(n.cubin_size))dlsym(h, "nvrtcGetCUBINSize");
+  n.cubin = (decltype(n.cubin))dlsym(h, "nvrtcGetCUBIN");
+  n.log_size = (decltype(n.log_size))dlsym(h, "nvrtcGetProgramLogSize");
+  n.log = (decltype(n.log))dlsym(h, "nvrtcGetProgramLog");
+  n.destroy = (decltype(n.destroy))dlsym(h, "nvrtcDestroyProgram");
+  n.version = (decltype(n.version))dlsym(h, "nvrtcVersion");
+  n.ok = n.create && n.compile && n.cubin_size && n.cubin && n.log_size && n.log && n.destroy;
+  if (!n.ok) n.why = "libnvrtc lacks the expected symbols";
+  return n;
+}
+
+Nvrtc& nvrtc() {
+  static Nvrtc n = load_nvrtc();
+  return n;
+}
+
+uint64_t fnv1a(const std::string& s) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char c : s) { h ^= c; h *= 1099511628211ull; }
+  return h;
+}
+
+std::mutex g_mu;
+std::unordered_map<uint64_t, cudaLibrary_t> g_libs;  // per-process cubin cache (per current device)
+
+// $HQ_JIT_CACHE, else <package>/_jit_cache next to libhq.so (travels with the
+// repo, so cubins precompiled by build() are reused on the GPU box)
+std::string cache_dir() {
+  const char* e = std::getenv("HQ_JIT_CACHE");
+  if (e && *e) return e;
+  Dl_info info;
+  if (dladdr((void*)&cache_dir, &info) && info.dli_fname) {
+    std::string so = info.dli_fname;
+    const size_t k = so.rfind('/');
+    if (k != std::string::npos) return so.substr(0, k) + "/_jit_cache";
+  }
+  const char* home = std::getenv("HOME");
+  return std::string(home ? home : "/tmp") + "/.cache/hq_jit";
+}
+
+bool read_file(const std::string& path, std::vector<char>& out) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) return false;
+  out.assign(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+  return !out.empty();
+}
+
+void write_file(const std::string& path, const std::vector<char>& data) {
+  const std::string dir = path.substr(0, path.rfind('/'));
+  std::string cur;
+  for (size_t i = 1; i <= dir.size(); ++i)
+    if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
+  const std::string tmp = path + ".tmp" + std::to_string((long)getpid());
+  std::ofstream f(tmp, std::ios::binary);
+  f.write(data.data(), (std::streamsize)data.size());
+  f.close();
+  std::rename(tmp.c_str(), path.c_str());
+}
+
+// ---------------------------------------------------------------------------
+// source generation
+std::string hexu(uint32_t v) {
+  char b[32];
+  std::snprintf(b, sizeof b, "0x%xu", v);
+  return b;
+}
+
+struct Gen {
+  std::ostringstream o;
+  int RB, N, T, Q;
+  bool c64, exact;
+  std::vector<int> map;  // logical register index -> variable number
+  bool pending = false;  // a per-thread phase is pending in this window
+
+  std::string R() const { return c64 ? "float" : "double"; }
+  std::string P(int i) const { return "p" + std::to_string(map[i]); }
+  std::string L(int i) const { return "l" + std::to_string(map[i]); }
+
+  // operand expression for a runtime (thread / tile constant) bit
+  static std::string cond(int code) {
+    if (code >= 64) return "((base >> " + std::to_string(code - 64) + ") & 1ull)";
+    return "((tid >> " + std::to_string(code - 16) + ") & 1)";
+  }
+  static bool is_reg(int code) { return code >= 0 && code < 16; }
+
+  std::string trig(int s, int k) const { return "trig[" + std::to_string(4 * s + k) + "]"; }
+
+  void cmul_amp(const std::string& a, const std::string& x, const std::string& y) {
+    o << "{ const C z_ = " << a << "; " << a << ".x = z_.x * " << x << " - z_.y * " << y << "; "
+      << a << ".y = z_.x * " << y << " + z_.y * " << x << "; }\n";
+  }
+  void pend(const std::string& c, const std::string& x, const std::string& y) {
+    // php *= (c ? (x, y) : (1, 0))
+    if (!pending) { o << "R phx = (R)1, phy = (R)0;\n"; pending = true; }
+    o << "{ const bool c_ = " << c << "; const R ex = c_ ? (R)(" << x << ") : (R)1, ey = c_ ? (R)(" << y
+      << ") : (R)0; const R t_ = phx * ex - phy * ey; phy = phx * ey + phy * ex; phx = t_; }\n";
+  }
+  void flush_pending(bool both) {
+    if (!pending) return;
+    for (int i = 0; i < N; ++i) {
+      cmul_amp(P(i), "phx", "phy");
+      if (both) cmul_amp(L(i), "phx", "phy");
+    }
+    pending = false;
+  }
+
+  // one gate on the named register set(s); inv = apply the inverse
+  void apply(const WOp& op, bool inv, bool both) {
+    const int a = op.a, b = op.b;
+    const char* sg = inv ? "-" : "";
+    auto sets = [&](auto fn) { fn(false); if (both) fn(true); };
+    auto nm = [&](int i, bool lam) { return lam ? L(i) : P(i); };
+    switch (op.kind) {
+      case HQ_GATE_H: {
+        const int k = a;
+        sets([&](bool lam) {
+          for (int i = 0; i < N; ++i) {
+            if (i >> k & 1) continue;
+            const std::string A = nm(i, lam), B = nm(i | 1 << k, lam);
+            o << "{ const C a_ = " << A << ", b_ = " << B << "; " << A << ".x = HH * (a_.x + b_.x); " << A
+              << ".y = HH * (a_.y + b_.y); " << B << ".x = HH * (a_.x - b_.x); " << B << ".y = HH * (a_.y - b_.y); }\n";
+          }
+        });
+        break;
+      }
+      case HQ_GATE_X: {
+        const int k = a;
+        for (int i = 0; i < N; ++i)
+          if (!(i >> k & 1)) std::swap(map[i], map[i | 1 << k]);
+        break;
+      }
+      case HQ_GATE_Y: {
+        const int k = a;
+        sets([&](bool lam) {
+          for (int i = 0; i < N; ++i) {
+            if (i >> k & 1) continue;
+            const std::string A = nm(i, lam), B = nm(i | 1 << k, lam);
+            o << "{ const C a_ = " << A << ", b_ = " << B << "; " << A << ".x = b_.y; " << A << ".y = -b_.x; "
+              << B << ".x = -a_.y; " << B << ".y = a_.x; }\n";
+          }
+        });
+        break;
+      }
+      case HQ_GATE_RY: case HQ_GATE_RX: {
+        const int k = a;
+        o << "{ const R c_ = " << trig(op.slot, 0) << ", s_ = " << sg << trig(op.slot, 1) << ";\n";
+        sets([&](bool lam) {
+          for (int i = 0; i < N; ++i) {
+            if (i >> k & 1) continue;
+            const std::string A = nm(i, lam), B = nm(i | 1 << k, lam);
+            o << "{ const C a_ = " << A << ", b_ = " << B << "; ";
+            if (op.kind == HQ_GATE_RY)
+              o << A << ".x = c_ * a_.x - s_ * b_.x; " << A << ".y = c_ * a_.y - s_ * b_.y; " << B
+                << ".x = s_ * a_.x + c_ * b_.x; " << B << ".y = s_ * a_.y + c_ * b_.y; }\n";
+            else
+              o << A << ".x = c_ * a_.x + s_ * b_.y; " << A << ".y = c_ * a_.y - s_ * b_.x; " << B
+                << ".x = s_ * a_.y + c_ * b_.x; " << B << ".y = c_ * b_.y - s_ * a_.x; }\n";
+          }
+        });
+        o << "}\n";
+        break;
+      }
+      case HQ_GATE_Z: {
+        if (is_reg(a)) {
+          sets([&](bool lam) {
+            for (int i = 0; i < N; ++i)
+              if (i >> a & 1) o << nm(i, lam) << ".x = -" << nm(i, lam) << ".x; " << nm(i, lam) << ".y = -"
+                                << nm(i, lam) << ".y;\n";
+          });
+        } else {
+          pend(cond(a), "-1", "0");
+        }
+        break;
+      }
+      case HQ_GATE_RZ: {
+        if (exact) {
+          // diag(e^{-iφ/2}, e^{iφ/2}); inverse conjugates
+          const std::string s0 = inv ? "" : "-", s1 = inv ? "-" : "";
+          if (is_reg(a)) {
+            o << "{ const R c_ = " << trig(op.slot, 0) << ", s_ = " << trig(op.slot, 1) << ";\n";
+            sets([&](bool lam) {
+              for (int i = 0; i < N; ++i)
+                cmul_amp(nm(i, lam), "c_", (i >> a & 1) ? s1 + "s_" : s0 + "s_");
+            });
+            o << "}\n";
+          } else {
+            if (!pending) { o << "R phx = (R)1, phy = (R)0;\n"; pending = true; }
+            o << "{ const R c_ = " << trig(op.slot, 0) << ", s_ = " << cond(a) << " ? " << s1 << trig(op.slot, 1)
+              << " : " << s0 << trig(op.slot, 1) << "; const R t_ = phx * c_ - phy * s_; phy = phx * s_ + phy * c_; phx = t_; }\n";
+          }
+        } else {
+          // global phase dropped: |1> half times e^{iφ}
+          if (is_reg(a)) {
+            o << "{ const R c_ = " << trig(op.slot, 2) << ", s_ = " << sg << trig(op.slot, 3) << ";\n";
+            sets([&](bool lam) {
+              for (int i = 0; i < N; ++i)
+                if (i >> a & 1) cmul_amp(nm(i, lam), "c_", "s_");
+            });
+            o << "}\n";
+          } else {
+            pend(cond(a), trig(op.slot, 2), std::string(sg) + trig(op.slot, 3));
+          }
+        }
+        break;
+      }
+      case HQ_GATE_CNOT: {
+        const int kt = b;  // target: register bit (planner guarantees)
+        if (is_reg(a)) {
+          for (int i = 0; i < N; ++i)
+            if ((i >> a & 1) && !(i >> kt & 1)) std::swap(map[i], map[i | 1 << kt]);
+        } else {
+          o << "{ const bool c_ = " << cond(a) << ";\n";
+          sets([&](bool lam) {
+            for (int i = 0; i < N; ++i) {
+              if (i >> kt & 1) continue;
+              const std::string A = nm(i, lam), B = nm(i | 1 << kt, lam);
+              o << "{ const C a_ = " << A << ", b_ = " << B << "; " << A << " = c_ ? b_ : a_; " << B
+                << " = c_ ? a_ : b_; }\n";
+            }
+          });
+          o << "}\n";
+        }
+        break;
+      }
+      case HQ_GATE_CZ: case HQ_GATE_CR: {
+        int M = 0;
+        std::string cnd;
+        for (int code : {a, b}) {
+          if (is_reg(code)) M |= 1 << code;
+          else cnd += (cnd.empty() ? "" : " && ") + cond(code);
+        }
+        const std::string px = op.kind == HQ_GATE_CZ ? "(R)-1" : trig(op.slot, 2);
+        const std::string py = op.kind == HQ_GATE_CZ ? "(R)0" : std::string(sg) + trig(op.slot, 3);
+        if (cnd.empty()) {
+          o << "{ const R x_ = " << px << ", y_ = " << py << ";\n";
+          sets([&](bool lam) {
+            for (int i = 0; i < N; ++i)
+              if ((i & M) == M) cmul_amp(nm(i, lam), "x_", "y_");
+          });
+          o << "}\n";
+        } else if (M == 0) {
+          pend(cnd, px, py);
+        } else {
+          o << "{ const bool c_ = " << cnd << "; const R x_ = c_ ? (R)(" << px << ") : (R)1, y_ = c_ ? (R)(" << py
+            << ") : (R)0;\n";
+          sets([&](bool lam) {
+            for (int i = 0; i < N; ++i)
+              if ((i & M) == M) cmul_amp(nm(i, lam), "x_", "y_");
+          });
+          o << "}\n";
+        }
+        break;
+      }
+      case HQ_GATE_SWAP: {
+        for (int i = 0; i < N; ++i)
+          if ((i >> a & 1) && !(i >> b & 1)) std::swap(map[i], map[i ^ (1 << a) ^ (1 << b)]);
+        break;
+      }
+      default:
+        break;
+    }
+  }
+
+  // derivative dot at (ψ_k, λ_k) for ops with dl >= 0 (see hq_window.cuh for the formulas)
+  void dot(const WOp& op, bool per_thread, int nw) {
+    if (op.dl < 0) return;
+    const int a = op.a;
+    o << "{ R acc_ = (R)0;\n";
+    auto imd = [&](int i) { return "(" + L(i) + ".x * " + P(i) + ".y - " + L(i) + ".y * " + P(i) + ".x)"; };
+    switch (op.kind) {
+      case HQ_GATE_RY:
+        for (int i = 0; i < N; ++i) {
+          if (i >> a & 1) continue;
+          const int j = i | 1 << a;
+          o << "acc_ += " << L(j) << ".x * " << P(i) << ".x + " << L(j) << ".y * " << P(i) << ".y - " << L(i)
+            << ".x * " << P(j) << ".x - " << L(i) << ".y * " << P(j) << ".y;\n";
+        }
+        break;
+      case HQ_GATE_RX:
+        for (int i = 0; i < N; ++i) {
+          if (i >> a & 1) continue;
+          const int j = i | 1 << a;
+          o << "acc_ += " << L(i) << ".x * " << P(j) << ".y - " << L(i) << ".y * " << P(j) << ".x + " << L(j)
+            << ".x * " << P(i) << ".y - " << L(j) << ".y * " << P(i) << ".x;\n";
+        }
+        break;
+      case HQ_GATE_RZ: case HQ_GATE_CR: {
+        int M = 0;
+        std::string cnd;
+        std::vector<int> codes = {a};
+        if (op.kind == HQ_GATE_CR) codes.push_back(op.b);
+        for (int code : codes) {
+          if (is_reg(code)) M |= 1 << code;
+          else cnd += (cnd.empty() ? "" : " && ") + cond(code);
+        }
+        for (int i = 0; i < N; ++i)
+          if ((i & M) == M) o << "acc_ += " << imd(i) << ";\n";
+        if (!cnd.empty()) o << "if (!(" << cnd << ")) acc_ = (R)0;\n";
+        o << "acc_ *= (R)-2;\n";
+        break;
+      }
+      default:
+        break;
+    }
+    if (per_thread) {
+      o << "dacc[" << op.dl << " * T + tid] += acc_; }\n";
+    } else {
+      o << "acc_ = warp_sum_r(acc_); if ((tid & 31) == 0) dacc[" << op.dl << " * " << nw
+        << " + (tid >> 5)] += acc_; }\n";
+    }
+  }
+
+  void win_tb(const WinDev& w, int tbits) {
+    o << "const uint32_t tb = 0u";
+    for (int s = 0; s < tbits; ++s) o << " ^ ((tid & " << (1 << s) << ") ? " << hexu(w.ps[s]) << " : 0u)";
+    o << ";\n";
+  }
+  uint32_t phys(const WinDev& w, int i) const {
+    uint32_t p = 0;
+    for (int b = 0; b < RB; ++b)
+      if (i >> b & 1) p ^= w.pr[b];
+    return p;
+  }
+  void load_regs(const WinDev& w, const char* arr, const char* tile) {
+    for (int i = 0; i < N; ++i) o << arr << map[i] << " = " << tile << "[tb ^ " << hexu(phys(w, i)) << "];\n";
+  }
+  void store_regs(const WinDev& w, const char* arr, const char* tile) {
+    for (int i = 0; i < N; ++i) o << tile << "[tb ^ " << hexu(phys(w, i)) << "] = " << arr << map[i] << ";\n";
+  }
+};
+
+const char* kHeader = R"(
+typedef signed char int8_t; typedef unsigned char uint8_t; typedef short int16_t; typedef unsigned short uint16_t;
+typedef int int32_t; typedef unsigned int uint32_t; typedef long long int64_t; typedef unsigned long long uint64_t;
+typedef unsigned long size_t;
+#define HQ_GATE_H 0
+#define HQ_GATE_X 1
+#define HQ_GATE_Y 2
+#define HQ_GATE_Z 3
+#define HQ_GATE_RX 4
+#define HQ_GATE_RY 5
+#define HQ_GATE_RZ 6
+#define HQ_GATE_CNOT 7
+#define HQ_GATE_CZ 8
+#define HQ_GATE_CR 9
+#define HQ_GATE_SWAP 10
+)";
+
+const char* kHelpers = R"(
+namespace hq {
+__device__ __forceinline__ float warp_sum_r(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_r(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+}  // namespace hq
+)";
+
+size_t a16(size_t v) { return (v + 15) & ~(size_t)15; }
+
+}  // namespace
+
+// shared-memory layout of generated kernels (host and generator agree)
+JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd) {
+  const Pass& P = pl->passes[i];
+  const int RB = pl->precision == HQ_C64 ? 4 : 3;
+  const int T = 1 << (pl->tile_bits - RB);
+  const size_t amp = pl->precision == HQ_C64 ? 8 : 16, rsz = amp / 2;
+  JitLayout L{};
+  size_t o = a16((bwd ? 2 : 1) * (amp << pl->tile_bits));
+  L.lut = o; o = a16(o + 208 * 8);
+  L.trig = o; o = a16(o + P.slots.size() * 4 * rsz);
+  L.extra = o;
+  if (bwd) {
+    const size_t pt = (size_t)P.n_dslots_pass * T * rsz;
+    L.per_thread = pt <= 40 * 1024;
+    o = a16(o + (L.per_thread ? pt : (size_t)P.n_dslots_pass * (T / 32) * rsz));
+  } else {
+    o = a16(o + (96 + (size_t)(i == 0 ? ((pl->prep_total + 1) & ~1) : 0)) * 8);
+  }
+  L.total = o;
+  return L;
+}
+
+static std::string gen_pass(const hq_plan_s* pl, int pi, bool bwd) {
+  const bool exact = false;  // hq_state corrects the dropped RZ phases in the last pass
+  const Pass& P = pl->passes[pi];
+  const bool c64 = pl->precision == HQ_C64;
+  Gen g;
+  g.RB = c64 ? 4 : 3;
+  g.N = 1 << g.RB;
+  g.Q = pl->tile_bits;
+  g.T = 1 << (g.Q - g.RB);
+  g.c64 = c64;
+  g.exact = exact;
+  const int tbits = g.Q - g.RB;
+  const bool first = pi == 0, last = pi == (int)pl->passes.size() - 1;
+  const JitLayout L = jit_layout(pl, pi, bwd);
+  const int nw = g.T / 32;
+  std::ostringstream& o = g.o;
+  o << "extern \"C\" __global__ void __launch_bounds__(" << g.T << ", " << (bwd ? 2 : 3) << ") "
+    << (bwd ? "hq_b" : "hq_f") << pi << "(const hq::KArgs a, const hq::JPass ps) {\n"
+    << "using namespace hq;\n"
+    << "typedef " << g.R() << " R; typedef " << (c64 ? "float2" : "double2") << " C;\n"
+    << "constexpr int T = " << g.T << ", Q = " << g.Q << ";\n"
+    << "const R HH = (R)0.70710678118654752440;\n (void)HH;\n"
+    << "extern __shared__ __align__(16) unsigned char smem[];\n"
+    << "const DevPlan& p = a.p;\nconst int tid = threadIdx.x;\n"
+    << "const int64_t vl = blockIdx.x / ps.n_chunks;\nconst int chunk = (int)(blockIdx.x - vl * ps.n_chunks);\n"
+    << "const int64_t v = ps.v0 + vl;\nconst VSample vs = decode_vsample(p, v, a.B);\n"
+    << "C* tp = reinterpret_cast<C*>(smem);\n"
+    << (bwd ? "C* tl = tp + (1 << Q);\n" : "")
+    << "uint64_t* lut = reinterpret_cast<uint64_t*>(smem + " << L.lut << ");\nuint64_t* hi = lut + 192;\n"
+    << "R* trig = reinterpret_cast<R*>(smem + " << L.trig << ");\n";
+  if (bwd) {
+    o << "R* dacc = reinterpret_cast<R*>(smem + " << L.extra << ");\n"
+      << "for (int i = tid; i < " << P.n_dslots_pass * (L.per_thread ? g.T : nw) << "; i += T) dacc[i] = (R)0;\n";
+  } else {
+    o << "double* dx = reinterpret_cast<double*>(smem + " << L.extra << ");\n"
+      << "double* red = dx; double* inv = dx + 32; double* wt = dx + 64; double* sval = dx + 96;\n"
+      << "(void)red; (void)inv; (void)wt; (void)sval;\n";
+  }
+  o << "lut_build(ps.local, Q, lut, tid, T);\nload_trig4<R>(a, vs, ps.slots, ps.n_slots, trig, tid, T);\n";
+  if (!bwd && first) o << "if (p.n_preps > 0) load_prep_values(a, vs, sval, tid, T);\n";
+  if (!bwd && last)
+    o << "__shared__ double gph[2];\nif (a.state && tid == 0) { const double* xr = a.x + vs.b * a.ldx; double f = 0.0; "
+         "for (int k = 0; k < p.n_rz; ++k) f += eval_slot(p, p.rz_slots[k], xr, a.theta, vs.shvar, vs.shval); "
+         "gph[0] = cos(-0.5 * f); gph[1] = sin(-0.5 * f); }\n";
+  if (!bwd && last)
+    o << "if (tid < Q) { double w = 0.0; for (int i = 0; i < p.n_measured; ++i) if (p.measured[i] == ps.local[tid]) "
+         "w = (double)(1ull << i); wt[tid] = w; }\n";
+  o << "__syncthreads();\nconst uint64_t ot = lut_off(lut, (uint32_t)tid);\n"
+    << "if (tid < " << g.N << ") hi[tid] = lut_off(lut, (uint32_t)(tid * T));\n";
+  if (!bwd && first) o << "if (p.n_preps > 0) prep_norms(a, sval, inv, tid);\n";
+  o << "__syncthreads();\n"
+    << "C* gpsi = reinterpret_cast<C*>(ps.psi) + (size_t)vl * ((size_t)1 << p.n_qubits);\n"
+    << "C* glam = ps.lam ? reinterpret_cast<C*>(ps.lam) + (size_t)vl * ((size_t)1 << p.n_qubits) : nullptr;\n"
+    << "(void)glam;\n";
+  if (!bwd) o << "double e = 0.0; (void)e;\n";
+  o << "C";
+  for (int i = 0; i < g.N; ++i) o << (i ? ", " : " ") << "p" << i;
+  o << ";\n";
+  if (bwd) {
+    o << "C";
+    for (int i = 0; i < g.N; ++i) o << (i ? ", " : " ") << "l" << i;
+    o << ";\n";
+  }
+  o << "for (int tt = 0; tt < ps.tpc; ++tt) {\n"
+    << "const uint64_t base = tile_base_of(ps.nonlocal, p.n_qubits - Q, (uint64_t)chunk * ps.tpc + tt);\n";
+  // ---- stage in
+  if (!bwd && first) {
+    o << "if (a.init) { const double* src = a.init + (a.init_rows > 1 ? v : 0) * ((int64_t)1 << p.n_qubits) * 2;\n"
+      << "  for (uint32_t j = tid; j < (1u << Q); j += T) { const uint64_t g2 = base | lut_off(lut, j); "
+         "tp[swz(j)].x = (R)src[2 * g2]; tp[swz(j)].y = (R)src[2 * g2 + 1]; } }\n"
+      << "else if (p.n_preps > 0) { for (uint32_t j = tid; j < (1u << Q); j += T) { const double2 z = "
+         "init_amp(a, sval, inv, base | lut_off(lut, j)); tp[swz(j)].x = (R)z.x; tp[swz(j)].y = (R)z.y; } }\n"
+      << "else { for (uint32_t j = tid; j < (1u << Q); j += T) { tp[swz(j)].x = (R)((base | lut_off(lut, j)) == 0); "
+         "tp[swz(j)].y = (R)0; } }\n";
+  } else {
+    for (int i = 0; i < g.N; ++i) o << "p" << i << " = gpsi[base | ot | hi[" << i << "]];\n";
+    if (bwd)
+      for (int i = 0; i < g.N; ++i) o << "l" << i << " = glam[base | ot | hi[" << i << "]];\n";
+    for (int i = 0; i < g.N; ++i) o << "tp[swz((uint32_t)(tid + " << i << " * T))] = p" << i << ";\n";
+    if (bwd)
+      for (int i = 0; i < g.N; ++i) o << "tl[swz((uint32_t)(tid + " << i << " * T))] = l" << i << ";\n";
+  }
+  o << "__syncthreads();\n";
+  // ---- windows
+  const int nwin = (int)P.wins.size();
+  for (int wi = 0; wi < nwin; ++wi) {
+    const int w = bwd ? nwin - 1 - wi : wi;
+    const WinDev& W = P.wins[w];
+    g.map.assign(g.N, 0);
+    for (int i = 0; i < g.N; ++i) g.map[i] = i;
+    g.pending = false;
+    o << "{ // window " << w << "\n";
+    g.win_tb(W, tbits);
+    g.load_regs(W, "p", "tp");
+    if (bwd) g.load_regs(W, "l", "tl");
+    if (!bwd) {
+      for (int k = W.op0; k < W.op1; ++k) g.apply(P.wops[k], false, false);
+      g.flush_pending(false);
+    } else {
+      for (int k = W.op1 - 1; k >= W.op0; --k) {
+        g.dot(P.wops[k], L.per_thread, nw);
+        g.apply(P.wops[k], true, true);
+      }
+      g.flush_pending(true);
+    }
+    const bool need_store = !(bwd && first && wi == nwin - 1);
+    if (need_store) {
+      o << "__syncthreads();\n";
+      g.store_regs(W, "p", "tp");
+      if (bwd) g.store_regs(W, "l", "tl");
+      o << "__syncthreads();\n";
+    }
+    o << "}\n";
+  }
+  // ---- stage out
+  if (!bwd && last) {
+    o << "{ double wb = 0.0; for (int i = 0; i < p.n_measured; ++i) if ((base >> p.measured[i]) & 1ull) "
+         "wb += (double)(1ull << i);\n"
+      << "for (int bb = 0; bb < Q - " << g.RB << "; ++bb) if ((tid >> bb) & 1) wb += wt[bb];\n";
+    for (int i = 0; i < g.N; ++i) {
+      o << "{ double w = wb";
+      for (int b2 = 0; b2 < g.RB; ++b2)
+        if (i >> b2 & 1) o << " + wt[" << (g.Q - g.RB + b2) << "]";
+      o << "; const C z = tp[swz((uint32_t)(tid + " << i << " * T))]; const uint64_t g2 = base | ot | hi[" << i
+        << "]; e += w * (double)(z.x * z.x + z.y * z.y); gpsi[g2] = z;"
+        << " if (glam) { C y; y.x = (R)w * z.x; y.y = (R)w * z.y; glam[g2] = y; }"
+        << " if (a.state) { double* dst = a.state + v * ((int64_t)1 << p.n_qubits) * 2; "
+           "dst[2 * g2] = (double)z.x * gph[0] - (double)z.y * gph[1]; "
+           "dst[2 * g2 + 1] = (double)z.x * gph[1] + (double)z.y * gph[0]; } }\n";
+    }
+    o << "}\n";
+  } else if (!(bwd && first)) {
+    for (int i = 0; i < g.N; ++i) {
+      o << "gpsi[base | ot | hi[" << i << "]] = tp[swz((uint32_t)(tid + " << i << " * T))];\n";
+      if (bwd) o << "glam[base | ot | hi[" << i << "]] = tl[swz((uint32_t)(tid + " << i << " * T))];\n";
+    }
+  }
+  o << "__syncthreads();\n}\n";  // tile loop
+  if (!bwd && last) {
+    o << "e = block_sum<R>(e, red, tid, T);\nif (tid == 0) ps.rpart[vl * ps.n_chunks + chunk] = e;\n";
+  }
+  if (bwd) {
+    const int stride = L.per_thread ? g.T : nw;
+    o << "__syncthreads();\nfor (int i = tid; i < " << P.n_dslots_pass << "; i += T) { double s = 0.0; "
+      << "for (int k = 0; k < " << stride << "; ++k) s += (double)dacc[i * " << stride << " + k]; "
+      << "a.dpart[((int64_t)v * p.n_adj + ps.dlist[i]) * a.n_parts + chunk] = s; }\n";
+  }
+  o << "}\n";
+  return o.str();
+}
+
+namespace {
+
+struct Unit {
+  std::string src;
+  uint64_t hash = 0;
+  std::vector<char> cubin;
+  std::string err;
+  bool need_compile = false;
+};
+
+void compile_unit(Nvrtc& nv, Unit& u) {
+  nvrtcProgram prog = nullptr;
+  if (nv.create(&prog, u.src.c_str(), "hq_jit.cu", 0, nullptr, nullptr) != 0) {
+    u.err = "nvrtcCreateProgram failed";
+    return;
+  }
+  const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "--fmad=true"};
+  const int rc = nv.compile(prog, 4, opts);
+  if (rc != 0) {
+    size_t ls = 0;
+    nv.log_size(prog, &ls);
+    std::string log(ls, '\0');
+    if (ls) nv.log(prog, &log[0]);
+    u.err = "nvrtc compile failed: " + log.substr(0, 4000);
+  } else {
+    size_t cs = 0;
+    nv.cubin_size(prog, &cs);
+    u.cubin.resize(cs);
+    nv.cubin(prog, u.cubin.data());
+  }
+  nv.destroy(&prog);
+}
+
+}  // namespace
+
+// Build (or fetch) one cubin per pass (fwd + bwd kernels); missing cubins are
+// compiled concurrently on the host cores.
+hq_status jit_build(hq_plan_s* pl, std::string& err) {
+  const char* env = std::getenv("HQ_JIT");
+  if (env && env[0] == '0') { err = "disabled by HQ_JIT=0"; return HQ_E_CONFIG; }
+  Nvrtc& nv = nvrtc();
+  const int np = (int)pl->passes.size();
+  const std::string head = std::string(kHeader) + kJitPod + kJitDev + kHelpers;
+  std::vector<Unit> units(np);
+  std::string dump;
+  for (int i = 0; i < np; ++i) {
+    units[i].src = head + gen_pass(pl, i, false) + gen_pass(pl, i, true);
+    units[i].hash = fnv1a(units[i].src);
+    if (std::getenv("HQ_JIT_DUMP")) dump += units[i].src;
+  }
+  if (const char* path = std::getenv("HQ_JIT_DUMP")) {
+    std::ofstream f(path);
+    f << dump;
+  }
+  const std::string dir = cache_dir();
+  auto path_of = [&](uint64_t h) {
+    char name[64];
+    std::snprintf(name, sizeof name, "/%016llx.sm_100a.cubin", (unsigned long long)h);
+    return dir + name;
+  };
+  std::vector<int> todo;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (int i = 0; i < np; ++i) {
+      if (g_libs.count(units[i].hash)) continue;
+      if (!read_file(path_of(units[i].hash), units[i].cubin)) { units[i].need_compile = true; todo.push_back(i); }
+    }
+  }
+  if (!todo.empty()) {
+    if (!nv.ok) { err = nv.why; return HQ_E_CONFIG; }
+    unsigned nthr = std::thread::hardware_concurrency();
+    if (const char* e = std::getenv("HQ_JIT_THREADS")) nthr = (unsigned)std::atoi(e);
+    if (nthr < 1) nthr = 1;
+    nthr = std::min<unsigned>(nthr, (unsigned)todo.size());
+    std::atomic<size_t> next{0};
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < nthr; ++t)
+      pool.emplace_back([&]() {
+        for (size_t k; (k = next.fetch_add(1)) < todo.size();) compile_unit(nv, units[todo[k]]);
+      });
+    for (auto& th : pool) th.join();
+    for (int i : todo) {
+      if (!units[i].err.empty()) { err = units[i].err; return HQ_E_CUDA; }
+      write_file(path_of(units[i].hash), units[i].cubin);
+    }
+  }
+  if (std::getenv("HQ_JIT_COMPILE_ONLY")) { err = "compile-only"; return HQ_E_CONFIG; }
+  pl->jit.fwd.assign(np, nullptr);
+  pl->jit.bwd.assign(np, nullptr);
+  for (int i = 0; i < np; ++i) {
+    cudaLibrary_t lib = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      auto it = g_libs.find(units[i].hash);
+      if (it != g_libs.end()) lib = it->second;
+    }
+    if (!lib) {
+      cudaError_t ce = cudaLibraryLoadData(&lib, units[i].cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+      if (ce != cudaSuccess) {
+        err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(ce);
+        return HQ_E_CUDA;
+      }
+      std::lock_guard<std::mutex> lk(g_mu);
+      g_libs[units[i].hash] = lib;
+    }
+    const std::string s = std::to_string(i);
+    if (cudaLibraryGetKernel(&pl->jit.fwd[i], lib, ("hq_f" + s).c_str()) != cudaSuccess ||
+        cudaLibraryGetKernel(&pl->jit.bwd[i], lib, ("hq_b" + s).c_str()) != cudaSuccess) {
+      err = "generated kernel missing";
+      return HQ_E_CUDA;
+    }
+    for (bool b : {false, true}) {
+      const JitLayout L = jit_layout(pl, i, b);
+      cudaError_t ce = cudaFuncSetAttribute((const void*)(b ? pl->jit.bwd[i] : pl->jit.fwd[i]),
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+      if (ce != cudaSuccess) {
+        err = std::string("smem attribute: ") + cudaGetErrorString(ce);
+        return HQ_E_CUDA;
+      }
+    }
+  }
+  pl->jit.ok = true;
+  return HQ_OK;
+}
+
+cudaError_t jit_launch_pass(const hq_plan_s* pl, int i, bool bwd, const KArgs& a, const JPass& ps,
+                            unsigned grid, cudaStream_t st) {
+  const JitLayout L = jit_layout(pl, i, bwd);
+  cudaKernel_t k = bwd ? pl->jit.bwd[i] : pl->jit.fwd[i];
+  const int RB = pl->precision == HQ_C64 ? 4 : 3;
+  const int T = 1 << (pl->tile_bits - RB);
+  KArgs ac = a;
+  JPass pc = ps;
+  void* args[] = {&ac, &pc};
+  cudaError_t e = cudaLaunchKernel((const void*)k, dim3(grid), dim3(T), args, L.total, st);
+  if (e != cudaSuccess && std::getenv("HQ_JIT_DEBUG")) {
+    cudaFuncAttributes fa{};
+    cudaError_t e2 = cudaFuncGetAttributes(&fa, (const void*)k);
+    std::fprintf(stderr, "hq_jit launch %s%d grid=%u block=%d smem=%zu -> %s | attrs(%s): regs=%d maxthr=%d "
+                 "static_smem=%zu maxdyn=%d local=%zu\n", bwd ? "hq_b" : "hq_f", i, grid, T, L.total,
+                 cudaGetErrorString(e), cudaGetErrorString(e2), fa.numRegs, fa.maxThreadsPerBlock,
+                 fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.localSizeBytes);
+  }
+  return e;
+}
+
+}  // namespace hq

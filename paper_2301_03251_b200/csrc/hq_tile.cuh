@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include "hq_internal.h"
+#include "hq_dev.cuh"
 
 namespace hq {
 
@@ -83,53 +84,6 @@ __device__ __forceinline__ uint32_t ins0(uint32_t p, int t) {
 }
 __device__ __forceinline__ uint32_t ins00(uint32_t p, int lo, int hi) {
   return ins0(ins0(p, lo), hi);
-}
-
-// Value of a tape variable for virtual sample (xrow, shifted var).
-__device__ __forceinline__ double var_value(const DevPlan& p, int var, const double* xrow,
-                                            const double* theta, int shvar, double shval) {
-  double v = var < p.n_inputs ? xrow[var] : theta[var - p.n_inputs];
-  if (var == shvar) v += shval;
-  return v;
-}
-
-__device__ __forceinline__ double eval_slot(const DevPlan& p, int s, const double* xrow,
-                                            const double* theta, int shvar, double shval) {
-  double v = p.slot_const[s];
-  const int k1 = p.slot_ptr[s + 1];
-  for (int k = p.slot_ptr[s]; k < k1; ++k)
-    v += p.slot_coef[k] * var_value(p, p.slot_var[k], xrow, theta, shvar, shval);
-  return v;
-}
-
-// Virtual sample v: v < B are the real rows; the rest are the shifted rows of
-// the batched two-point rule (qnn.py:44-51): row b, variable tp_var[j],
-// +shift (k even) / -shift (k odd).
-struct VSample {
-  int64_t b;
-  int shvar;
-  double shval;
-  int64_t u;  // index into the two-point result buffer, -1 for real rows
-};
-
-__device__ __forceinline__ VSample decode_vsample(const DevPlan& p, int64_t v, int64_t B) {
-  VSample r;
-  if (v < B) { r.b = v; r.shvar = -1; r.shval = 0.0; r.u = -1; return r; }
-  const int64_t u = v - B;
-  const int64_t per = 2 * (int64_t)p.n_tp;
-  r.b = u / per;
-  const int k = (int)(u - r.b * per);
-  r.shvar = p.tp_var[k >> 1];
-  r.shval = (k & 1) ? -p.shift : p.shift;
-  r.u = u;
-  return r;
-}
-
-template <typename R>
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
 }
 
 // ---------------------------------------------------------------------------

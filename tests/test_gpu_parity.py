@@ -28,7 +28,7 @@ PRECS = ["c128", "c64"]
 
 def check_vals(got, want, prec, grad=False):
     if prec == "c128":
-        assert relative_error(got, want, floor=1e-4) < 1e-10
+        assert relative_error(got, want, floor=1e-3 if grad else 1e-4) < 1e-10
     elif grad:
         assert normwise_error(got, want, floor=0.1) < 1e-5
     else:
@@ -196,7 +196,7 @@ def _random_layer_builder(n, depth, seed):
     return builder
 
 
-@pytest.mark.parametrize("n,tile_bits", [(5, None), (9, None), (9, 4), (14, None), (15, 6)])
+@pytest.mark.parametrize("n,tile_bits", [(5, None), (9, None), (11, 9), (13, 9), (14, None), (15, 10), (17, 9)])
 @pytest.mark.parametrize("prec", PRECS)
 def test_random_layers_vs_oracle(n, tile_bits, prec, monkeypatch):
     if tile_bits is not None:
