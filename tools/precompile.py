@@ -1,0 +1,44 @@
+"""Precompile (NVRTC, sm_100a) the specialised pass kernels of known plans on
+the build host, so GPU runs find their cubins in paper_2301_03251_b200/_jit_cache.
+
+No GPU needed: plan creation compiles first and only then fails at device upload.
+"""
+import math
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("HQ_JIT_COMPILE_ONLY", "1")
+
+from paper_2301_03251_b200 import engine, qsim, tracer as tr, workloads as wl  # noqa: E402
+from paper_2301_03251_b200 import templates as T  # noqa: E402
+
+
+class _FakeCuda:
+    @staticmethod
+    def current_device():
+        return 0
+
+
+class _FakeTorch:
+    cuda = _FakeCuda
+
+
+def plan_for(cfg, prec, want_x=False, want_p=True):
+    n, d, P, _, _ = wl.CONFIGS[cfg]
+    b = wl.make_builder(cfg, qsim, T)
+    tape, ok = tr.trace(b, wl.inputs_for(cfg, 2), wl.params_for(cfg))
+    grad = tr.classify(tape, d + P, [want_x] * d + [want_p] * P, math.pi / 2, 0.5)
+    try:
+        engine.Plan(tape, d, P, prec, grad)
+    except Exception:
+        pass  # expected without a GPU: the cubins are already on disk
+
+
+if __name__ == "__main__":
+    engine._torch = lambda: _FakeTorch
+    jobs = sys.argv[1:] or ["cfg4:c64", "cfg4:c128"]
+    for job in jobs:
+        cfg, prec = job.split(":")
+        plan_for(cfg, prec)
+        print("precompiled", job)
