@@ -213,3 +213,77 @@ def run_virtual(sch: Schedule, apply_local, initial=None):
     shards = [s * ph for s, ph in zip(shards, phases)]
     E = sum(readout_partial(shards[r], L, r, sch.final_layout, sch.measured) for r in range(R))
     return shards, E
+
+
+# ---------------------------------------------------------------------------
+# GPU execution
+def gpu_apply_local(L, precision="c128"):
+    """Local executor on the current CUDA device: the shard's gate list runs as
+    a plan with its angles as per-call inputs, starting from the shard."""
+    from . import engine
+
+    def apply_local(shard, ops):
+        from .qsim import Circuit, GateOp
+        c = Circuit(L)
+        for kind, t, a in ops:
+            c.add(GateOp(kind, t, a))
+        return engine.final_states([c], precision, init=shard)[0]
+    return apply_local
+
+
+def _pack_half(shard, l, bit):
+    """Elements of a device shard whose local bit l == bit, in index order."""
+    import torch
+    n = shard.shape[0]
+    v = shard.view(n >> (l + 1), 2, 1 << l)
+    return v[:, bit, :].reshape(-1)
+
+
+def run_nccl(sch: Schedule, apply_local_dev, rank: int, world: int, device, group=None):
+    """One rank per process.  ``apply_local_dev(shard_tensor, ops) -> tensor``
+    runs a local gate list on this rank's complex128 device shard; swaps are
+    pairwise NCCL send/recv of half a shard.  Returns (shard, E)."""
+    import torch
+    import torch.distributed as dist
+    L = sch.L
+    if (1 << sch.g) != world:
+        raise ValueError(f"schedule is for {1 << sch.g} ranks, world is {world}")
+    shard = torch.zeros(1 << L, dtype=torch.complex128, device=device)
+    if rank == 0:
+        shard[0] = 1.0
+    phase = 1.0 + 0.0j
+    for step in sch.steps:
+        if step[0] == "local":
+            ops, ph = resolve_local(step[1], L, rank)
+            if ops:
+                shard = apply_local_dev(shard, ops)
+            phase *= ph
+        else:
+            G, l = step[1], step[2]
+            k = G - L
+            rb = (rank >> k) & 1
+            partner = rank ^ (1 << k)
+            shard = shard * phase
+            phase = 1.0 + 0.0j
+            send = _pack_half(shard, l, 1 - rb).contiguous()
+            recv = torch.empty_like(send)
+            reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, send, partner, group),
+                                           dist.P2POp(dist.irecv, recv, partner, group)])
+            for r in reqs:
+                r.wait()
+            # our elements with bit l = 1-rb are replaced by the partner's with bit l = rb
+            v = shard.view((1 << L) >> (l + 1), 2, 1 << l)
+            v[:, 1 - rb, :] = recv.view((1 << L) >> (l + 1), 1 << l)
+    shard = shard * phase
+    p = shard.real ** 2 + shard.imag ** 2
+    idx = torch.arange(1 << L, device=device)
+    w = torch.zeros(1 << L, dtype=torch.float64, device=device)
+    for i, q in enumerate(sch.measured):
+        P = sch.final_layout[q]
+        if P < L:
+            w += ((idx >> P) & 1).double() * float(1 << i)
+        elif (rank >> (P - L)) & 1:
+            w += float(1 << i)
+    e = (w * p).sum().reshape(1)
+    dist.all_reduce(e, group=group)
+    return shard, float(e.item())
