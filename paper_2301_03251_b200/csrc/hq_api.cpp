@@ -539,9 +539,11 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
     }
   }
 
-  std::vector<int32_t> rz_slots;
-  for (int i = 0; i < d->n_ops; ++i)
+  std::vector<int32_t> rz_slots, rot_slots;
+  for (int i = 0; i < d->n_ops; ++i) {
     if (d->ops[i].kind == HQ_GATE_RZ) rz_slots.push_back(d->ops[i].slot);
+    if (d->ops[i].kind == HQ_GATE_RX || d->ops[i].kind == HQ_GATE_RY) rot_slots.push_back(d->ops[i].slot);
+  }
 
   if (!pl->onchip) {
     std::string why;
@@ -600,8 +602,9 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
   const hq::WOp* r_wops;
   put(blob, off, all_wins.data(), all_wins.size(), r_wins);
   put(blob, off, all_wops.data(), all_wops.size(), r_wops);
-  const int32_t* r_rz;
+  const int32_t *r_rz, *r_rot;
   put(blob, off, rz_slots.data(), rz_slots.size(), r_rz);
+  put(blob, off, rot_slots.data(), rot_slots.size(), r_rot);
   blob.resize(align_up(std::max<size_t>(blob.size(), 16)));
   cudaError_t ce = cudaMalloc(&pl->dmem, blob.size());
   if (ce != cudaSuccess) {
@@ -649,6 +652,8 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
   pl->d_wins = rebase(r_wins, base);
   dv.n_rz = (int32_t)rz_slots.size();
   dv.rz_slots = rebase(r_rz, base);
+  dv.n_rot = (int32_t)rot_slots.size();
+  dv.rot_slots = rebase(r_rot, base);
   pl->dev = dv;
   pl->d_wops = rebase(r_wops, base);
 

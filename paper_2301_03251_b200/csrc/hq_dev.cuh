@@ -158,19 +158,28 @@ __device__ __forceinline__ uint64_t tile_base_of(const int32_t* nonlocal, int nb
   return base;
 }
 
-// (c, s) of half the angle plus (cos, sin) of the full angle, per listed slot
+// Per listed slot, 8 values: (c, s) of half the angle, (cos, sin) of the full
+// angle, and the 3-shear form of the half-angle rotation
+//   [[c,-s],[s,c]] = sg * shear(t) * shear_y(u) * shear(t),
+// folded to |phi| <= pi/2 (sg = -1 absorbs the rest) so |t| <= 1.
 template <typename R>
-__device__ __forceinline__ void load_trig4(const KArgs& a, const VSample& vs, const int32_t* slots,
+__device__ __forceinline__ void load_trig8(const KArgs& a, const VSample& vs, const int32_t* slots,
                                            int n_slots, R* trig, int tid, int T) {
   const double* xr = a.x + vs.b * a.ldx;
   for (int i = tid; i < n_slots; i += T) {
     const double v = eval_slot(a.p, slots[i], xr, a.theta, vs.shvar, vs.shval);
     double sn, cs;
     sincos(0.5 * v, &sn, &cs);
-    trig[4 * i + 0] = (R)cs;
-    trig[4 * i + 1] = (R)sn;
-    trig[4 * i + 2] = (R)(cs * cs - sn * sn);
-    trig[4 * i + 3] = (R)(2.0 * cs * sn);
+    const double sg = cs < 0.0 ? -1.0 : 1.0;
+    const double c2 = sg * cs, s2 = sg * sn;
+    trig[8 * i + 0] = (R)cs;
+    trig[8 * i + 1] = (R)sn;
+    trig[8 * i + 2] = (R)(cs * cs - sn * sn);
+    trig[8 * i + 3] = (R)(2.0 * cs * sn);
+    trig[8 * i + 4] = (R)(-s2 / (1.0 + c2));
+    trig[8 * i + 5] = (R)s2;
+    trig[8 * i + 6] = (R)sg;
+    trig[8 * i + 7] = (R)0;
   }
 }
 

@@ -154,7 +154,17 @@ struct Gen {
   }
   static bool is_reg(int code) { return code >= 0 && code < 16; }
 
-  std::string trig(int s, int k) const { return "trig[" + std::to_string(4 * s + k) + "]"; }
+  std::string trig(int s, int k) const { return "trig[" + std::to_string(8 * s + k) + "]"; }
+
+  void ensure_pending() {
+    if (!pending) { o << "R phx = (R)1, phy = (R)0;\n"; pending = true; }
+  }
+  // in-place rotation of the real pair (x, y) by the slot's half angle (sign
+  // folded into the pending phase by the caller): 3 FMA
+  void shear(const std::string& x, const std::string& y, const char* t, const char* u) {
+    o << x << " = fmaf_r(" << t << ", " << y << ", " << x << "); " << y << " = fmaf_r(" << u << ", " << x << ", "
+      << y << "); " << x << " = fmaf_r(" << t << ", " << y << ", " << x << ");\n";
+  }
 
   void cmul_amp(const std::string& a, const std::string& x, const std::string& y) {
     o << "{ const C z_ = " << a << "; " << a << ".x = z_.x * " << x << " - z_.y * " << y << "; "
@@ -213,19 +223,24 @@ struct Gen {
         break;
       }
       case HQ_GATE_RY: case HQ_GATE_RX: {
+        // [[c,-s],[s,c]] = sg * shears; sg is the same for every amplitude of
+        // the sample (a global sign: irrelevant to E and to <λ|G|ψ>, restored
+        // for hq_state in the last pass).  Inverse: t, u -> -t, -u.
         const int k = a;
-        o << "{ const R c_ = " << trig(op.slot, 0) << ", s_ = " << sg << trig(op.slot, 1) << ";\n";
+        o << "{ const R t_ = " << sg << trig(op.slot, 4) << ", u_ = " << sg << trig(op.slot, 5) << ";\n";
         sets([&](bool lam) {
           for (int i = 0; i < N; ++i) {
             if (i >> k & 1) continue;
             const std::string A = nm(i, lam), B = nm(i | 1 << k, lam);
-            o << "{ const C a_ = " << A << ", b_ = " << B << "; ";
-            if (op.kind == HQ_GATE_RY)
-              o << A << ".x = c_ * a_.x - s_ * b_.x; " << A << ".y = c_ * a_.y - s_ * b_.y; " << B
-                << ".x = s_ * a_.x + c_ * b_.x; " << B << ".y = s_ * a_.y + c_ * b_.y; }\n";
-            else
-              o << A << ".x = c_ * a_.x + s_ * b_.y; " << A << ".y = c_ * a_.y - s_ * b_.x; " << B
-                << ".x = s_ * a_.y + c_ * b_.x; " << B << ".y = c_ * b_.y - s_ * a_.x; }\n";
+            if (op.kind == HQ_GATE_RY) {
+              // (a, b) -> R(phi)(a, b) componentwise
+              shear(A + ".x", B + ".x", "t_", "u_");
+              shear(A + ".y", B + ".y", "t_", "u_");
+            } else {
+              // RX: (a.x, b.y) rotate by -phi, (a.y, b.x) by +phi
+              shear(B + ".y", A + ".x", "t_", "u_");
+              shear(A + ".y", B + ".x", "t_", "u_");
+            }
           }
         });
         o << "}\n";
@@ -337,22 +352,26 @@ struct Gen {
     if (op.dl < 0) return;
     const int a = op.a;
     o << "{ R acc_ = (R)0;\n";
-    auto imd = [&](int i) { return "(" + L(i) + ".x * " + P(i) + ".y - " + L(i) + ".y * " + P(i) + ".x)"; };
+    auto imd = [&](int i) {
+      return "acc_ = fmaf_r(" + L(i) + ".x, " + P(i) + ".y, acc_); acc_ = fmaf_r(-" + L(i) + ".y, " + P(i) + ".x, acc_)";
+    };
     switch (op.kind) {
       case HQ_GATE_RY:
         for (int i = 0; i < N; ++i) {
           if (i >> a & 1) continue;
           const int j = i | 1 << a;
-          o << "acc_ += " << L(j) << ".x * " << P(i) << ".x + " << L(j) << ".y * " << P(i) << ".y - " << L(i)
-            << ".x * " << P(j) << ".x - " << L(i) << ".y * " << P(j) << ".y;\n";
+          o << "acc_ = fmaf_r(" << L(j) << ".x, " << P(i) << ".x, acc_); acc_ = fmaf_r(" << L(j) << ".y, " << P(i)
+            << ".y, acc_); acc_ = fmaf_r(-" << L(i) << ".x, " << P(j) << ".x, acc_); acc_ = fmaf_r(-" << L(i)
+            << ".y, " << P(j) << ".y, acc_);\n";
         }
         break;
       case HQ_GATE_RX:
         for (int i = 0; i < N; ++i) {
           if (i >> a & 1) continue;
           const int j = i | 1 << a;
-          o << "acc_ += " << L(i) << ".x * " << P(j) << ".y - " << L(i) << ".y * " << P(j) << ".x + " << L(j)
-            << ".x * " << P(i) << ".y - " << L(j) << ".y * " << P(i) << ".x;\n";
+          o << "acc_ = fmaf_r(" << L(i) << ".x, " << P(j) << ".y, acc_); acc_ = fmaf_r(-" << L(i) << ".y, " << P(j)
+            << ".x, acc_); acc_ = fmaf_r(" << L(j) << ".x, " << P(i) << ".y, acc_); acc_ = fmaf_r(-" << L(j)
+            << ".y, " << P(i) << ".x, acc_);\n";
         }
         break;
       case HQ_GATE_RZ: case HQ_GATE_CR: {
@@ -365,7 +384,7 @@ struct Gen {
           else cnd += (cnd.empty() ? "" : " && ") + cond(code);
         }
         for (int i = 0; i < N; ++i)
-          if ((i & M) == M) o << "acc_ += " << imd(i) << ";\n";
+          if ((i & M) == M) o << imd(i) << ";\n";
         if (!cnd.empty()) o << "if (!(" << cnd << ")) acc_ = (R)0;\n";
         o << "acc_ *= (R)-2;\n";
         break;
@@ -381,22 +400,30 @@ struct Gen {
     }
   }
 
+  // Padded shared layout: element j at pad(j) = j + (j>>4) + (j>>8).  pad is
+  // additive over disjoint bit sets, so a window address is a per-thread base
+  // (thread bits) plus an immediate (register bits); the bank of an 8-byte
+  // element is Σ bit_b·2^(b mod 4) mod 16, conflict-free when the lane bits
+  // cover the four classes (plan_windows picks them that way).
+  static uint32_t pad(uint32_t j) { return j + (j >> 4) + (j >> 8); }
+  static int bit_of(uint16_t m) { return 31 - __builtin_clz((unsigned)m); }  // raw bit behind swz(1<<b)
   void win_tb(const WinDev& w, int tbits) {
     o << "const uint32_t tb = 0u";
-    for (int s = 0; s < tbits; ++s) o << " ^ ((tid & " << (1 << s) << ") ? " << hexu(w.ps[s]) << " : 0u)";
+    for (int s = 0; s < tbits; ++s)
+      o << " + ((tid & " << (1 << s) << ") ? " << pad(1u << bit_of(w.ps[s])) << "u : 0u)";
     o << ";\n";
   }
   uint32_t phys(const WinDev& w, int i) const {
-    uint32_t p = 0;
+    uint32_t j = 0;
     for (int b = 0; b < RB; ++b)
-      if (i >> b & 1) p ^= w.pr[b];
-    return p;
+      if (i >> b & 1) j |= 1u << bit_of(w.pr[b]);
+    return pad(j);
   }
   void load_regs(const WinDev& w, const char* arr, const char* tile) {
-    for (int i = 0; i < N; ++i) o << arr << map[i] << " = " << tile << "[tb ^ " << hexu(phys(w, i)) << "];\n";
+    for (int i = 0; i < N; ++i) o << arr << map[i] << " = " << tile << "[tb + " << phys(w, i) << "u];\n";
   }
   void store_regs(const WinDev& w, const char* arr, const char* tile) {
-    for (int i = 0; i < N; ++i) o << tile << "[tb ^ " << hexu(phys(w, i)) << "] = " << arr << map[i] << ";\n";
+    for (int i = 0; i < N; ++i) o << tile << "[tb + " << phys(w, i) << "u] = " << arr << map[i] << ";\n";
   }
 };
 
@@ -419,6 +446,9 @@ typedef unsigned long size_t;
 
 const char* kHelpers = R"(
 namespace hq {
+__device__ __forceinline__ uint32_t jpad(uint32_t j) { return j + (j >> 4) + (j >> 8); }
+__device__ __forceinline__ float fmaf_r(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fmaf_r(double a, double b, double c) { return fma(a, b, c); }
 __device__ __forceinline__ float warp_sum_r(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -443,9 +473,11 @@ JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd) {
   const int T = 1 << (pl->tile_bits - RB);
   const size_t amp = pl->precision == HQ_C64 ? 8 : 16, rsz = amp / 2;
   JitLayout L{};
-  size_t o = a16((bwd ? 2 : 1) * (amp << pl->tile_bits));
+  const size_t tnp = (size_t)1 << pl->tile_bits;
+  const size_t padded = tnp + tnp / 16 + tnp / 256;   // pad(TN-1)+1
+  size_t o = a16((bwd ? 2 : 1) * amp * padded);
   L.lut = o; o = a16(o + 208 * 8);
-  L.trig = o; o = a16(o + P.slots.size() * 4 * rsz);
+  L.trig = o; o = a16(o + P.slots.size() * 8 * rsz);
   L.extra = o;
   if (bwd) {
     const size_t pt = (size_t)P.n_dslots_pass * T * rsz;
@@ -485,7 +517,8 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, bool bwd) {
     << "const int64_t vl = blockIdx.x / ps.n_chunks;\nconst int chunk = (int)(blockIdx.x - vl * ps.n_chunks);\n"
     << "const int64_t v = ps.v0 + vl;\nconst VSample vs = decode_vsample(p, v, a.B);\n"
     << "C* tp = reinterpret_cast<C*>(smem);\n"
-    << (bwd ? "C* tl = tp + (1 << Q);\n" : "")
+    << (bwd ? "C* tl = tp + ((1 << Q) + (1 << Q) / 16 + (1 << Q) / 256);\n" : "")
+    << "const uint32_t tpad = (uint32_t)tid + ((uint32_t)tid >> 4) + ((uint32_t)tid >> 8);\n"
     << "uint64_t* lut = reinterpret_cast<uint64_t*>(smem + " << L.lut << ");\nuint64_t* hi = lut + 192;\n"
     << "R* trig = reinterpret_cast<R*>(smem + " << L.trig << ");\n";
   if (bwd) {
@@ -496,12 +529,14 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, bool bwd) {
       << "double* red = dx; double* inv = dx + 32; double* wt = dx + 64; double* sval = dx + 96;\n"
       << "(void)red; (void)inv; (void)wt; (void)sval;\n";
   }
-  o << "lut_build(ps.local, Q, lut, tid, T);\nload_trig4<R>(a, vs, ps.slots, ps.n_slots, trig, tid, T);\n";
+  o << "lut_build(ps.local, Q, lut, tid, T);\nload_trig8<R>(a, vs, ps.slots, ps.n_slots, trig, tid, T);\n";
   if (!bwd && first) o << "if (p.n_preps > 0) load_prep_values(a, vs, sval, tid, T);\n";
   if (!bwd && last)
     o << "__shared__ double gph[2];\nif (a.state && tid == 0) { const double* xr = a.x + vs.b * a.ldx; double f = 0.0; "
          "for (int k = 0; k < p.n_rz; ++k) f += eval_slot(p, p.rz_slots[k], xr, a.theta, vs.shvar, vs.shval); "
-         "gph[0] = cos(-0.5 * f); gph[1] = sin(-0.5 * f); }\n";
+         "double sg = 1.0; for (int k = 0; k < p.n_rot; ++k) if (cos(0.5 * eval_slot(p, p.rot_slots[k], xr, a.theta, "
+         "vs.shvar, vs.shval)) < 0.0) sg = -sg; "
+         "gph[0] = sg * cos(-0.5 * f); gph[1] = sg * sin(-0.5 * f); }\n";
   if (!bwd && last)
     o << "if (tid < Q) { double w = 0.0; for (int i = 0; i < p.n_measured; ++i) if (p.measured[i] == ps.local[tid]) "
          "w = (double)(1ull << i); wt[tid] = w; }\n";
@@ -527,18 +562,18 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, bool bwd) {
   if (!bwd && first) {
     o << "if (a.init) { const double* src = a.init + (a.init_rows > 1 ? v : 0) * ((int64_t)1 << p.n_qubits) * 2;\n"
       << "  for (uint32_t j = tid; j < (1u << Q); j += T) { const uint64_t g2 = base | lut_off(lut, j); "
-         "tp[swz(j)].x = (R)src[2 * g2]; tp[swz(j)].y = (R)src[2 * g2 + 1]; } }\n"
+         "tp[jpad(j)].x = (R)src[2 * g2]; tp[jpad(j)].y = (R)src[2 * g2 + 1]; } }\n"
       << "else if (p.n_preps > 0) { for (uint32_t j = tid; j < (1u << Q); j += T) { const double2 z = "
-         "init_amp(a, sval, inv, base | lut_off(lut, j)); tp[swz(j)].x = (R)z.x; tp[swz(j)].y = (R)z.y; } }\n"
-      << "else { for (uint32_t j = tid; j < (1u << Q); j += T) { tp[swz(j)].x = (R)((base | lut_off(lut, j)) == 0); "
-         "tp[swz(j)].y = (R)0; } }\n";
+         "init_amp(a, sval, inv, base | lut_off(lut, j)); tp[jpad(j)].x = (R)z.x; tp[jpad(j)].y = (R)z.y; } }\n"
+      << "else { for (uint32_t j = tid; j < (1u << Q); j += T) { tp[jpad(j)].x = (R)((base | lut_off(lut, j)) == 0); "
+         "tp[jpad(j)].y = (R)0; } }\n";
   } else {
     for (int i = 0; i < g.N; ++i) o << "p" << i << " = gpsi[base | ot | hi[" << i << "]];\n";
     if (bwd)
       for (int i = 0; i < g.N; ++i) o << "l" << i << " = glam[base | ot | hi[" << i << "]];\n";
-    for (int i = 0; i < g.N; ++i) o << "tp[swz((uint32_t)(tid + " << i << " * T))] = p" << i << ";\n";
+    for (int i = 0; i < g.N; ++i) o << "tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u] = p" << i << ";\n";
     if (bwd)
-      for (int i = 0; i < g.N; ++i) o << "tl[swz((uint32_t)(tid + " << i << " * T))] = l" << i << ";\n";
+      for (int i = 0; i < g.N; ++i) o << "tl[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u] = l" << i << ";\n";
   }
   o << "__syncthreads();\n";
   // ---- windows
@@ -581,7 +616,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, bool bwd) {
       o << "{ double w = wb";
       for (int b2 = 0; b2 < g.RB; ++b2)
         if (i >> b2 & 1) o << " + wt[" << (g.Q - g.RB + b2) << "]";
-      o << "; const C z = tp[swz((uint32_t)(tid + " << i << " * T))]; const uint64_t g2 = base | ot | hi[" << i
+      o << "; const C z = tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u]; const uint64_t g2 = base | ot | hi[" << i
         << "]; e += w * (double)(z.x * z.x + z.y * z.y); gpsi[g2] = z;"
         << " if (glam) { C y; y.x = (R)w * z.x; y.y = (R)w * z.y; glam[g2] = y; }"
         << " if (a.state) { double* dst = a.state + v * ((int64_t)1 << p.n_qubits) * 2; "
@@ -591,8 +626,8 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, bool bwd) {
     o << "}\n";
   } else if (!(bwd && first)) {
     for (int i = 0; i < g.N; ++i) {
-      o << "gpsi[base | ot | hi[" << i << "]] = tp[swz((uint32_t)(tid + " << i << " * T))];\n";
-      if (bwd) o << "glam[base | ot | hi[" << i << "]] = tl[swz((uint32_t)(tid + " << i << " * T))];\n";
+      o << "gpsi[base | ot | hi[" << i << "]] = tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u];\n";
+      if (bwd) o << "glam[base | ot | hi[" << i << "]] = tl[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u];\n";
     }
   }
   o << "__syncthreads();\n}\n";  // tile loop

@@ -32,6 +32,8 @@ struct DevPlan {
   const double* var_factor;    // [n_vars] ADJOINT: 2*grad_scale*sin(coef*shift)
   int32_t n_rz;                // RZ gates (their dropped half-angle phases, for exact amplitudes)
   const int32_t* rz_slots;
+  int32_t n_rot;               // RX/RY gates (their dropped global signs, specialised kernels)
+  const int32_t* rot_slots;
 };
 
 struct KArgs {
