@@ -266,6 +266,7 @@ std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int 
 
 // register bits per thread in the streaming kernels (must match hq_stream.cu RBits)
 int reg_bits_for(int precision) { return precision == HQ_C64 ? 4 : 3; }
+#define RBITS(p) reg_bits_for(p)
 
 uint16_t swz_host(uint32_t j) { return (uint16_t)(j ^ (((j >> 4) ^ (j >> 8)) & 15u)); }
 
@@ -319,7 +320,17 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB) 
         }
       }
       if (first_scan) {
-        for (int b = q - 1; b >= 0 && popc(Rm) < RB; --b) Rm |= 1u << b;
+        // top up the register bits, keeping at least one thread bit in each of
+        // the 4 bank classes (b & 3) so window loads/stores stay conflict-free
+        auto class_left = [&](uint32_t m, int cls) {
+          int c = 0;
+          for (int b = 0; b < q; ++b)
+            if (!(m >> b & 1u) && (b & 3) == cls) ++c;
+          return c;
+        };
+        for (int pass2 = 0; pass2 < 2; ++pass2)
+          for (int b = q - 1; b >= 0 && popc(Rm) < RB; --b)
+            if (!(Rm >> b & 1u) && (pass2 == 1 || class_left(Rm, b & 3) > 1)) Rm |= 1u << b;
         first_scan = false;
         progress = true;
       }
@@ -556,6 +567,34 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
     }
   }
 
+  std::ostringstream os;
+  os << "n=" << n << " " << (d->precision == HQ_C64 ? "c64" : "c128") << " gates=" << gates.size()
+     << " slots=" << d->n_slots << " preps=" << d->n_preps << " adjoint_slots=" << pl->n_adj
+     << " twopoint_vars=" << pl->n_tp;
+  if (pl->onchip) {
+    os << " path=onchip smem=" << hq::onchip_smem_bytes(pl);
+  } else {
+    os << " path=stream kernels=" << (pl->jit.ok ? "jit" : "generic") << " tile_bits=" << pl->tile_bits << " passes=" << pl->passes.size() << " [";
+    for (size_t i = 0; i < pl->passes.size(); ++i)
+      os << (i ? "," : "") << pl->passes[i].n_dops << "/" << pl->passes[i].wins.size() << "w";
+    os << "]";
+    if (std::getenv("HQ_PLAN_VERBOSE")) {
+      auto bit = [](uint16_t m) { return 31 - __builtin_clz((unsigned)m); };
+      for (size_t i = 0; i < pl->passes.size(); ++i) {
+        os << "\n pass " << i << " local=";
+        for (int b : pl->passes[i].local) os << b << ",";
+        for (const auto& w : pl->passes[i].wins) {
+          os << "\n   win ops=" << (w.op1 - w.op0) << " R=";
+          for (int k = 0; k < RBITS(d->precision); ++k) os << bit(w.pr[k]) << ",";
+          os << " S=";
+          for (int k = 0; k < pl->tile_bits - RBITS(d->precision); ++k) os << bit(w.ps[k]) << ",";
+        }
+      }
+    }
+  }
+  pl->description = os.str();
+  if (std::getenv("HQ_PLAN_VERBOSE")) std::fprintf(stderr, "%s\n", pl->description.c_str());
+
   // ---- upload -------------------------------------------------------------
   std::vector<char> blob;
   size_t off = 0;
@@ -657,19 +696,6 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
   pl->dev = dv;
   pl->d_wops = rebase(r_wops, base);
 
-  std::ostringstream os;
-  os << "n=" << n << " " << (d->precision == HQ_C64 ? "c64" : "c128") << " gates=" << gates.size()
-     << " slots=" << d->n_slots << " preps=" << d->n_preps << " adjoint_slots=" << pl->n_adj
-     << " twopoint_vars=" << pl->n_tp;
-  if (pl->onchip) {
-    os << " path=onchip smem=" << hq::onchip_smem_bytes(pl);
-  } else {
-    os << " path=stream kernels=" << (pl->jit.ok ? "jit" : "generic") << " tile_bits=" << pl->tile_bits << " passes=" << pl->passes.size() << " [";
-    for (size_t i = 0; i < pl->passes.size(); ++i)
-      os << (i ? "," : "") << pl->passes[i].n_dops << "/" << pl->passes[i].wins.size() << "w";
-    os << "]";
-  }
-  pl->description = os.str();
   *out = pl;
   return HQ_OK;
 }
@@ -781,7 +807,8 @@ extern "C" hq_status hq_stats(hq_plan pl, int64_t batch, int32_t flags, hq_plan_
       const int64_t shifted = L.V - batch;
       const int64_t sh_chunks = (shifted + cs - 1) / cs;
       const bool adj = jac && pl->n_adj > 0;
-      launches = real_chunks * (np + 1 + (adj ? np : 0)) + sh_chunks * (np + 1);
+      const bool fused = adj && pl->jit.ok && pl->jit.fused != nullptr;
+      launches = real_chunks * (np + 1 + (adj ? (fused ? np - 1 : np) : 0)) + sh_chunks * (np + 1);
       s.chunk_samples = cs;
     }
     if (jac && (int64_t)batch * (pl->n_inputs + pl->n_params) > 0) launches += 1;

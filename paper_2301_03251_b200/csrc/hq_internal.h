@@ -113,5 +113,6 @@ struct hq_plan_s {
     bool ok = false;
     std::string why;                      // why the static kernels run instead
     std::vector<cudaKernel_t> fwd, bwd;   // per pass
+    cudaKernel_t fused = nullptr;         // last forward pass + its backward
   } jit;
 };

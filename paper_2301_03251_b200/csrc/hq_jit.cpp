@@ -447,6 +447,15 @@ typedef unsigned long size_t;
 const char* kHelpers = R"(
 namespace hq {
 __device__ __forceinline__ uint32_t jpad(uint32_t j) { return j + (j >> 4) + (j >> 8); }
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* dst, const void* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  if (BYTES == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 __device__ __forceinline__ float fmaf_r(float a, float b, float c) { return fmaf(a, b, c); }
 __device__ __forceinline__ double fmaf_r(double a, double b, double c) { return fma(a, b, c); }
 __device__ __forceinline__ float warp_sum_r(float v) {
@@ -464,10 +473,15 @@ __device__ __forceinline__ double warp_sum_r(double v) {
 
 size_t a16(size_t v) { return (v + 15) & ~(size_t)15; }
 
+bool jit_prefetch() {
+  const char* e = std::getenv("HQ_JIT_PREFETCH");
+  return e && e[0] == '1';   // measured slower on cfg4 (see profiles/); opt-in
+}
+
 }  // namespace
 
 // shared-memory layout of generated kernels (host and generator agree)
-JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd) {
+JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd, bool fused) {
   const Pass& P = pl->passes[i];
   const int RB = pl->precision == HQ_C64 ? 4 : 3;
   const int T = 1 << (pl->tile_bits - RB);
@@ -475,7 +489,8 @@ JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd) {
   JitLayout L{};
   const size_t tnp = (size_t)1 << pl->tile_bits;
   const size_t padded = tnp + tnp / 16 + tnp / 256;   // pad(TN-1)+1
-  size_t o = a16((bwd ? 2 : 1) * amp * padded);
+  const bool prefetch = !bwd && i != 0 && jit_prefetch();
+  size_t o = a16((bwd ? 2 : (prefetch ? 2 : 1)) * amp * padded);
   L.lut = o; o = a16(o + 208 * 8);
   L.trig = o; o = a16(o + P.slots.size() * 8 * rsz);
   L.extra = o;
@@ -483,15 +498,21 @@ JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd) {
     const size_t pt = (size_t)P.n_dslots_pass * T * rsz;
     L.per_thread = pt <= 40 * 1024;
     o = a16(o + (L.per_thread ? pt : (size_t)P.n_dslots_pass * (T / 32) * rsz));
-  } else {
-    o = a16(o + (96 + (size_t)(i == 0 ? ((pl->prep_total + 1) & ~1) : 0)) * 8);
   }
+  L.extra2 = o;
+  if (!bwd || fused) o = a16(o + (96 + (size_t)(i == 0 ? ((pl->prep_total + 1) & ~1) : 0)) * 8);
   L.total = o;
   return L;
 }
 
-static std::string gen_pass(const hq_plan_s* pl, int pi, bool bwd) {
+// mode 0: forward pass, 1: backward pass, 2: last forward pass fused with its
+// backward pass (λ = wψ formed in registers; the backward windows start from
+// the forward's final register mapping, so ψ/λ never round-trip through HBM)
+static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   const bool exact = false;  // hq_state corrects the dropped RZ phases in the last pass
+  const bool fused = mode == 2;
+  const bool bwd = mode != 0;    // needs λ, dacc
+  const bool fwd = mode != 1;    // applies forward gates / readout
   const Pass& P = pl->passes[pi];
   const bool c64 = pl->precision == HQ_C64;
   Gen g;
@@ -503,11 +524,11 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, bool bwd) {
   g.exact = exact;
   const int tbits = g.Q - g.RB;
   const bool first = pi == 0, last = pi == (int)pl->passes.size() - 1;
-  const JitLayout L = jit_layout(pl, pi, bwd);
+  const JitLayout L = jit_layout(pl, pi, bwd, fused);
   const int nw = g.T / 32;
   std::ostringstream& o = g.o;
   o << "extern \"C\" __global__ void __launch_bounds__(" << g.T << ", " << (bwd ? 2 : 3) << ") "
-    << (bwd ? "hq_b" : "hq_f") << pi << "(const hq::KArgs a, const hq::JPass ps) {\n"
+    << (fused ? "hq_fb" : (bwd ? "hq_b" : "hq_f")) << pi << "(const hq::KArgs a, const hq::JPass ps) {\n"
     << "using namespace hq;\n"
     << "typedef " << g.R() << " R; typedef " << (c64 ? "float2" : "double2") << " C;\n"
     << "constexpr int T = " << g.T << ", Q = " << g.Q << ";\n"
@@ -524,30 +545,31 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, bool bwd) {
   if (bwd) {
     o << "R* dacc = reinterpret_cast<R*>(smem + " << L.extra << ");\n"
       << "for (int i = tid; i < " << P.n_dslots_pass * (L.per_thread ? g.T : nw) << "; i += T) dacc[i] = (R)0;\n";
-  } else {
-    o << "double* dx = reinterpret_cast<double*>(smem + " << L.extra << ");\n"
+  }
+  if (fwd) {
+    o << "double* dx = reinterpret_cast<double*>(smem + " << L.extra2 << ");\n"
       << "double* red = dx; double* inv = dx + 32; double* wt = dx + 64; double* sval = dx + 96;\n"
       << "(void)red; (void)inv; (void)wt; (void)sval;\n";
   }
   o << "lut_build(ps.local, Q, lut, tid, T);\nload_trig8<R>(a, vs, ps.slots, ps.n_slots, trig, tid, T);\n";
-  if (!bwd && first) o << "if (p.n_preps > 0) load_prep_values(a, vs, sval, tid, T);\n";
+  if (fwd && first) o << "if (p.n_preps > 0) load_prep_values(a, vs, sval, tid, T);\n";
   if (!bwd && last)
     o << "__shared__ double gph[2];\nif (a.state && tid == 0) { const double* xr = a.x + vs.b * a.ldx; double f = 0.0; "
          "for (int k = 0; k < p.n_rz; ++k) f += eval_slot(p, p.rz_slots[k], xr, a.theta, vs.shvar, vs.shval); "
          "double sg = 1.0; for (int k = 0; k < p.n_rot; ++k) if (cos(0.5 * eval_slot(p, p.rot_slots[k], xr, a.theta, "
          "vs.shvar, vs.shval)) < 0.0) sg = -sg; "
          "gph[0] = sg * cos(-0.5 * f); gph[1] = sg * sin(-0.5 * f); }\n";
-  if (!bwd && last)
+  if (fwd && last)
     o << "if (tid < Q) { double w = 0.0; for (int i = 0; i < p.n_measured; ++i) if (p.measured[i] == ps.local[tid]) "
          "w = (double)(1ull << i); wt[tid] = w; }\n";
   o << "__syncthreads();\nconst uint64_t ot = lut_off(lut, (uint32_t)tid);\n"
     << "if (tid < " << g.N << ") hi[tid] = lut_off(lut, (uint32_t)(tid * T));\n";
-  if (!bwd && first) o << "if (p.n_preps > 0) prep_norms(a, sval, inv, tid);\n";
+  if (fwd && first) o << "if (p.n_preps > 0) prep_norms(a, sval, inv, tid);\n";
   o << "__syncthreads();\n"
     << "C* gpsi = reinterpret_cast<C*>(ps.psi) + (size_t)vl * ((size_t)1 << p.n_qubits);\n"
     << "C* glam = ps.lam ? reinterpret_cast<C*>(ps.lam) + (size_t)vl * ((size_t)1 << p.n_qubits) : nullptr;\n"
     << "(void)glam;\n";
-  if (!bwd) o << "double e = 0.0; (void)e;\n";
+  if (fwd) o << "double e = 0.0; (void)e;\n";
   o << "C";
   for (int i = 0; i < g.N; ++i) o << (i ? ", " : " ") << "p" << i;
   o << ";\n";
@@ -556,10 +578,32 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, bool bwd) {
     for (int i = 0; i < g.N; ++i) o << (i ? ", " : " ") << "l" << i;
     o << ";\n";
   }
+  // forward passes that read ψ: double-buffered tile, cp.async prefetch of
+  // tile t+1 while tile t computes
+  const bool pf = mode == 0 && !first && jit_prefetch();
+  const int cpb = c64 ? 8 : 16;
+  const std::string TNP = "((1 << Q) + (1 << Q) / 16 + (1 << Q) / 256)";
+  auto issue_prefetch = [&](const char* tile_expr, const char* buf) {
+    o << "{ const uint64_t nb = tile_base_of(ps.nonlocal, p.n_qubits - Q, " << tile_expr << ");\n";
+    for (int i = 0; i < g.N; ++i)
+      o << "cp_async<" << cpb << ">(" << buf << " + tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u, gpsi + (nb | ot | hi["
+        << i << "]));\n";
+    o << "}\ncp_commit();\n";
+  };
+  if (pf) {
+    o << "C* const tbuf0 = tp; C* const tbuf1 = tp + " << TNP << ";\n";
+    issue_prefetch("(uint64_t)chunk * ps.tpc", "tbuf0");
+  }
   o << "for (int tt = 0; tt < ps.tpc; ++tt) {\n"
     << "const uint64_t base = tile_base_of(ps.nonlocal, p.n_qubits - Q, (uint64_t)chunk * ps.tpc + tt);\n";
+  if (pf) {
+    o << "C* const tp = (tt & 1) ? tbuf1 : tbuf0;\n"
+      << "if (tt + 1 < ps.tpc) {\n";
+    issue_prefetch("(uint64_t)chunk * ps.tpc + tt + 1", "((tt & 1) ? tbuf0 : tbuf1)");
+    o << "cp_wait<1>(); } else { cp_wait<0>(); }\n";
+  }
   // ---- stage in
-  if (!bwd && first) {
+  if (fwd && first) {
     o << "if (a.init) { const double* src = a.init + (a.init_rows > 1 ? v : 0) * ((int64_t)1 << p.n_qubits) * 2;\n"
       << "  for (uint32_t j = tid; j < (1u << Q); j += T) { const uint64_t g2 = base | lut_off(lut, j); "
          "tp[jpad(j)].x = (R)src[2 * g2]; tp[jpad(j)].y = (R)src[2 * g2 + 1]; } }\n"
@@ -567,45 +611,100 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, bool bwd) {
          "init_amp(a, sval, inv, base | lut_off(lut, j)); tp[jpad(j)].x = (R)z.x; tp[jpad(j)].y = (R)z.y; } }\n"
       << "else { for (uint32_t j = tid; j < (1u << Q); j += T) { tp[jpad(j)].x = (R)((base | lut_off(lut, j)) == 0); "
          "tp[jpad(j)].y = (R)0; } }\n";
-  } else {
+  } else if (!pf) {
+    const bool in_lam = bwd && !fused;
     for (int i = 0; i < g.N; ++i) o << "p" << i << " = gpsi[base | ot | hi[" << i << "]];\n";
-    if (bwd)
+    if (in_lam)
       for (int i = 0; i < g.N; ++i) o << "l" << i << " = glam[base | ot | hi[" << i << "]];\n";
     for (int i = 0; i < g.N; ++i) o << "tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u] = p" << i << ";\n";
-    if (bwd)
+    if (in_lam)
       for (int i = 0; i < g.N; ++i) o << "tl[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u] = l" << i << ";\n";
   }
   o << "__syncthreads();\n";
   // ---- windows
   const int nwin = (int)P.wins.size();
-  for (int wi = 0; wi < nwin; ++wi) {
-    const int w = bwd ? nwin - 1 - wi : wi;
-    const WinDev& W = P.wins[w];
-    g.map.assign(g.N, 0);
-    for (int i = 0; i < g.N; ++i) g.map[i] = i;
-    g.pending = false;
-    o << "{ // window " << w << "\n";
-    g.win_tb(W, tbits);
-    g.load_regs(W, "p", "tp");
-    if (bwd) g.load_regs(W, "l", "tl");
-    if (!bwd) {
+  auto fwd_windows = [&](bool keep_last) {
+    for (int w = 0; w < nwin; ++w) {
+      const WinDev& W = P.wins[w];
+      g.map.assign(g.N, 0);
+      for (int i = 0; i < g.N; ++i) g.map[i] = i;
+      g.pending = false;
+      o << "{ // window " << w << "\n";
+      g.win_tb(W, tbits);
+      g.load_regs(W, "p", "tp");
       for (int k = W.op0; k < W.op1; ++k) g.apply(P.wops[k], false, false);
       g.flush_pending(false);
-    } else {
-      for (int k = W.op1 - 1; k >= W.op0; --k) {
+      if (!(keep_last && w == nwin - 1)) {
+        o << "__syncthreads();\n";
+        g.store_regs(W, "p", "tp");
+        o << "__syncthreads();\n}\n";
+      }
+    }
+  };
+  // In the first pass nothing is written back, so the backward sweep can stop
+  // at the earliest derivative-bearing gate (e.g. the input-encoding layer is
+  // never un-applied).
+  int stop_op = 0, stop_win = 0;
+  if (first) {
+    stop_op = (int)P.wops.size();
+    for (int k = 0; k < (int)P.wops.size(); ++k)
+      if (P.wops[k].dl >= 0) { stop_op = k; break; }
+    for (int w = 0; w < nwin; ++w)
+      if (P.wins[w].op1 > stop_op) { stop_win = w; break; }
+  }
+  auto bwd_windows = [&](bool continue_last) {
+    for (int wi = 0; wi < nwin; ++wi) {
+      const int w = nwin - 1 - wi;
+      if (first && w < stop_win) break;
+      const WinDev& W = P.wins[w];
+      const bool cont = continue_last && wi == 0;   // registers already hold window w
+      if (!cont) {
+        g.map.assign(g.N, 0);
+        for (int i = 0; i < g.N; ++i) g.map[i] = i;
+        o << "{ // window " << w << " (adjoint)\n";
+        g.win_tb(W, tbits);
+        g.load_regs(W, "p", "tp");
+        g.load_regs(W, "l", "tl");
+      }
+      g.pending = false;
+      const int lo = std::max<int>(W.op0, first ? stop_op : 0);
+      for (int k = W.op1 - 1; k >= lo; --k) {
         g.dot(P.wops[k], L.per_thread, nw);
-        g.apply(P.wops[k], true, true);
+        if (!(first && k == lo && P.wops[k].dl >= 0 && k == stop_op)) g.apply(P.wops[k], true, true);
       }
       g.flush_pending(true);
+      const bool need_store = !(first && (wi == nwin - 1 || w == stop_win));
+      if (need_store) {
+        o << "__syncthreads();\n";
+        g.store_regs(W, "p", "tp");
+        g.store_regs(W, "l", "tl");
+        o << "__syncthreads();\n";
+      }
+      o << "}\n";
     }
-    const bool need_store = !(bwd && first && wi == nwin - 1);
-    if (need_store) {
-      o << "__syncthreads();\n";
-      g.store_regs(W, "p", "tp");
-      if (bwd) g.store_regs(W, "l", "tl");
-      o << "__syncthreads();\n";
+  };
+  if (!fused) {
+    if (fwd) fwd_windows(false);
+    else bwd_windows(false);
+  } else {
+    fwd_windows(true);
+    // readout + λ = wψ on the last window's registers (tile index of logical
+    // register i = deposit(i, R) | deposit(tid, S))
+    const WinDev& W = P.wins[nwin - 1];
+    o << "{ double wb = 0.0; for (int i = 0; i < p.n_measured; ++i) if ((base >> p.measured[i]) & 1ull) "
+         "wb += (double)(1ull << i);\n";
+    for (int s2 = 0; s2 < tbits; ++s2)
+      o << "if ((tid >> " << s2 << ") & 1) wb += wt[" << Gen::bit_of(W.ps[s2]) << "];\n";
+    for (int i = 0; i < g.N; ++i) {
+      o << "{ const double w = wb";
+      for (int b2 = 0; b2 < g.RB; ++b2)
+        if (i >> b2 & 1) o << " + wt[" << Gen::bit_of(W.pr[b2]) << "]";
+      const std::string P_ = g.P(i), L_ = g.L(i);
+      o << "; e += w * (double)(" << P_ << ".x * " << P_ << ".x + " << P_ << ".y * " << P_ << ".y); "
+        << L_ << ".x = (R)w * " << P_ << ".x; " << L_ << ".y = (R)w * " << P_ << ".y; }\n";
     }
     o << "}\n";
+    bwd_windows(true);
   }
   // ---- stage out
   if (!bwd && last) {
@@ -631,7 +730,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, bool bwd) {
     }
   }
   o << "__syncthreads();\n}\n";  // tile loop
-  if (!bwd && last) {
+  if (fwd && last) {
     o << "e = block_sum<R>(e, red, tid, T);\nif (tid == 0) ps.rpart[vl * ps.n_chunks + chunk] = e;\n";
   }
   if (bwd) {
@@ -690,7 +789,7 @@ hq_status jit_build(hq_plan_s* pl, std::string& err) {
   std::vector<Unit> units(np);
   std::string dump;
   for (int i = 0; i < np; ++i) {
-    units[i].src = head + gen_pass(pl, i, false) + gen_pass(pl, i, true);
+    units[i].src = head + gen_pass(pl, i, 0) + gen_pass(pl, i, 1) + (i == np - 1 ? gen_pass(pl, i, 2) : "");
     units[i].hash = fnv1a(units[i].src);
     if (std::getenv("HQ_JIT_DUMP")) dump += units[i].src;
   }
@@ -751,14 +850,15 @@ hq_status jit_build(hq_plan_s* pl, std::string& err) {
     }
     const std::string s = std::to_string(i);
     if (cudaLibraryGetKernel(&pl->jit.fwd[i], lib, ("hq_f" + s).c_str()) != cudaSuccess ||
-        cudaLibraryGetKernel(&pl->jit.bwd[i], lib, ("hq_b" + s).c_str()) != cudaSuccess) {
+        cudaLibraryGetKernel(&pl->jit.bwd[i], lib, ("hq_b" + s).c_str()) != cudaSuccess ||
+        (i == np - 1 && cudaLibraryGetKernel(&pl->jit.fused, lib, ("hq_fb" + s).c_str()) != cudaSuccess)) {
       err = "generated kernel missing";
       return HQ_E_CUDA;
     }
-    for (bool b : {false, true}) {
-      const JitLayout L = jit_layout(pl, i, b);
-      cudaError_t ce = cudaFuncSetAttribute((const void*)(b ? pl->jit.bwd[i] : pl->jit.fwd[i]),
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+    for (int mode = 0; mode < (i == np - 1 ? 3 : 2); ++mode) {
+      const JitLayout L = jit_layout(pl, i, mode != 0, mode == 2);
+      cudaKernel_t k = mode == 0 ? pl->jit.fwd[i] : (mode == 1 ? pl->jit.bwd[i] : pl->jit.fused);
+      cudaError_t ce = cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
       if (ce != cudaSuccess) {
         err = std::string("smem attribute: ") + cudaGetErrorString(ce);
         return HQ_E_CUDA;
@@ -769,10 +869,11 @@ hq_status jit_build(hq_plan_s* pl, std::string& err) {
   return HQ_OK;
 }
 
-cudaError_t jit_launch_pass(const hq_plan_s* pl, int i, bool bwd, const KArgs& a, const JPass& ps,
+cudaError_t jit_launch_pass(const hq_plan_s* pl, int i, int mode, const KArgs& a, const JPass& ps,
                             unsigned grid, cudaStream_t st) {
-  const JitLayout L = jit_layout(pl, i, bwd);
-  cudaKernel_t k = bwd ? pl->jit.bwd[i] : pl->jit.fwd[i];
+  const bool bwd = mode != 0;
+  const JitLayout L = jit_layout(pl, i, bwd, mode == 2);
+  cudaKernel_t k = mode == 0 ? pl->jit.fwd[i] : (mode == 1 ? pl->jit.bwd[i] : pl->jit.fused);
   const int RB = pl->precision == HQ_C64 ? 4 : 3;
   const int T = 1 << (pl->tile_bits - RB);
   KArgs ac = a;

@@ -10,14 +10,15 @@
 namespace hq {
 
 struct JitLayout {
-  size_t lut, trig, extra, total;
+  size_t lut, trig, extra, extra2, total;
   bool per_thread;  // bwd: per-thread derivative accumulators (else per warp)
 };
 
-JitLayout jit_layout(const hq_plan_s* pl, int pass, bool bwd);
+JitLayout jit_layout(const hq_plan_s* pl, int pass, bool bwd, bool fused = false);
 // compile (or fetch from the in-process / on-disk cache) the plan's pass kernels
 hq_status jit_build(hq_plan_s* pl, std::string& err);
-cudaError_t jit_launch_pass(const hq_plan_s* pl, int pass, bool bwd, const KArgs& a, const JPass& ps,
+// mode 0 forward, 1 backward, 2 fused last-forward + first-backward
+cudaError_t jit_launch_pass(const hq_plan_s* pl, int pass, int mode, const KArgs& a, const JPass& ps,
                             unsigned grid, cudaStream_t st);
 
 }  // namespace hq

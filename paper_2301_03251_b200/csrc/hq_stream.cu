@@ -420,12 +420,21 @@ static cudaError_t run_stream_t(const hq_plan_s* pl, const KArgs& a, const Strea
       sa.lam = adj ? ws.lam : nullptr;
       sa.rpart = ws.rpart;
       const double vec = (double)nv * amp;
+      // specialised kernels + adjoint: the last forward pass and its backward
+      // run fused (λ = wψ in registers, no ψ/λ round trip through HBM)
+      const bool fuse = pl->jit.ok && adj && pl->jit.fused != nullptr;
       for (int i = 0; i < np; ++i) {
         sa.ps = wpass(pl, i);
         const size_t sm = wsmem(pl, i, false);
+        if (fuse && i == np - 1) {
+          ProfScope prof(pl, st, HQ_K_PASS_BWD, vec * ((i == 0 ? 0 : 1) + (i == 0 ? 0 : 2)));
+          cudaError_t e = jit_launch_pass(pl, i, 2, a, jpass(pl, i, sa), (unsigned)(nv * n_chunks), st);
+          if (e != cudaSuccess) return e;
+          continue;
+        }
         ProfScope prof(pl, st, HQ_K_PASS_FWD, vec * ((i == 0 ? 0 : 1) + 1 + ((i == np - 1 && adj) ? 1 : 0)));
         if (pl->jit.ok) {
-          cudaError_t e = jit_launch_pass(pl, i, false, a, jpass(pl, i, sa), (unsigned)(nv * n_chunks), st);
+          cudaError_t e = jit_launch_pass(pl, i, 0, a, jpass(pl, i, sa), (unsigned)(nv * n_chunks), st);
           if (e != cudaSuccess) return e;
         } else if (exact) {
           k_wfwd<R, true><<<(unsigned)(nv * n_chunks), T, sm, st>>>(a, sa);
@@ -439,12 +448,12 @@ static cudaError_t run_stream_t(const hq_plan_s* pl, const KArgs& a, const Strea
                                                                     a.out, a.tp);
       }
       if (adj) {
-        for (int i = np - 1; i >= 0; --i) {
+        for (int i = fuse ? np - 2 : np - 1; i >= 0; --i) {
           sa.ps = wpass(pl, i);
           const size_t sm = wsmem(pl, i, true);
           ProfScope prof(pl, st, HQ_K_PASS_BWD, vec * (2 + (i == 0 ? 0 : 2)));
           if (pl->jit.ok) {
-            cudaError_t e = jit_launch_pass(pl, i, true, a, jpass(pl, i, sa), (unsigned)(nv * n_chunks), st);
+            cudaError_t e = jit_launch_pass(pl, i, 1, a, jpass(pl, i, sa), (unsigned)(nv * n_chunks), st);
             if (e != cudaSuccess) return e;
           } else {
             k_wbwd<R><<<(unsigned)(nv * n_chunks), T, sm, st>>>(a, sa);
