@@ -257,17 +257,35 @@ def run_ours(a):
     S = int(st["n_passes"])
     fwd, bwd = prof["pass_fwd"], prof["pass_bwd"]
     if st["path"] == 1:
-        dom, name = (bwd, "k_pass_bwd") if bwd["ms"] >= fwd["ms"] else (fwd, "k_pass_fwd")
-        # fwd moves 2·2^n·b per pass, bwd 2·2·2^n·b (ψ and λ)
-        per_pass = (4 if name == "k_pass_bwd" else 2) * (1 << n) * b
+        # dominant kernel class: the backward passes (hq_b*, incl. the fused
+        # last-forward+first-backward kernel).  SURVEY.md §8(d): a backward pass
+        # moves 4·2^n·b bytes per sample (ψ and λ, read + write).
+        name = "hq_b* (backward passes)" if bwd["ms"] >= fwd["ms"] else "hq_f* (forward passes)"
+        dom = bwd if bwd["ms"] >= fwd["ms"] else fwd
+        per_pass = (4 if dom is bwd else 2) * (1 << n) * b
         alg = per_pass * S * B * a.steps
         achieved = alg / (dom["ms"] / 1e3) / 1e9
+        # all amplitude-update kernels together: 2·2^n·b·(S_f + 2·S_b)
+        alg_all = 2 * (1 << n) * b * (S + 2 * S) * B * a.steps
+        t_all = (fwd["ms"] + bwd["ms"]) / 1e3
+        traffic = None
+        try:
+            with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
+                ref = json.load(f)["hq_b" if dom is bwd else "hq_f"]
+            traffic = ref["dram_bytes_per_launch"] / ref["algorithmic_bytes_per_launch"] * (alg / max(dom["launches"], 1))
+        except Exception:
+            pass
         roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                "frac": achieved / peak, "traffic": traffic,
+                "traffic_note": "ncu dram__bytes_read+write per launch, ratio to algorithmic bytes from "
+                                "profiles/ncu_traffic.json scaled to this launch size",
+                "peak_source": peak_kind,
                 "launches": dom["launches"], "avg_launch_ms": dom["ms"] / max(dom["launches"], 1),
                 "algorithmic_bytes_per_launch": alg / max(dom["launches"], 1),
                 "passes_per_direction": S,
                 "share_of_step": dom["ms"] / (ms * a.steps),
+                "all_passes": {"achieved": alg_all / t_all / 1e9, "frac": alg_all / t_all / 1e9 / peak,
+                               "algorithmic_bytes_per_sample": alg_all / (B * a.steps)},
                 "all_kernels_ms_per_step": {k: v["ms"] / a.steps for k, v in prof.items()}}
     else:
         dom = prof["onchip"]

@@ -473,10 +473,6 @@ __device__ __forceinline__ double warp_sum_r(double v) {
 
 size_t a16(size_t v) { return (v + 15) & ~(size_t)15; }
 
-bool jit_prefetch() {
-  const char* e = std::getenv("HQ_JIT_PREFETCH");
-  return e && e[0] == '1';   // measured slower on cfg4 (see profiles/); opt-in
-}
 
 }  // namespace
 
@@ -489,9 +485,8 @@ JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd, bool fused) {
   JitLayout L{};
   const size_t tnp = (size_t)1 << pl->tile_bits;
   const size_t padded = tnp + tnp / 16 + tnp / 256;   // pad(TN-1)+1
-  const bool prefetch = !bwd && i != 0 && jit_prefetch();
-  size_t o = a16((bwd ? 2 : (prefetch ? 2 : 1)) * amp * padded);
-  L.lut = o; o = a16(o + 208 * 8);
+  size_t o = a16((bwd ? 2 : 1) * amp * padded);
+  L.lut = o;
   L.trig = o; o = a16(o + P.slots.size() * 8 * rsz);
   L.extra = o;
   if (bwd) {
@@ -507,12 +502,17 @@ JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd, bool fused) {
 
 // mode 0: forward pass, 1: backward pass, 2: last forward pass fused with its
 // backward pass (λ = wψ formed in registers; the backward windows start from
-// the forward's final register mapping, so ψ/λ never round-trip through HBM)
+// the forward's final register mapping, so ψ/λ never round-trip through HBM).
+//
+// Everything about the pass is known here, so global offsets are literals:
+// tile bit b sits at global bit local[b].  When a window's first f lane bits
+// are tile bits {0..f-1} (one contiguous 64 B run per 2^f lanes), its
+// registers are loaded from / stored to HBM directly, skipping the
+// shared-memory staging round trip at that end of the tile.
 static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
-  const bool exact = false;  // hq_state corrects the dropped RZ phases in the last pass
   const bool fused = mode == 2;
-  const bool bwd = mode != 0;    // needs λ, dacc
-  const bool fwd = mode != 1;    // applies forward gates / readout
+  const bool bwd = mode != 0;
+  const bool fwd = mode != 1;
   const Pass& P = pl->passes[pi];
   const bool c64 = pl->precision == HQ_C64;
   Gen g;
@@ -521,52 +521,125 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   g.Q = pl->tile_bits;
   g.T = 1 << (g.Q - g.RB);
   g.c64 = c64;
-  g.exact = exact;
+  g.exact = false;  // hq_state corrects the dropped RZ phases / rotation signs in the last pass
   const int tbits = g.Q - g.RB;
-  const bool first = pi == 0, last = pi == (int)pl->passes.size() - 1;
+  const int n = pl->n_qubits;
+  const int np = (int)pl->passes.size();
+  const bool first = pi == 0, last = pi == np - 1;
+  const int f = c64 ? 3 : 2;
   const JitLayout L = jit_layout(pl, pi, bwd, fused);
   const int nw = g.T / 32;
+  const int nwin = (int)P.wins.size();
   std::ostringstream& o = g.o;
+
+  std::vector<uint64_t> gbit(g.Q);
+  for (int b2 = 0; b2 < g.Q; ++b2) gbit[b2] = 1ull << P.local[b2];
+  std::vector<int> nonlocal;
+  for (int q = 0; q < n; ++q)
+    if (std::find(P.local.begin(), P.local.end(), q) == P.local.end()) nonlocal.push_back(q);
+  auto goff = [&](uint32_t tile_mask) {
+    uint64_t off = 0;
+    for (int b2 = 0; b2 < g.Q; ++b2)
+      if (tile_mask >> b2 & 1u) off |= gbit[b2];
+    return off;
+  };
+  auto hex64 = [](uint64_t v) {
+    char b[40];
+    std::snprintf(b, sizeof b, "0x%llxull", (unsigned long long)v);
+    return std::string(b);
+  };
+  auto Sbits = [&](const WinDev& W) {
+    std::vector<int> v;
+    for (int s2 = 0; s2 < tbits; ++s2) v.push_back(Gen::bit_of(W.ps[s2]));
+    return v;
+  };
+  auto Rbits = [&](const WinDev& W) {
+    std::vector<int> v;
+    for (int r = 0; r < g.RB; ++r) v.push_back(Gen::bit_of(W.pr[r]));
+    return v;
+  };
+  auto direct_ok = [&](const WinDev& W) {
+    const std::vector<int> S = Sbits(W);
+    for (int k = 0; k < f; ++k)
+      if (std::find(S.begin(), S.begin() + f, k) == S.begin() + f) return false;
+    return true;
+  };
+  // per-thread global offset of window W's thread bits
+  auto emit_tw = [&](const WinDev& W) {
+    const std::vector<int> S = Sbits(W);
+    o << "const uint64_t tw = 0ull";
+    for (int s2 = 0; s2 < tbits; ++s2) o << " | ((tid & " << (1 << s2) << ") ? " << hex64(gbit[S[s2]]) << " : 0ull)";
+    o << ";\n";
+  };
+  auto reg_goff = [&](const WinDev& W, int i) {
+    const std::vector<int> R = Rbits(W);
+    uint32_t m = 0;
+    for (int r = 0; r < g.RB; ++r)
+      if (i >> r & 1) m |= 1u << R[r];
+    return goff(m);
+  };
+  auto direct_load = [&](const WinDev& W, bool lam) {
+    o << "{\n";
+    emit_tw(W);
+    for (int i = 0; i < g.N; ++i) {
+      o << "p" << g.map[i] << " = gpsi[base | tw | " << hex64(reg_goff(W, i)) << "];\n";
+      if (lam) o << "l" << g.map[i] << " = glam[base | tw | " << hex64(reg_goff(W, i)) << "];\n";
+    }
+    o << "}\n";
+  };
+  auto direct_store = [&](const WinDev& W, bool lam) {
+    o << "{\n";
+    emit_tw(W);
+    for (int i = 0; i < g.N; ++i) {
+      o << "gpsi[base | tw | " << hex64(reg_goff(W, i)) << "] = p" << g.map[i] << ";\n";
+      if (lam) o << "glam[base | tw | " << hex64(reg_goff(W, i)) << "] = l" << g.map[i] << ";\n";
+    }
+    o << "}\n";
+  };
+  auto identity_map = [&]() {
+    g.map.assign(g.N, 0);
+    for (int i = 0; i < g.N; ++i) g.map[i] = i;
+  };
+  auto hi_off = [&](int i) { return goff((uint32_t)(i * g.T)); };
+
+  // ---- header / prologue
   o << "extern \"C\" __global__ void __launch_bounds__(" << g.T << ", " << (bwd ? 2 : 3) << ") "
     << (fused ? "hq_fb" : (bwd ? "hq_b" : "hq_f")) << pi << "(const hq::KArgs a, const hq::JPass ps) {\n"
     << "using namespace hq;\n"
     << "typedef " << g.R() << " R; typedef " << (c64 ? "float2" : "double2") << " C;\n"
     << "constexpr int T = " << g.T << ", Q = " << g.Q << ";\n"
-    << "const R HH = (R)0.70710678118654752440;\n (void)HH;\n"
+    << "const R HH = (R)0.70710678118654752440;\n(void)HH;\n"
     << "extern __shared__ __align__(16) unsigned char smem[];\n"
     << "const DevPlan& p = a.p;\nconst int tid = threadIdx.x;\n"
     << "const int64_t vl = blockIdx.x / ps.n_chunks;\nconst int chunk = (int)(blockIdx.x - vl * ps.n_chunks);\n"
     << "const int64_t v = ps.v0 + vl;\nconst VSample vs = decode_vsample(p, v, a.B);\n"
     << "C* tp = reinterpret_cast<C*>(smem);\n"
-    << (bwd ? "C* tl = tp + ((1 << Q) + (1 << Q) / 16 + (1 << Q) / 256);\n" : "")
-    << "const uint32_t tpad = (uint32_t)tid + ((uint32_t)tid >> 4) + ((uint32_t)tid >> 8);\n"
-    << "uint64_t* lut = reinterpret_cast<uint64_t*>(smem + " << L.lut << ");\nuint64_t* hi = lut + 192;\n"
+    << (bwd ? "C* tl = tp + ((1 << Q) + (1 << Q) / 16 + (1 << Q) / 256);\n(void)tl;\n" : "")
+    << "const uint32_t tpad = (uint32_t)tid + ((uint32_t)tid >> 4) + ((uint32_t)tid >> 8);\n(void)tpad;\n"
     << "R* trig = reinterpret_cast<R*>(smem + " << L.trig << ");\n";
-  if (bwd) {
+  o << "const uint64_t ot = 0ull";
+  for (int s2 = 0; s2 < tbits; ++s2) o << " | ((tid & " << (1 << s2) << ") ? " << hex64(gbit[s2]) << " : 0ull)";
+  o << ";\n(void)ot;\n";
+  if (bwd)
     o << "R* dacc = reinterpret_cast<R*>(smem + " << L.extra << ");\n"
       << "for (int i = tid; i < " << P.n_dslots_pass * (L.per_thread ? g.T : nw) << "; i += T) dacc[i] = (R)0;\n";
-  }
-  if (fwd) {
+  if (fwd)
     o << "double* dx = reinterpret_cast<double*>(smem + " << L.extra2 << ");\n"
       << "double* red = dx; double* inv = dx + 32; double* wt = dx + 64; double* sval = dx + 96;\n"
       << "(void)red; (void)inv; (void)wt; (void)sval;\n";
-  }
-  o << "lut_build(ps.local, Q, lut, tid, T);\nload_trig8<R>(a, vs, ps.slots, ps.n_slots, trig, tid, T);\n";
+  o << "load_trig8<R>(a, vs, ps.slots, ps.n_slots, trig, tid, T);\n";
   if (fwd && first) o << "if (p.n_preps > 0) load_prep_values(a, vs, sval, tid, T);\n";
-  if (!bwd && last)
-    o << "__shared__ double gph[2];\nif (a.state && tid == 0) { const double* xr = a.x + vs.b * a.ldx; double f = 0.0; "
-         "for (int k = 0; k < p.n_rz; ++k) f += eval_slot(p, p.rz_slots[k], xr, a.theta, vs.shvar, vs.shval); "
+  if (mode == 0 && last)
+    o << "__shared__ double gph[2];\nif (a.state && tid == 0) { const double* xr = a.x + vs.b * a.ldx; double fph = 0.0; "
+         "for (int k = 0; k < p.n_rz; ++k) fph += eval_slot(p, p.rz_slots[k], xr, a.theta, vs.shvar, vs.shval); "
          "double sg = 1.0; for (int k = 0; k < p.n_rot; ++k) if (cos(0.5 * eval_slot(p, p.rot_slots[k], xr, a.theta, "
-         "vs.shvar, vs.shval)) < 0.0) sg = -sg; "
-         "gph[0] = sg * cos(-0.5 * f); gph[1] = sg * sin(-0.5 * f); }\n";
+         "vs.shvar, vs.shval)) < 0.0) sg = -sg; gph[0] = sg * cos(-0.5 * fph); gph[1] = sg * sin(-0.5 * fph); }\n";
   if (fwd && last)
     o << "if (tid < Q) { double w = 0.0; for (int i = 0; i < p.n_measured; ++i) if (p.measured[i] == ps.local[tid]) "
          "w = (double)(1ull << i); wt[tid] = w; }\n";
-  o << "__syncthreads();\nconst uint64_t ot = lut_off(lut, (uint32_t)tid);\n"
-    << "if (tid < " << g.N << ") hi[tid] = lut_off(lut, (uint32_t)(tid * T));\n";
-  if (fwd && first) o << "if (p.n_preps > 0) prep_norms(a, sval, inv, tid);\n";
-  o << "__syncthreads();\n"
-    << "C* gpsi = reinterpret_cast<C*>(ps.psi) + (size_t)vl * ((size_t)1 << p.n_qubits);\n"
+  o << "__syncthreads();\n";
+  if (fwd && first) o << "if (p.n_preps > 0) prep_norms(a, sval, inv, tid);\n__syncthreads();\n";
+  o << "C* gpsi = reinterpret_cast<C*>(ps.psi) + (size_t)vl * ((size_t)1 << p.n_qubits);\n"
     << "C* glam = ps.lam ? reinterpret_cast<C*>(ps.lam) + (size_t)vl * ((size_t)1 << p.n_qubits) : nullptr;\n"
     << "(void)glam;\n";
   if (fwd) o << "double e = 0.0; (void)e;\n";
@@ -578,72 +651,13 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     for (int i = 0; i < g.N; ++i) o << (i ? ", " : " ") << "l" << i;
     o << ";\n";
   }
-  // forward passes that read ψ: double-buffered tile, cp.async prefetch of
-  // tile t+1 while tile t computes
-  const bool pf = mode == 0 && !first && jit_prefetch();
-  const int cpb = c64 ? 8 : 16;
-  const std::string TNP = "((1 << Q) + (1 << Q) / 16 + (1 << Q) / 256)";
-  auto issue_prefetch = [&](const char* tile_expr, const char* buf) {
-    o << "{ const uint64_t nb = tile_base_of(ps.nonlocal, p.n_qubits - Q, " << tile_expr << ");\n";
-    for (int i = 0; i < g.N; ++i)
-      o << "cp_async<" << cpb << ">(" << buf << " + tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u, gpsi + (nb | ot | hi["
-        << i << "]));\n";
-    o << "}\ncp_commit();\n";
-  };
-  if (pf) {
-    o << "C* const tbuf0 = tp; C* const tbuf1 = tp + " << TNP << ";\n";
-    issue_prefetch("(uint64_t)chunk * ps.tpc", "tbuf0");
+  if (first && fwd) {
+    o << "const int LOCAL[Q] = {";
+    for (int b2 = 0; b2 < g.Q; ++b2) o << (b2 ? "," : "") << P.local[b2];
+    o << "};\n";
   }
-  o << "for (int tt = 0; tt < ps.tpc; ++tt) {\n"
-    << "const uint64_t base = tile_base_of(ps.nonlocal, p.n_qubits - Q, (uint64_t)chunk * ps.tpc + tt);\n";
-  if (pf) {
-    o << "C* const tp = (tt & 1) ? tbuf1 : tbuf0;\n"
-      << "if (tt + 1 < ps.tpc) {\n";
-    issue_prefetch("(uint64_t)chunk * ps.tpc + tt + 1", "((tt & 1) ? tbuf0 : tbuf1)");
-    o << "cp_wait<1>(); } else { cp_wait<0>(); }\n";
-  }
-  // ---- stage in
-  if (fwd && first) {
-    o << "if (a.init) { const double* src = a.init + (a.init_rows > 1 ? v : 0) * ((int64_t)1 << p.n_qubits) * 2;\n"
-      << "  for (uint32_t j = tid; j < (1u << Q); j += T) { const uint64_t g2 = base | lut_off(lut, j); "
-         "tp[jpad(j)].x = (R)src[2 * g2]; tp[jpad(j)].y = (R)src[2 * g2 + 1]; } }\n"
-      << "else if (p.n_preps > 0) { for (uint32_t j = tid; j < (1u << Q); j += T) { const double2 z = "
-         "init_amp(a, sval, inv, base | lut_off(lut, j)); tp[jpad(j)].x = (R)z.x; tp[jpad(j)].y = (R)z.y; } }\n"
-      << "else { for (uint32_t j = tid; j < (1u << Q); j += T) { tp[jpad(j)].x = (R)((base | lut_off(lut, j)) == 0); "
-         "tp[jpad(j)].y = (R)0; } }\n";
-  } else if (!pf) {
-    const bool in_lam = bwd && !fused;
-    for (int i = 0; i < g.N; ++i) o << "p" << i << " = gpsi[base | ot | hi[" << i << "]];\n";
-    if (in_lam)
-      for (int i = 0; i < g.N; ++i) o << "l" << i << " = glam[base | ot | hi[" << i << "]];\n";
-    for (int i = 0; i < g.N; ++i) o << "tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u] = p" << i << ";\n";
-    if (in_lam)
-      for (int i = 0; i < g.N; ++i) o << "tl[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u] = l" << i << ";\n";
-  }
-  o << "__syncthreads();\n";
-  // ---- windows
-  const int nwin = (int)P.wins.size();
-  auto fwd_windows = [&](bool keep_last) {
-    for (int w = 0; w < nwin; ++w) {
-      const WinDev& W = P.wins[w];
-      g.map.assign(g.N, 0);
-      for (int i = 0; i < g.N; ++i) g.map[i] = i;
-      g.pending = false;
-      o << "{ // window " << w << "\n";
-      g.win_tb(W, tbits);
-      g.load_regs(W, "p", "tp");
-      for (int k = W.op0; k < W.op1; ++k) g.apply(P.wops[k], false, false);
-      g.flush_pending(false);
-      if (!(keep_last && w == nwin - 1)) {
-        o << "__syncthreads();\n";
-        g.store_regs(W, "p", "tp");
-        o << "__syncthreads();\n}\n";
-      }
-    }
-  };
-  // In the first pass nothing is written back, so the backward sweep can stop
-  // at the earliest derivative-bearing gate (e.g. the input-encoding layer is
-  // never un-applied).
+
+  // first-pass backward: stop at the earliest derivative-bearing gate
   int stop_op = 0, stop_win = 0;
   if (first) {
     stop_op = (int)P.wops.size();
@@ -652,17 +666,133 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     for (int w = 0; w < nwin; ++w)
       if (P.wins[w].op1 > stop_op) { stop_win = w; break; }
   }
-  auto bwd_windows = [&](bool continue_last) {
+
+  // ---- tile loop
+  o << "for (int tt = 0; tt < ps.tpc; ++tt) {\n"
+    << "const uint64_t t = (uint64_t)chunk * ps.tpc + tt;\n"
+    << "const uint64_t base = 0ull";
+  for (size_t i = 0; i < nonlocal.size(); ++i) o << " | (((t >> " << i << ") & 1ull) << " << nonlocal[i] << ")";
+  o << ";\n";
+
+  bool regs_live = false;  // registers hold the current window's data
+  if (fwd) {
+    // -- stage in ψ
+    const WinDev& W0 = P.wins[0];
+    identity_map();
+    if (first) {
+      o << "{ auto goff_j = [&](uint32_t j) { uint64_t r = 0; for (int b = 0; b < Q; ++b) if ((j >> b) & 1u) "
+           "r |= 1ull << LOCAL[b]; return r; };\n"
+        << "if (a.init) { const double* src = a.init + (a.init_rows > 1 ? v : 0) * ((int64_t)1 << p.n_qubits) * 2;\n"
+        << "  for (uint32_t j = tid; j < (1u << Q); j += T) { const uint64_t g2 = base | goff_j(j); "
+           "tp[jpad(j)].x = (R)src[2 * g2]; tp[jpad(j)].y = (R)src[2 * g2 + 1]; } }\n"
+        << "else if (p.n_preps > 0) { for (uint32_t j = tid; j < (1u << Q); j += T) { const double2 z = "
+           "init_amp(a, sval, inv, base | goff_j(j)); tp[jpad(j)].x = (R)z.x; tp[jpad(j)].y = (R)z.y; } }\n"
+        << "else { for (uint32_t j = tid; j < (1u << Q); j += T) { tp[jpad(j)].x = (R)((base | goff_j(j)) == 0); "
+           "tp[jpad(j)].y = (R)0; } } }\n__syncthreads();\n";
+    } else if (direct_ok(W0)) {
+      o << "{ // window 0: direct load\n";
+      direct_load(W0, false);
+      o << "}\n";
+      regs_live = true;
+    } else {
+      for (int i = 0; i < g.N; ++i) o << "p" << i << " = gpsi[base | ot | " << hex64(hi_off(i)) << "];\n";
+      for (int i = 0; i < g.N; ++i) o << "tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u] = p" << i << ";\n";
+      o << "__syncthreads();\n";
+    }
+    // -- forward windows
+    for (int w = 0; w < nwin; ++w) {
+      const WinDev& W = P.wins[w];
+      o << "{ // window " << w << "\n";
+      g.win_tb(W, tbits);
+      if (!(w == 0 && regs_live)) {
+        identity_map();
+        g.load_regs(W, "p", "tp");
+      }
+      g.pending = false;
+      for (int k = W.op0; k < W.op1; ++k) g.apply(P.wops[k], false, false);
+      g.flush_pending(false);
+      if (w < nwin - 1) {
+        o << "__syncthreads();\n";
+        g.store_regs(W, "p", "tp");
+        o << "__syncthreads();\n}\n";
+      }
+    }
+    // the last window's block is still open here
+    const WinDev& WL = P.wins[nwin - 1];
+    if (fused) {
+      // readout + λ = wψ on the registers (tile index of logical register i =
+      // deposit(i, R) | deposit(tid, S))
+      const std::vector<int> S = Sbits(WL), R = Rbits(WL);
+      o << "{ double wb = 0.0; for (int i = 0; i < p.n_measured; ++i) if ((base >> p.measured[i]) & 1ull) "
+           "wb += (double)(1ull << i);\n";
+      for (int s2 = 0; s2 < tbits; ++s2) o << "if ((tid >> " << s2 << ") & 1) wb += wt[" << S[s2] << "];\n";
+      for (int i = 0; i < g.N; ++i) {
+        o << "{ const double w = wb";
+        for (int r = 0; r < g.RB; ++r)
+          if (i >> r & 1) o << " + wt[" << R[r] << "]";
+        const std::string P_ = g.P(i), L_ = g.L(i);
+        o << "; e += w * (double)(" << P_ << ".x * " << P_ << ".x + " << P_ << ".y * " << P_ << ".y); " << L_
+          << ".x = (R)w * " << P_ << ".x; " << L_ << ".y = (R)w * " << P_ << ".y; }\n";
+      }
+      o << "}\n";
+      regs_live = true;  // continue into the backward windows (block stays open)
+    } else if (last) {
+      o << "__syncthreads();\n";
+      g.store_regs(WL, "p", "tp");
+      o << "__syncthreads();\n}\n";
+      o << "{ double wb = 0.0; for (int i = 0; i < p.n_measured; ++i) if ((base >> p.measured[i]) & 1ull) "
+           "wb += (double)(1ull << i);\n"
+        << "for (int bb = 0; bb < Q - " << g.RB << "; ++bb) if ((tid >> bb) & 1) wb += wt[bb];\n";
+      for (int i = 0; i < g.N; ++i) {
+        o << "{ double w = wb";
+        for (int b2 = 0; b2 < g.RB; ++b2)
+          if (i >> b2 & 1) o << " + wt[" << (g.Q - g.RB + b2) << "]";
+        o << "; const C z = tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u]; const uint64_t g2 = base | ot | "
+          << hex64(hi_off(i)) << "; e += w * (double)(z.x * z.x + z.y * z.y); gpsi[g2] = z;"
+          << " if (glam) { C y; y.x = (R)w * z.x; y.y = (R)w * z.y; glam[g2] = y; }"
+          << " if (a.state) { double* dst = a.state + v * ((int64_t)1 << p.n_qubits) * 2; "
+             "dst[2 * g2] = (double)z.x * gph[0] - (double)z.y * gph[1]; "
+             "dst[2 * g2 + 1] = (double)z.x * gph[1] + (double)z.y * gph[0]; } }\n";
+      }
+      o << "}\n";
+    } else if (direct_ok(WL)) {
+      direct_store(WL, false);
+      o << "}\n";
+    } else {
+      o << "__syncthreads();\n";
+      g.store_regs(WL, "p", "tp");
+      o << "__syncthreads();\n}\n";
+      for (int i = 0; i < g.N; ++i)
+        o << "gpsi[base | ot | " << hex64(hi_off(i)) << "] = tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u];\n";
+    }
+  }
+  if (bwd) {
+    const WinDev& WL = P.wins[nwin - 1];
+    if (!fused) {
+      identity_map();
+      if (direct_ok(WL)) {
+        o << "{ // window " << nwin - 1 << " (adjoint): direct load\n";
+        g.win_tb(WL, tbits);
+        direct_load(WL, true);
+        regs_live = true;
+      } else {
+        for (int i = 0; i < g.N; ++i) o << "p" << i << " = gpsi[base | ot | " << hex64(hi_off(i)) << "];\n";
+        for (int i = 0; i < g.N; ++i) o << "l" << i << " = glam[base | ot | " << hex64(hi_off(i)) << "];\n";
+        for (int i = 0; i < g.N; ++i) o << "tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u] = p" << i << ";\n";
+        for (int i = 0; i < g.N; ++i) o << "tl[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u] = l" << i << ";\n";
+        o << "__syncthreads();\n";
+        regs_live = false;
+      }
+    }
     for (int wi = 0; wi < nwin; ++wi) {
       const int w = nwin - 1 - wi;
       if (first && w < stop_win) break;
       const WinDev& W = P.wins[w];
-      const bool cont = continue_last && wi == 0;   // registers already hold window w
+      const bool cont = wi == 0 && regs_live;  // block already open, registers hold window w
       if (!cont) {
-        g.map.assign(g.N, 0);
-        for (int i = 0; i < g.N; ++i) g.map[i] = i;
         o << "{ // window " << w << " (adjoint)\n";
         g.win_tb(W, tbits);
+        identity_map();
         g.load_regs(W, "p", "tp");
         g.load_regs(W, "l", "tl");
       }
@@ -670,69 +800,37 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       const int lo = std::max<int>(W.op0, first ? stop_op : 0);
       for (int k = W.op1 - 1; k >= lo; --k) {
         g.dot(P.wops[k], L.per_thread, nw);
-        if (!(first && k == lo && P.wops[k].dl >= 0 && k == stop_op)) g.apply(P.wops[k], true, true);
+        if (!(first && k == stop_op && P.wops[k].dl >= 0)) g.apply(P.wops[k], true, true);
       }
       g.flush_pending(true);
-      const bool need_store = !(first && (wi == nwin - 1 || w == stop_win));
-      if (need_store) {
-        o << "__syncthreads();\n";
-        g.store_regs(W, "p", "tp");
-        g.store_regs(W, "l", "tl");
-        o << "__syncthreads();\n";
+      const bool end = first ? (wi == nwin - 1 || w == stop_win) : (w == 0);
+      if (end) {
+        if (!first) {
+          if (direct_ok(W)) {
+            direct_store(W, true);
+          } else {
+            o << "__syncthreads();\n";
+            g.store_regs(W, "p", "tp");
+            g.store_regs(W, "l", "tl");
+            o << "__syncthreads();\n";
+            for (int i = 0; i < g.N; ++i) {
+              o << "gpsi[base | ot | " << hex64(hi_off(i)) << "] = tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u];\n";
+              o << "glam[base | ot | " << hex64(hi_off(i)) << "] = tl[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u];\n";
+            }
+          }
+        }
+        o << "}\n";
+        break;
       }
-      o << "}\n";
-    }
-  };
-  if (!fused) {
-    if (fwd) fwd_windows(false);
-    else bwd_windows(false);
-  } else {
-    fwd_windows(true);
-    // readout + λ = wψ on the last window's registers (tile index of logical
-    // register i = deposit(i, R) | deposit(tid, S))
-    const WinDev& W = P.wins[nwin - 1];
-    o << "{ double wb = 0.0; for (int i = 0; i < p.n_measured; ++i) if ((base >> p.measured[i]) & 1ull) "
-         "wb += (double)(1ull << i);\n";
-    for (int s2 = 0; s2 < tbits; ++s2)
-      o << "if ((tid >> " << s2 << ") & 1) wb += wt[" << Gen::bit_of(W.ps[s2]) << "];\n";
-    for (int i = 0; i < g.N; ++i) {
-      o << "{ const double w = wb";
-      for (int b2 = 0; b2 < g.RB; ++b2)
-        if (i >> b2 & 1) o << " + wt[" << Gen::bit_of(W.pr[b2]) << "]";
-      const std::string P_ = g.P(i), L_ = g.L(i);
-      o << "; e += w * (double)(" << P_ << ".x * " << P_ << ".x + " << P_ << ".y * " << P_ << ".y); "
-        << L_ << ".x = (R)w * " << P_ << ".x; " << L_ << ".y = (R)w * " << P_ << ".y; }\n";
-    }
-    o << "}\n";
-    bwd_windows(true);
-  }
-  // ---- stage out
-  if (!bwd && last) {
-    o << "{ double wb = 0.0; for (int i = 0; i < p.n_measured; ++i) if ((base >> p.measured[i]) & 1ull) "
-         "wb += (double)(1ull << i);\n"
-      << "for (int bb = 0; bb < Q - " << g.RB << "; ++bb) if ((tid >> bb) & 1) wb += wt[bb];\n";
-    for (int i = 0; i < g.N; ++i) {
-      o << "{ double w = wb";
-      for (int b2 = 0; b2 < g.RB; ++b2)
-        if (i >> b2 & 1) o << " + wt[" << (g.Q - g.RB + b2) << "]";
-      o << "; const C z = tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u]; const uint64_t g2 = base | ot | hi[" << i
-        << "]; e += w * (double)(z.x * z.x + z.y * z.y); gpsi[g2] = z;"
-        << " if (glam) { C y; y.x = (R)w * z.x; y.y = (R)w * z.y; glam[g2] = y; }"
-        << " if (a.state) { double* dst = a.state + v * ((int64_t)1 << p.n_qubits) * 2; "
-           "dst[2 * g2] = (double)z.x * gph[0] - (double)z.y * gph[1]; "
-           "dst[2 * g2 + 1] = (double)z.x * gph[1] + (double)z.y * gph[0]; } }\n";
-    }
-    o << "}\n";
-  } else if (!(bwd && first)) {
-    for (int i = 0; i < g.N; ++i) {
-      o << "gpsi[base | ot | hi[" << i << "]] = tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u];\n";
-      if (bwd) o << "glam[base | ot | hi[" << i << "]] = tl[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u];\n";
+      o << "__syncthreads();\n";
+      g.store_regs(W, "p", "tp");
+      g.store_regs(W, "l", "tl");
+      o << "__syncthreads();\n}\n";
     }
   }
   o << "__syncthreads();\n}\n";  // tile loop
-  if (fwd && last) {
+  if (fwd && last)
     o << "e = block_sum<R>(e, red, tid, T);\nif (tid == 0) ps.rpart[vl * ps.n_chunks + chunk] = e;\n";
-  }
   if (bwd) {
     const int stride = L.per_thread ? g.T : nw;
     o << "__syncthreads();\nfor (int i = tid; i < " << P.n_dslots_pass << "; i += T) { double s = 0.0; "
