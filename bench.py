@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--precision", default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--backend", default="nccl", help="process-group backend (gloo: dry runs of the "
+                    "multi-rank path with several ranks on one device)")
     return ap.parse_args()
 
 
@@ -194,9 +196,13 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if a.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(a.backend)
     cfg = a.config
     n, d, P, B0, prec = wl.CONFIGS[cfg]
     prec = a.precision or prec

@@ -501,7 +501,9 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
       }
     }
     gates.swap(g2);
-    const int RB = reg_bits_for(d->precision);
+    int RB = reg_bits_for(d->precision);
+    if (const char* e = std::getenv("HQ_REG_BITS")) RB = std::max(2, std::min(4, std::atoi(e)));
+    pl->reg_bits = RB;
     if (pl->tile_bits - RB < 5 || pl->tile_bits - RB > 10) {
       delete pl;
       return fail(HQ_E_CONFIG, "tile must hold 2^9..2^14 amplitudes");
@@ -558,7 +560,12 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
 
   if (!pl->onchip) {
     std::string why;
-    if (hq::jit_build(pl, why) != HQ_OK) {
+    const hq_status js = hq::jit_build(pl, why);
+    if (js != HQ_OK && pl->reg_bits != reg_bits_for(d->precision)) {
+      delete pl;
+      return fail(HQ_E_CONFIG, "HQ_REG_BITS needs the specialised kernels: " + why);
+    }
+    if (js != HQ_OK) {
       pl->jit.ok = false;
       pl->jit.why = why;
       if (!(std::getenv("HQ_JIT") && std::getenv("HQ_JIT")[0] == '0'))
@@ -574,7 +581,8 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
   if (pl->onchip) {
     os << " path=onchip smem=" << hq::onchip_smem_bytes(pl);
   } else {
-    os << " path=stream kernels=" << (pl->jit.ok ? "jit" : "generic") << " tile_bits=" << pl->tile_bits << " passes=" << pl->passes.size() << " [";
+    os << " path=stream kernels=" << (pl->jit.ok ? "jit" : "generic") << " tile_bits=" << pl->tile_bits
+       << " reg_bits=" << pl->reg_bits << " passes=" << pl->passes.size() << " [";
     for (size_t i = 0; i < pl->passes.size(); ++i)
       os << (i ? "," : "") << pl->passes[i].n_dops << "/" << pl->passes[i].wins.size() << "w";
     os << "]";
@@ -585,9 +593,9 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
         for (int b : pl->passes[i].local) os << b << ",";
         for (const auto& w : pl->passes[i].wins) {
           os << "\n   win ops=" << (w.op1 - w.op0) << " R=";
-          for (int k = 0; k < RBITS(d->precision); ++k) os << bit(w.pr[k]) << ",";
+          for (int k = 0; k < pl->reg_bits; ++k) os << bit(w.pr[k]) << ",";
           os << " S=";
-          for (int k = 0; k < pl->tile_bits - RBITS(d->precision); ++k) os << bit(w.ps[k]) << ",";
+          for (int k = 0; k < pl->tile_bits - pl->reg_bits; ++k) os << bit(w.ps[k]) << ",";
         }
       }
     }

@@ -479,7 +479,7 @@ size_t a16(size_t v) { return (v + 15) & ~(size_t)15; }
 // shared-memory layout of generated kernels (host and generator agree)
 JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd, bool fused) {
   const Pass& P = pl->passes[i];
-  const int RB = pl->precision == HQ_C64 ? 4 : 3;
+  const int RB = pl->reg_bits;
   const int T = 1 << (pl->tile_bits - RB);
   const size_t amp = pl->precision == HQ_C64 ? 8 : 16, rsz = amp / 2;
   JitLayout L{};
@@ -516,7 +516,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   const Pass& P = pl->passes[pi];
   const bool c64 = pl->precision == HQ_C64;
   Gen g;
-  g.RB = c64 ? 4 : 3;
+  g.RB = pl->reg_bits;
   g.N = 1 << g.RB;
   g.Q = pl->tile_bits;
   g.T = 1 << (g.Q - g.RB);
@@ -972,7 +972,7 @@ cudaError_t jit_launch_pass(const hq_plan_s* pl, int i, int mode, const KArgs& a
   const bool bwd = mode != 0;
   const JitLayout L = jit_layout(pl, i, bwd, mode == 2);
   cudaKernel_t k = mode == 0 ? pl->jit.fwd[i] : (mode == 1 ? pl->jit.bwd[i] : pl->jit.fused);
-  const int RB = pl->precision == HQ_C64 ? 4 : 3;
+  const int RB = pl->reg_bits;
   const int T = 1 << (pl->tile_bits - RB);
   KArgs ac = a;
   JPass pc = ps;

@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(256, 2) k_wbwd(KArgs a, SArgs sa) {
 }
 
 // ---------------------------------------------------------------------------
-static int rb_of(const hq_plan_s* pl) { return pl->precision == HQ_C64 ? RBits<float>::v : RBits<double>::v; }
+static int rb_of(const hq_plan_s* pl) { return pl->reg_bits; }
 
 static WPass wpass(const hq_plan_s* pl, int i) {
   const Pass& P = pl->passes[i];
