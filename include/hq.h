@@ -144,6 +144,21 @@ hq_status hq_state(hq_plan plan, const double* x, int64_t ldx, const double* the
                    int64_t batch, const double* init, int64_t init_rows, double* state,
                    void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- SHOT_SAMPLING (qsim.py:222-248, qnn.py:27-32) ------------------------ */
+
+/* Per row of `state` ([rows, 2^n, 2] complex128, device): marginal over
+ * `measured` (host array, outcome bit i = measured[i]), np.cumsum order,
+ * `shots` draws u_s = Philox4x64-10(key=[seed, s]).random(), outcome =
+ * searchsorted(cum, u, side="right") clamped.  Outputs (device, optional):
+ * counts [rows, 2^m] uint64, expectation [rows] = Σ outcome / shots. */
+size_t hq_sample_workspace_bytes(int64_t rows, int32_t n_qubits, int32_t n_measured);
+hq_status hq_sample(const double* state, int64_t rows, int32_t n_qubits, const int32_t* measured,
+                    int32_t n_measured, int64_t shots, uint64_t seed, uint64_t* counts,
+                    double* expectation, void* workspace, size_t workspace_bytes, void* stream);
+
+/* u_s for s in [shot0, shot0 + count): the per-shot uniform stream of shot_rng (qsim.py:222-224) */
+hq_status hq_shot_uniforms(uint64_t seed, int64_t shot0, int64_t count, double* out, void* stream);
+
 /* ---- introspection / measurement ---------------------------------------- */
 
 typedef struct {

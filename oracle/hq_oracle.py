@@ -363,3 +363,42 @@ def qae_builder(trash_qubits, total_qubits):
         return c
     build.n_params = 6 * t + 3 * t * (t - 1)
     return build
+
+
+# ---------------------------------------------------------------------------
+# SHOT_SAMPLING (qsim.py:222-248, qnn.py:27-32, 117-118)
+_M0, _M1 = 0xD2E7470EE14C6C93, 0xCA5A826395121157
+_W0, _W1 = 0x9E3779B97F4A7C15, 0xBB67AE8584CAA73B
+_MASK = (1 << 64) - 1
+
+
+def philox_uniform(seed, shot):
+    """First draw of np.random.Generator(np.random.Philox(key=[seed, shot])).random():
+    Philox4x64-10, counter (1,0,0,0) (bumped before the first block), key
+    (seed, shot), output word 0 >> 11 times 2^-53."""
+    c = [1, 0, 0, 0]
+    k = [seed & _MASK, shot & _MASK]
+    for r in range(10):
+        if r:
+            k = [(k[0] + _W0) & _MASK, (k[1] + _W1) & _MASK]
+        p0, p1 = _M0 * c[0], _M1 * c[2]
+        c = [(p1 >> 64) ^ c[1] ^ k[0], p1 & _MASK, (p0 >> 64) ^ c[3] ^ k[1], p0 & _MASK]
+    return (c[0] >> 11) * (1.0 / 9007199254740992.0)
+
+
+def measure_shots(psi, n, qubits, shots, seed):
+    """Counts dict {bitstring: count} (qsim.py:236-248)."""
+    cum = np.cumsum(probabilities(psi, n, qubits))
+    tally = {}
+    for s in range(shots):
+        u = philox_uniform(seed, s)
+        idx = min(int(np.searchsorted(cum, u, side="right")), len(cum) - 1)
+        key = format(idx, f"0{len(qubits)}b")
+        tally[key] = tally.get(key, 0) + 1
+    return tally
+
+
+def shot_expectation(circuit, shots, seed):
+    qubits = list(circuit.measured_qubits) or list(range(circuit.n_qubits))
+    counts = measure_shots(simulate(circuit), circuit.n_qubits, qubits, shots, seed)
+    return sum(int(k, 2) * c for k, c in counts.items()) / shots

@@ -21,7 +21,8 @@ KIND_CODE = {"H": 0, "X": 1, "Y": 2, "Z": 3, "RX": 4, "RY": 5, "RZ": 6, "CNOT": 
 
 EXPORTS = ("hq_abi_version", "hq_last_error", "hq_plan_create", "hq_plan_destroy",
            "hq_plan_describe", "hq_workspace_bytes", "hq_forward", "hq_vjp", "hq_state",
-           "hq_stats", "hq_profile_enable", "hq_profile_read")
+           "hq_stats", "hq_profile_enable", "hq_profile_read", "hq_sample_workspace_bytes", "hq_sample",
+           "hq_shot_uniforms")
 K_CLASSES = ("onchip", "pass_fwd", "pass_bwd", "other")
 
 
@@ -95,6 +96,13 @@ def lib():
     h.hq_profile_enable.restype = ctypes.c_int
     h.hq_profile_read.argtypes = [_P, ctypes.POINTER(HqProfile)]
     h.hq_profile_read.restype = ctypes.c_int
+    h.hq_sample_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32]
+    h.hq_sample_workspace_bytes.restype = ctypes.c_size_t
+    h.hq_sample.argtypes = [_P, ctypes.c_int64, ctypes.c_int32, _P, ctypes.c_int32, ctypes.c_int64,
+                            ctypes.c_uint64, _P, _P, _P, ctypes.c_size_t, _P]
+    h.hq_sample.restype = ctypes.c_int
+    h.hq_shot_uniforms.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, _P, _P]
+    h.hq_shot_uniforms.restype = ctypes.c_int
     if h.hq_abi_version() != 1:
         raise NativeError(f"libhq ABI {h.hq_abi_version()} != 1")
     _lib = h

@@ -379,3 +379,99 @@ def run_per_sample(builder, xd, pd, want_x, want_p, precision, shift, grad_scale
         torch = _torch()
         jac = torch.from_numpy(jac).to(f"cuda:{torch.cuda.current_device()}")
     return out, jac, {"plan": None, "path": "per_sample"}
+
+
+# ------------------------------------------------------------------------------
+# SHOT_SAMPLING (qsim.py:222-248): device sampling of final states
+def sample_states(states, n_qubits: int, measured, shots: int, seed: int, want_counts: bool = False):
+    """states: cuda f64 [rows, 2^n, 2] -> (expectation [rows] cuda, counts [rows, 2^m] | None)."""
+    torch = _torch()
+    L = nat.lib()
+    rows = int(states.shape[0])
+    m = len(measured)
+    meas = (ctypes.c_int32 * m)(*[int(q) for q in measured])
+    dev = states.device
+    E = torch.empty(rows, dtype=torch.float64, device=dev)
+    counts = torch.empty((rows, 1 << m), dtype=torch.int64, device=dev) if want_counts else None
+    nb = int(L.hq_sample_workspace_bytes(rows, n_qubits, m))
+    ws = torch.empty(nb, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    status = L.hq_sample(_ptr(states.contiguous()), rows, n_qubits, meas, m, int(shots), int(seed) & (2**64 - 1),
+                         _ptr(counts), _ptr(E), _ptr(ws), nb, st)
+    nat.check(status, "sample")
+    return E, counts
+
+
+def shot_uniforms(seed: int, shot0: int, count: int):
+    torch = _torch()
+    out = torch.empty(count, dtype=torch.float64, device="cuda")
+    nat.check(nat.lib().hq_shot_uniforms(int(seed), int(shot0), int(count), _ptr(out),
+                                         torch.cuda.current_stream().cuda_stream), "uniforms")
+    return out
+
+
+def run_batch_shots(builder, xd, pd, want_x, want_p, shots, seed, precision="c128", shift=math.pi / 2,
+                    grad_scale=0.5, measured_override=None, counts_outcome=None, row_budget_bytes=2 << 30):
+    """Reference SHOT_SAMPLING semantics on device: every evaluation (base rows
+    and the two-point shifted ones) samples ``shots`` outcomes with the same
+    seed (qnn.py:117-118, 35-52).  Params ride along as extra per-row inputs so
+    shifted-θ rows are ordinary rows of one plan.
+
+    Returns (E [B] numpy, jac [B, d+P] cuda | None); with ``counts_outcome`` the
+    value is counts[outcome]/shots instead of the mean outcome (QAELayer)."""
+    torch = _torch()
+    B, d = xd.shape
+    P = pd.shape[0]
+    tape, ok = tr.trace(builder, xd, pd)
+    if ok and tape.preps:
+        _check_preps(tape, xd, pd)
+    ext = np.hstack([xd, np.broadcast_to(pd, (B, P))])
+    rows = [ext]
+    index = []
+    if want_x or want_p:
+        for j in range(d + P):
+            if (j < d and not want_x) or (j >= d and not want_p):
+                continue
+            for sgn in (1.0, -1.0):
+                r = ext.copy()
+                r[:, j] = ext[:, j] + sgn * shift
+                rows.append(r)
+                index.append((j, sgn))
+    allrows = np.concatenate(rows)
+    measured = measured_override or (tape.measured if ok else None)
+    if not ok:
+        # per-circuit path (data-dependent / non-affine builders)
+        from .qnn import build_circuit
+        circuits = [build_circuit(builder, r[:d], r[d:]) for r in allrows]
+        vals = []
+        for c in circuits:
+            amps = simulate_circuit(c, None, precision)
+            stt = torch.from_numpy(np.stack([amps.real, amps.imag], -1)[None]).to("cuda")
+            meas = measured_override or ([int(q) for q in c.measured_qubits] or list(range(c.n_qubits)))
+            E, cnt = sample_states(stt, c.n_qubits, meas, shots, seed, counts_outcome is not None)
+            vals.append(float((cnt[0, counts_outcome].double() / shots).item()) if counts_outcome is not None
+                        else float(E.item()))
+        vals = np.array(vals)
+    else:
+        plan = _global_cache.get(tape, d + P, 0, precision, None, shift, grad_scale)
+        n = tape.n_qubits
+        per = max(1, int(row_budget_bytes // (16 << n)))
+        vals = np.empty(allrows.shape[0])
+        pt = torch.zeros(1, dtype=torch.float64, device=f"cuda:{plan.device}")
+        for r0 in range(0, allrows.shape[0], per):
+            chunk = torch.from_numpy(np.ascontiguousarray(allrows[r0:r0 + per])).to(f"cuda:{plan.device}")
+            stt = plan.state(chunk, pt)
+            E, cnt = sample_states(stt, n, measured, shots, seed, counts_outcome is not None)
+            v = (cnt[:, counts_outcome].double() / shots) if counts_outcome is not None else E
+            vals[r0:r0 + chunk.shape[0]] = v.cpu().numpy()
+    out = vals[:B]
+    jac = None
+    if index:
+        J = np.zeros((B, d + P))
+        for k in range(0, len(index), 2):
+            j = index[k][0]
+            ep = vals[B * (1 + k):B * (2 + k)]
+            em = vals[B * (2 + k):B * (3 + k)]
+            J[:, j] = (ep - em) * grad_scale
+        jac = torch.from_numpy(J).to("cuda")
+    return out, jac

@@ -141,6 +141,46 @@ def qae_cases():
          grad_p=layer.params.grad)
 
 
+def shots_case():
+    # measure_shots counts (qsim.py:236-248) and SHOT_SAMPLING layer outputs
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from conftest import random_circuit
+    rng = np.random.default_rng(99)
+    kinds, q0, q1, ang, starts, nq, shots, seeds = [], [], [], [], [0], [], [], []
+    extra = {}
+    for k in range(6):
+        n = int(rng.integers(1, 5))
+        c = random_circuit(rng, n, int(rng.integers(1, 12)))
+        for op in c.ops:
+            kinds.append(op.kind)
+            q0.append(op.targets[0])
+            q1.append(op.targets[1] if len(op.targets) > 1 else -1)
+            ang.append(np.nan if op.angle is None else op.angle)
+        starts.append(len(kinds))
+        nq.append(n)
+        S, seed = int(rng.integers(50, 400)), int(rng.integers(0, 1000))
+        shots.append(S)
+        seeds.append(seed)
+        counts = rq.measure_shots(rq.simulate(c), list(range(n)), S, seed)
+        extra[f"keys{k}"] = np.array(list(counts.keys()))
+        extra[f"vals{k}"] = np.array(list(counts.values()))
+
+    def h_ry(inputs, params):
+        c = rq.Circuit(1)
+        c.h(0)
+        c.ry(0, inputs[0])
+        c.measure(0)
+        return c
+    th = np.linspace(-2, 2, 7)
+    layer = QuantumLayer(h_ry, 0, machine_type="shot_sampling", shots=137, seed=5)
+    x = Tensor(th.reshape(-1, 1), requires_grad=True, dtype=np.float64)
+    out = layer(x)
+    backward(tsum(out))
+    save("shots", kinds=np.array(kinds), q0=np.array(q0), q1=np.array(q1), angle=np.array(ang),
+         starts=np.array(starts), n_qubits=np.array(nq), shots=np.array(shots), seed=np.array(seeds),
+         layer_theta=th, layer_out=out.numpy()[:, 0], layer_grad=x.grad[:, 0], **extra)
+
+
 def embedding_case():
     rng = np.random.default_rng(5)
     vecs = [np.array([0.2, -0.4, 0.4, -0.8]), np.array([3, 1, -4, 1, -5, 9, -2, 6], float),
@@ -157,7 +197,7 @@ def embedding_case():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "cfg4", "random", "reupload", "qae", "embed"]
+    which = sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "cfg4", "random", "reupload", "qae", "embed", "shots"]
     if "cfg1" in which:
         layer_case("cfg1", "cfg1", 16, True)
     if "cfg2" in which:
@@ -174,3 +214,5 @@ if __name__ == "__main__":
         qae_cases()
     if "embed" in which:
         embedding_case()
+    if "shots" in which:
+        shots_case()

@@ -313,3 +313,24 @@ def test_cfg4_full_size_norm_and_round_trip():
         st = plan.state(torch.tensor(x, device="cuda"), torch.tensor(th, device="cuda"))
         z = st[..., 0].double() ** 2 + st[..., 1].double() ** 2
         np.testing.assert_allclose(z.sum(dim=1).cpu().numpy(), 1.0, atol=tol)
+
+
+def test_layer_builds_output_in_the_inputs_graph_module():
+    """A hyqnet Tensor in -> a hyqnet Tensor out, with GraphNodes of hyqnet's
+    own module (qnn._boundary).  A stand-in module plays hyqnet.tensor here
+    (the reference itself is not available on the GPU box)."""
+    import sys
+    import types
+    from paper_2301_03251_b200 import tensor as ours
+    fake = types.ModuleType("fake_hyqnet_tensor")
+    src = open(ours.__file__).read().replace("from .errors import", "from paper_2301_03251_b200.errors import")
+    exec(compile(src, "fake_hyqnet_tensor", "exec"), fake.__dict__)
+    sys.modules["fake_hyqnet_tensor"] = fake
+    for obj in (fake.Tensor, fake.GraphNode):
+        obj.__module__ = "fake_hyqnet_tensor"
+    layer = QuantumLayer(h_ry, n_params=0)
+    x = fake.Tensor(np.array([[0.4], [1.1]]), requires_grad=True, dtype=np.float64)
+    out = layer(x)
+    assert type(out) is fake.Tensor and all(type(nd) is fake.GraphNode for nd in out.nodes)
+    fake.backward(fake.tsum(out))
+    np.testing.assert_allclose(x.grad[:, 0], np.cos([0.4, 1.1]) / 2, atol=1e-12)

@@ -115,3 +115,33 @@ def test_cfg4_forward_and_jacobian_entries():
         tm = g["theta"].copy(); tm[j] -= np.pi / 2
         val = (O.run(b, g["x"][0], tp) - O.run(b, g["x"][0], tm)) * 0.5
         assert val == pytest.approx(g["jac0"][k], abs=1e-12)
+
+
+def test_philox_stream_matches_numpy():
+    # the reference's shot_rng (qsim.py:222-224) is numpy's Philox; pin the restatement
+    for seed in (0, 3, 7, 2**40 + 5):
+        for shot in (0, 1, 2, 99, 4000, 2**33):
+            want = np.random.Generator(np.random.Philox(key=[seed, shot])).random()
+            assert O.philox_uniform(seed, shot) == want
+
+
+def test_shot_counts_golden():
+    g = golden("shots")
+    for k, c in enumerate(_circuits_from(g)):
+        counts = O.measure_shots(O.simulate(c), c.n_qubits, list(range(c.n_qubits)), int(g["shots"][k]),
+                                 int(g["seed"][k]))
+        want = {str(key): int(v) for key, v in zip(g[f"keys{k}"], g[f"vals{k}"])}
+        assert counts == want
+    assert list(g["layer_out"]) == [O.shot_expectation(_hry(t), 137, 5) for t in g["layer_theta"]]
+
+
+def _hry(theta):
+    c = O.Circuit(1)
+    c.h(0)
+    c.ry(0, theta)
+    c.measure(0)
+    return c
+
+
+def _circuits_from(g):
+    return _circuits({k: g[k] for k in ("kinds", "q0", "q1", "angle", "starts", "n_qubits")})
