@@ -321,13 +321,12 @@ def test_layer_builds_output_in_the_inputs_graph_module():
     (the reference itself is not available on the GPU box)."""
     import sys
     import types
-    from paper_2301_03251_b200 import tensor as ours
+    import importlib
+    ours = importlib.import_module("paper_2301_03251_b200.tensor")
     fake = types.ModuleType("fake_hyqnet_tensor")
     src = open(ours.__file__).read().replace("from .errors import", "from paper_2301_03251_b200.errors import")
+    sys.modules["fake_hyqnet_tensor"] = fake      # dataclasses resolve annotations via sys.modules
     exec(compile(src, "fake_hyqnet_tensor", "exec"), fake.__dict__)
-    sys.modules["fake_hyqnet_tensor"] = fake
-    for obj in (fake.Tensor, fake.GraphNode):
-        obj.__module__ = "fake_hyqnet_tensor"
     layer = QuantumLayer(h_ry, n_params=0)
     x = fake.Tensor(np.array([[0.4], [1.1]]), requires_grad=True, dtype=np.float64)
     out = layer(x)
