@@ -482,7 +482,7 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
   if (!pl->onchip) {
     pl->dops.clear();
     pl->tile_bits = tile_bits_for(d->precision);
-    if (tb_env) pl->tile_bits = std::max(3, std::min(pl->tile_bits, std::atoi(tb_env)));
+    if (tb_env) pl->tile_bits = std::max(3, std::min(14, std::atoi(tb_env)));
     if (n <= pl->tile_bits) pl->tile_bits = n - 1;
     if (pl->tile_bits < 2) {
       delete pl;

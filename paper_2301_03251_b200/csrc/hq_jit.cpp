@@ -453,6 +453,9 @@ __device__ __forceinline__ void cp_async(void* dst, const void* src) {
   if (BYTES == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
   else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
 }
+__device__ __forceinline__ void prefetch_l2_64(const void* p) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], 64;\n" ::"l"(p));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -603,7 +606,9 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   auto hi_off = [&](int i) { return goff((uint32_t)(i * g.T)); };
 
   // ---- header / prologue
-  o << "extern \"C\" __global__ void __launch_bounds__(" << g.T << ", " << (bwd ? 2 : 3) << ") "
+  // occupancy hint: ~128 registers per thread for ψ+λ kernels, ~80 for forward
+  const int minb = std::max(1, 65536 / (g.T * (bwd ? 128 : 80)));
+  o << "extern \"C\" __global__ void __launch_bounds__(" << g.T << ", " << minb << ") "
     << (fused ? "hq_fb" : (bwd ? "hq_b" : "hq_f")) << pi << "(const hq::KArgs a, const hq::JPass ps) {\n"
     << "using namespace hq;\n"
     << "typedef " << g.R() << " R; typedef " << (c64 ? "float2" : "double2") << " C;\n"
@@ -674,6 +679,28 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   for (size_t i = 0; i < nonlocal.size(); ++i) o << " | (((t >> " << i << ") & 1ull) << " << nonlocal[i] << ")";
   o << ";\n";
 
+  // L2 prefetch of the next tile: 2^(Q-f) contiguous runs of 2^f amplitudes
+  // (64 B) per vector, spread over the threads; issued once the current tile's
+  // loads are out, so the next tile's loads hit L2 instead of HBM.
+  // measured slower on cfg4 (3,276 vs 3,533 samples/s): opt-in via HQ_L2PF=1
+  const bool l2pf = std::getenv("HQ_L2PF") && !(fwd && first && !bwd);
+  auto emit_prefetch = [&](bool lam) {
+    if (!l2pf) return;
+    const int runs = 1 << (g.Q - f);
+    o << "if (tt + 1 < ps.tpc) { const uint64_t t2 = t + 1; const uint64_t base2 = 0ull";
+    for (size_t i = 0; i < nonlocal.size(); ++i) o << " | (((t2 >> " << i << ") & 1ull) << " << nonlocal[i] << ")";
+    o << ";\n";
+    for (int r0 = 0; r0 < runs; r0 += g.T) {
+      // run index = tid + r0; its tile index bits start at bit f
+      o << "{ const uint32_t run = (uint32_t)tid + " << r0 << "u; if (run < " << runs << "u) { uint64_t off = 0ull;";
+      for (int bb = 0; bb < g.Q - f; ++bb) o << " if ((run >> " << bb << ") & 1u) off |= " << hex64(gbit[f + bb]) << ";";
+      o << " prefetch_l2_64(gpsi + (base2 | off));";
+      if (lam) o << " prefetch_l2_64(glam + (base2 | off));";
+      o << " } }\n";
+    }
+    o << "}\n";
+  };
+
   bool regs_live = false;  // registers hold the current window's data
   if (fwd) {
     // -- stage in ψ
@@ -699,6 +726,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       for (int i = 0; i < g.N; ++i) o << "tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u] = p" << i << ";\n";
       o << "__syncthreads();\n";
     }
+    if (!first) emit_prefetch(false);
     // -- forward windows
     for (int w = 0; w < nwin; ++w) {
       const WinDev& W = P.wins[w];
@@ -784,6 +812,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         regs_live = false;
       }
     }
+    if (!fused) emit_prefetch(true);
     for (int wi = 0; wi < nwin; ++wi) {
       const int w = nwin - 1 - wi;
       if (first && w < stop_win) break;
