@@ -140,6 +140,7 @@ struct Gen {
   std::ostringstream o;
   int RB, N, T, Q;
   bool c64, exact;
+  bool packed = false;  // complex64: FFMA2/FMUL2 on (re, im) pairs
   std::vector<int> map;  // logical register index -> variable number
   bool pending = false;  // a per-thread phase is pending in this window
 
@@ -167,6 +168,10 @@ struct Gen {
   }
 
   void cmul_amp(const std::string& a, const std::string& x, const std::string& y) {
+    if (packed) {
+      o << a << " = cmul2f(" << a << ", " << x << ", " << y << ");\n";
+      return;
+    }
     o << "{ const C z_ = " << a << "; " << a << ".x = z_.x * " << x << " - z_.y * " << y << "; "
       << a << ".y = z_.x * " << y << " + z_.y * " << x << "; }\n";
   }
@@ -198,8 +203,12 @@ struct Gen {
           for (int i = 0; i < N; ++i) {
             if (i >> k & 1) continue;
             const std::string A = nm(i, lam), B = nm(i | 1 << k, lam);
-            o << "{ const C a_ = " << A << ", b_ = " << B << "; " << A << ".x = HH * (a_.x + b_.x); " << A
-              << ".y = HH * (a_.y + b_.y); " << B << ".x = HH * (a_.x - b_.x); " << B << ".y = HH * (a_.y - b_.y); }\n";
+            if (packed)
+              o << "{ const C a_ = " << A << ", b_ = " << B << "; " << A << " = mul2(add2(a_, b_), bc2(HH)); " << B
+                << " = mul2(fma2(bc2(-1.f), b_, a_), bc2(HH)); }\n";
+            else
+              o << "{ const C a_ = " << A << ", b_ = " << B << "; " << A << ".x = HH * (a_.x + b_.x); " << A
+                << ".y = HH * (a_.y + b_.y); " << B << ".x = HH * (a_.x - b_.x); " << B << ".y = HH * (a_.y - b_.y); }\n";
           }
         });
         break;
@@ -232,7 +241,11 @@ struct Gen {
           for (int i = 0; i < N; ++i) {
             if (i >> k & 1) continue;
             const std::string A = nm(i, lam), B = nm(i | 1 << k, lam);
-            if (op.kind == HQ_GATE_RY) {
+            if (op.kind == HQ_GATE_RY && packed) {
+              // (a, b) -> R(phi)(a, b) on both components at once: 3 FFMA2
+              o << A << " = fma2(bc2(t_), " << B << ", " << A << "); " << B << " = fma2(bc2(u_), " << A << ", " << B
+                << "); " << A << " = fma2(bc2(t_), " << B << ", " << A << ");\n";
+            } else if (op.kind == HQ_GATE_RY) {
               // (a, b) -> R(phi)(a, b) componentwise
               shear(A + ".x", B + ".x", "t_", "u_");
               shear(A + ".y", B + ".y", "t_", "u_");
@@ -250,8 +263,11 @@ struct Gen {
         if (is_reg(a)) {
           sets([&](bool lam) {
             for (int i = 0; i < N; ++i)
-              if (i >> a & 1) o << nm(i, lam) << ".x = -" << nm(i, lam) << ".x; " << nm(i, lam) << ".y = -"
-                                << nm(i, lam) << ".y;\n";
+              if (i >> a & 1) {
+                if (packed) o << nm(i, lam) << " = mul2(" << nm(i, lam) << ", bc2(-1.f));\n";
+                else o << nm(i, lam) << ".x = -" << nm(i, lam) << ".x; " << nm(i, lam) << ".y = -" << nm(i, lam)
+                       << ".y;\n";
+              }
           });
         } else {
           pend(cond(a), "-1", "0");
@@ -352,45 +368,88 @@ struct Gen {
     if (op.dl < 0) return;
     const int a = op.a;
     o << "{ R acc_ = (R)0;\n";
-    auto imd = [&](int i) {
-      return "acc_ = fmaf_r(" + L(i) + ".x, " + P(i) + ".y, acc_); acc_ = fmaf_r(-" + L(i) + ".y, " + P(i) + ".x, acc_)";
-    };
-    switch (op.kind) {
-      case HQ_GATE_RY:
-        for (int i = 0; i < N; ++i) {
-          if (i >> a & 1) continue;
-          const int j = i | 1 << a;
-          o << "acc_ = fmaf_r(" << L(j) << ".x, " << P(i) << ".x, acc_); acc_ = fmaf_r(" << L(j) << ".y, " << P(i)
-            << ".y, acc_); acc_ = fmaf_r(-" << L(i) << ".x, " << P(j) << ".x, acc_); acc_ = fmaf_r(-" << L(i)
-            << ".y, " << P(j) << ".y, acc_);\n";
+    if (packed) {
+      // componentwise FFMA2 accumulators, combined once at the end:
+      //   Re-dot Σ(λ.x ψ.x + λ.y ψ.y) = ap.x + ap.y ;  Im-dot Σ(λ.x ψ.y − λ.y ψ.x) = ai.x − ai.y
+      o << "C ap_ = make_float2(0.f, 0.f), am_ = ap_, ai_ = ap_;\n";
+      switch (op.kind) {
+        case HQ_GATE_RY:   // Re(λ1* ψ0) − Re(λ0* ψ1)
+          for (int i = 0; i < N; ++i) {
+            if (i >> a & 1) continue;
+            const int j = i | 1 << a;
+            o << "ap_ = fma2(" << L(j) << ", " << P(i) << ", ap_); am_ = fma2(" << L(i) << ", " << P(j) << ", am_);\n";
+          }
+          o << "acc_ = (ap_.x + ap_.y) - (am_.x + am_.y);\n";
+          break;
+        case HQ_GATE_RX:   // Im(λ0* ψ1) + Im(λ1* ψ0)
+          for (int i = 0; i < N; ++i) {
+            if (i >> a & 1) continue;
+            const int j = i | 1 << a;
+            o << "ai_ = fma2(" << L(i) << ", swp2(" << P(j) << "), ai_); ai_ = fma2(" << L(j) << ", swp2(" << P(i)
+              << "), ai_);\n";
+          }
+          o << "acc_ = ai_.x - ai_.y;\n";
+          break;
+        case HQ_GATE_RZ: case HQ_GATE_CR: {
+          int M = 0;
+          std::string cnd;
+          std::vector<int> codes = {a};
+          if (op.kind == HQ_GATE_CR) codes.push_back(op.b);
+          for (int code : codes) {
+            if (is_reg(code)) M |= 1 << code;
+            else cnd += (cnd.empty() ? "" : " && ") + cond(code);
+          }
+          for (int i = 0; i < N; ++i)
+            if ((i & M) == M) o << "ai_ = fma2(" << L(i) << ", swp2(" << P(i) << "), ai_);\n";
+          o << "acc_ = ai_.x - ai_.y;\n";
+          if (!cnd.empty()) o << "if (!(" << cnd << ")) acc_ = (R)0;\n";
+          o << "acc_ *= (R)-2;\n";
+          break;
         }
-        break;
-      case HQ_GATE_RX:
-        for (int i = 0; i < N; ++i) {
-          if (i >> a & 1) continue;
-          const int j = i | 1 << a;
-          o << "acc_ = fmaf_r(" << L(i) << ".x, " << P(j) << ".y, acc_); acc_ = fmaf_r(-" << L(i) << ".y, " << P(j)
-            << ".x, acc_); acc_ = fmaf_r(" << L(j) << ".x, " << P(i) << ".y, acc_); acc_ = fmaf_r(-" << L(j)
-            << ".y, " << P(i) << ".x, acc_);\n";
-        }
-        break;
-      case HQ_GATE_RZ: case HQ_GATE_CR: {
-        int M = 0;
-        std::string cnd;
-        std::vector<int> codes = {a};
-        if (op.kind == HQ_GATE_CR) codes.push_back(op.b);
-        for (int code : codes) {
-          if (is_reg(code)) M |= 1 << code;
-          else cnd += (cnd.empty() ? "" : " && ") + cond(code);
-        }
-        for (int i = 0; i < N; ++i)
-          if ((i & M) == M) o << imd(i) << ";\n";
-        if (!cnd.empty()) o << "if (!(" << cnd << ")) acc_ = (R)0;\n";
-        o << "acc_ *= (R)-2;\n";
-        break;
+        default:
+          break;
       }
-      default:
-        break;
+    } else {
+      auto imd = [&](int i) {
+        return "acc_ = fmaf_r(" + L(i) + ".x, " + P(i) + ".y, acc_); acc_ = fmaf_r(-" + L(i) + ".y, " + P(i) + ".x, acc_)";
+      };
+      switch (op.kind) {
+        case HQ_GATE_RY:
+          for (int i = 0; i < N; ++i) {
+            if (i >> a & 1) continue;
+            const int j = i | 1 << a;
+            o << "acc_ = fmaf_r(" << L(j) << ".x, " << P(i) << ".x, acc_); acc_ = fmaf_r(" << L(j) << ".y, " << P(i)
+              << ".y, acc_); acc_ = fmaf_r(-" << L(i) << ".x, " << P(j) << ".x, acc_); acc_ = fmaf_r(-" << L(i)
+              << ".y, " << P(j) << ".y, acc_);\n";
+          }
+          break;
+        case HQ_GATE_RX:
+          for (int i = 0; i < N; ++i) {
+            if (i >> a & 1) continue;
+            const int j = i | 1 << a;
+            o << "acc_ = fmaf_r(" << L(i) << ".x, " << P(j) << ".y, acc_); acc_ = fmaf_r(-" << L(i) << ".y, " << P(j)
+              << ".x, acc_); acc_ = fmaf_r(" << L(j) << ".x, " << P(i) << ".y, acc_); acc_ = fmaf_r(-" << L(j)
+              << ".y, " << P(i) << ".x, acc_);\n";
+          }
+          break;
+        case HQ_GATE_RZ: case HQ_GATE_CR: {
+          int M = 0;
+          std::string cnd;
+          std::vector<int> codes = {a};
+          if (op.kind == HQ_GATE_CR) codes.push_back(op.b);
+          for (int code : codes) {
+            if (is_reg(code)) M |= 1 << code;
+            else cnd += (cnd.empty() ? "" : " && ") + cond(code);
+          }
+          for (int i = 0; i < N; ++i)
+            if ((i & M) == M) o << imd(i) << ";\n";
+          if (!cnd.empty()) o << "if (!(" << cnd << ")) acc_ = (R)0;\n";
+          o << "acc_ *= (R)-2;\n";
+          break;
+        }
+        default:
+          break;
+      }
     }
     if (per_thread) {
       o << "dacc[" << op.dl << " * T + tid] += acc_; }\n";
@@ -447,6 +506,29 @@ typedef unsigned long size_t;
 const char* kHelpers = R"(
 namespace hq {
 __device__ __forceinline__ uint32_t jpad(uint32_t j) { return j + (j >> 4) + (j >> 8); }
+// packed FP32x2 (sm_100 FFMA2/FMUL2/FADD2): a complex64 amplitude is one
+// 64-bit register pair; half swaps and sign patterns fold into operand modifiers
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b)); return r; }
+__device__ __forceinline__ float2 up2(unsigned long long r) {
+  float2 v; asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r)); return v; }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)), "l"(pk2(c.x, c.y)));
+  return up2(r); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return up2(r); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return up2(r); }
+__device__ __forceinline__ float2 bc2(float s) { return make_float2(s, s); }
+__device__ __forceinline__ float2 swp2(float2 a) { return make_float2(a.y, a.x); }
+// z * (c + i s) = z*c + swap(z)*(-s, s)
+__device__ __forceinline__ float2 cmul2f(float2 z, float c, float s) {
+  return fma2(swp2(z), make_float2(-s, s), mul2(z, bc2(c))); }
 template <int BYTES>
 __device__ __forceinline__ void cp_async(void* dst, const void* src) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
@@ -524,6 +606,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   g.Q = pl->tile_bits;
   g.T = 1 << (g.Q - g.RB);
   g.c64 = c64;
+  g.packed = c64 && !std::getenv("HQ_NO_F32X2");
   g.exact = false;  // hq_state corrects the dropped RZ phases / rotation signs in the last pass
   const int tbits = g.Q - g.RB;
   const int n = pl->n_qubits;
