@@ -104,7 +104,14 @@ Layout layout_for(const hq_plan_s* pl, int64_t B, int32_t flags, bool need_state
     const int64_t n_tiles = 1ll << (pl->n_qubits - pl->tile_bits);
     const bool adj = jac && pl->n_adj > 0;
     const int64_t per = (int64_t)amp << pl->n_qubits;
-    int64_t cs = ws_budget() / (per * (adj ? 2 : 1));
+    // adjoint with specialised kernels: forward passes keep ψ checkpoints so the
+    // backward passes never write ψ back (3 instead of 4 vector transfers)
+    const int np = (int)pl->passes.size();
+    const char* nock = std::getenv("HQ_NO_CKPT");
+    if (adj && pl->jit.ok && np >= 2 && !(nock && nock[0] == '1') &&
+        (int64_t)np * per <= ws_budget())
+      L.sws.ckpt = np - 1;
+    int64_t cs = ws_budget() / (per * (L.sws.ckpt ? L.sws.ckpt + 1 : (adj ? 2 : 1)));
     if (cs < 1) cs = 1;
     if (cs > L.V) cs = L.V;
     if (cs < 1) cs = 1;
@@ -115,7 +122,7 @@ Layout layout_for(const hq_plan_s* pl, int64_t B, int32_t flags, bool need_state
     L.sws.chunk_samples = cs;
     L.sws.n_chunks = (int32_t)nc;
     L.n_parts = (int32_t)nc;
-    L.psi = off; off = align_up(off + (size_t)cs * per);
+    L.psi = off; off = align_up(off + (size_t)cs * per * (L.sws.ckpt ? L.sws.ckpt : 1));
     if (adj) { L.lam = off; off = align_up(off + (size_t)cs * per); }
     L.rpart = off; off = align_up(off + (size_t)cs * nc * 8);
   }

@@ -673,12 +673,16 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     }
     o << "}\n";
   };
+  // ψ goes to gout (the next checkpoint, or in place); backward passes with
+  // checkpoints have gout == null and store only λ
   auto direct_store = [&](const WinDev& W, bool lam) {
     o << "{\n";
     emit_tw(W);
-    for (int i = 0; i < g.N; ++i) {
-      o << "gpsi[base | tw | " << hex64(reg_goff(W, i)) << "] = p" << g.map[i] << ";\n";
-      if (lam) o << "glam[base | tw | " << hex64(reg_goff(W, i)) << "] = l" << g.map[i] << ";\n";
+    if (lam) o << "if (gout) {\n";
+    for (int i = 0; i < g.N; ++i) o << "gout[base | tw | " << hex64(reg_goff(W, i)) << "] = p" << g.map[i] << ";\n";
+    if (lam) {
+      o << "}\n";
+      for (int i = 0; i < g.N; ++i) o << "glam[base | tw | " << hex64(reg_goff(W, i)) << "] = l" << g.map[i] << ";\n";
     }
     o << "}\n";
   };
@@ -728,8 +732,9 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   o << "__syncthreads();\n";
   if (fwd && first) o << "if (p.n_preps > 0) prep_norms(a, sval, inv, tid);\n__syncthreads();\n";
   o << "C* gpsi = reinterpret_cast<C*>(ps.psi) + (size_t)vl * ((size_t)1 << p.n_qubits);\n"
+    << "C* gout = ps.psi_out ? reinterpret_cast<C*>(ps.psi_out) + (size_t)vl * ((size_t)1 << p.n_qubits) : nullptr;\n"
     << "C* glam = ps.lam ? reinterpret_cast<C*>(ps.lam) + (size_t)vl * ((size_t)1 << p.n_qubits) : nullptr;\n"
-    << "(void)glam;\n";
+    << "(void)glam; (void)gout; (void)gpsi;\n";
   if (fwd) o << "double e = 0.0; (void)e;\n";
   o << "C";
   for (int i = 0; i < g.N; ++i) o << (i ? ", " : " ") << "p" << i;
@@ -859,7 +864,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         for (int b2 = 0; b2 < g.RB; ++b2)
           if (i >> b2 & 1) o << " + wt[" << (g.Q - g.RB + b2) << "]";
         o << "; const C z = tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u]; const uint64_t g2 = base | ot | "
-          << hex64(hi_off(i)) << "; e += w * (double)(z.x * z.x + z.y * z.y); gpsi[g2] = z;"
+          << hex64(hi_off(i)) << "; e += w * (double)(z.x * z.x + z.y * z.y); gout[g2] = z;"
           << " if (glam) { C y; y.x = (R)w * z.x; y.y = (R)w * z.y; glam[g2] = y; }"
           << " if (a.state) { double* dst = a.state + v * ((int64_t)1 << p.n_qubits) * 2; "
              "dst[2 * g2] = (double)z.x * gph[0] - (double)z.y * gph[1]; "
@@ -874,7 +879,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       g.store_regs(WL, "p", "tp");
       o << "__syncthreads();\n}\n";
       for (int i = 0; i < g.N; ++i)
-        o << "gpsi[base | ot | " << hex64(hi_off(i)) << "] = tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u];\n";
+        o << "gout[base | ot | " << hex64(hi_off(i)) << "] = tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u];\n";
     }
   }
   if (bwd) {
@@ -926,7 +931,8 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
             g.store_regs(W, "l", "tl");
             o << "__syncthreads();\n";
             for (int i = 0; i < g.N; ++i) {
-              o << "gpsi[base | ot | " << hex64(hi_off(i)) << "] = tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u];\n";
+              o << "if (gout) gout[base | ot | " << hex64(hi_off(i)) << "] = tp[tpad + " << Gen::pad((uint32_t)(i * g.T))
+                << "u];\n";
               o << "glam[base | ot | " << hex64(hi_off(i)) << "] = tl[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u];\n";
             }
           }

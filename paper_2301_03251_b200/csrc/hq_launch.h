@@ -14,6 +14,7 @@ struct StreamWs {
   double* rpart = nullptr;    // [chunk_samples, n_chunks]
   int64_t chunk_samples = 0;  // virtual samples resident per launch
   int32_t n_chunks = 1;       // CTAs per sample per pass
+  int32_t ckpt = 0;           // >0: forward passes write ψ checkpoints C_1..C_ckpt out of place
 };
 
 struct LaunchIn {

@@ -62,7 +62,8 @@ struct JPass {
   int32_t n_chunks, tpc; // CTAs per sample, tiles per CTA
   int32_t first, last;   // pass index is 0 / the last one
   int32_t n_slots, n_dl;
-  void* psi;
+  void* psi;               // ψ read by this pass (sample vl at + vl·2^n)
+  void* psi_out;           // ψ written by this pass, or null (backward passes with checkpoints)
   void* lam;
   double* rpart;
   const int32_t* slots;    // pass-local slot list

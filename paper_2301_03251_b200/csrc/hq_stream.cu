@@ -362,6 +362,7 @@ static JPass jpass(const hq_plan_s* pl, int i, const SArgs& sa) {
   j.n_slots = (int32_t)P.slots.size();
   j.n_dl = P.n_dslots_pass;
   j.psi = sa.psi;
+  j.psi_out = sa.psi;
   j.lam = sa.lam;
   j.rpart = sa.rpart;
   j.slots = pl->d_pass_slots + P.first_slotlist;
@@ -423,18 +424,28 @@ static cudaError_t run_stream_t(const hq_plan_s* pl, const KArgs& a, const Strea
       // specialised kernels + adjoint: the last forward pass and its backward
       // run fused (λ = wψ in registers, no ψ/λ round trip through HBM)
       const bool fuse = pl->jit.ok && adj && pl->jit.fused != nullptr;
+      // checkpoint k (ψ after forward pass k-1) of this launch's samples
+      const bool ck = adj && ws.ckpt > 0;
+      auto ckpt_ptr = [&](int k) -> void* {
+        return static_cast<char*>(ws.psi) + (size_t)(k - 1) * (size_t)ws.chunk_samples *
+                                                 sizeof(typename Cx<R>::T) * ((size_t)1 << n);
+      };
       for (int i = 0; i < np; ++i) {
         sa.ps = wpass(pl, i);
         const size_t sm = wsmem(pl, i, false);
         if (fuse && i == np - 1) {
-          ProfScope prof(pl, st, HQ_K_PASS_BWD, vec * ((i == 0 ? 0 : 1) + (i == 0 ? 0 : 2)));
-          cudaError_t e = jit_launch_pass(pl, i, 2, a, jpass(pl, i, sa), (unsigned)(nv * n_chunks), st);
+          JPass jp = jpass(pl, i, sa);
+          if (ck) { jp.psi = ckpt_ptr(i); jp.psi_out = nullptr; }
+          ProfScope prof(pl, st, HQ_K_PASS_BWD, vec * ((i == 0 ? 0 : 1) + (i == 0 ? 0 : (ck ? 1 : 2))));
+          cudaError_t e = jit_launch_pass(pl, i, 2, a, jp, (unsigned)(nv * n_chunks), st);
           if (e != cudaSuccess) return e;
           continue;
         }
         ProfScope prof(pl, st, HQ_K_PASS_FWD, vec * ((i == 0 ? 0 : 1) + 1 + ((i == np - 1 && adj) ? 1 : 0)));
         if (pl->jit.ok) {
-          cudaError_t e = jit_launch_pass(pl, i, 0, a, jpass(pl, i, sa), (unsigned)(nv * n_chunks), st);
+          JPass jp = jpass(pl, i, sa);
+          if (ck) { jp.psi = i == 0 ? nullptr : ckpt_ptr(i); jp.psi_out = ckpt_ptr(i + 1); }
+          cudaError_t e = jit_launch_pass(pl, i, 0, a, jp, (unsigned)(nv * n_chunks), st);
           if (e != cudaSuccess) return e;
         } else if (exact) {
           k_wfwd<R, true><<<(unsigned)(nv * n_chunks), T, sm, st>>>(a, sa);
@@ -451,9 +462,11 @@ static cudaError_t run_stream_t(const hq_plan_s* pl, const KArgs& a, const Strea
         for (int i = fuse ? np - 2 : np - 1; i >= 0; --i) {
           sa.ps = wpass(pl, i);
           const size_t sm = wsmem(pl, i, true);
-          ProfScope prof(pl, st, HQ_K_PASS_BWD, vec * (2 + (i == 0 ? 0 : 2)));
+          ProfScope prof(pl, st, HQ_K_PASS_BWD, vec * (2 + (i == 0 ? 0 : (ck ? 1 : 2))));
           if (pl->jit.ok) {
-            cudaError_t e = jit_launch_pass(pl, i, 1, a, jpass(pl, i, sa), (unsigned)(nv * n_chunks), st);
+            JPass jp = jpass(pl, i, sa);
+            if (ck) { jp.psi = ckpt_ptr(i + 1); jp.psi_out = nullptr; }
+            cudaError_t e = jit_launch_pass(pl, i, 1, a, jp, (unsigned)(nv * n_chunks), st);
             if (e != cudaSuccess) return e;
           } else {
             k_wbwd<R><<<(unsigned)(nv * n_chunks), T, sm, st>>>(a, sa);
