@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <map>
 #include <mutex>
 #include <thread>
 #include <atomic>
@@ -363,95 +364,105 @@ struct Gen {
     }
   }
 
-  // derivative dot at (ψ_k, λ_k) for ops with dl >= 0 (see hq_window.cuh for the formulas)
-  void dot(const WOp& op, bool per_thread, int nw) {
+  // derivative dot at (ψ_k, λ_k) for ops with dl >= 0 (see hq_window.cuh for the formulas).
+  // The products are spread over kChains independent accumulators so the
+  // FMA latency chain is N/kChains long instead of N; dl < reg_acc adds into
+  // the register accumulator da<dl> (kept across the tile loop), otherwise
+  // into the shared-memory partials.
+  static constexpr int kChains = 4;
+  void dot(const WOp& op, bool per_thread, int nw, int reg_acc) {
     if (op.dl < 0) return;
     const int a = op.a;
     o << "{ R acc_ = (R)0;\n";
+    // term list: (sign, λ register, ψ register, kind) with kind 0 = Re(λ*ψ), 1 = Im(λ*ψ)
+    struct Term { int sg, li, pi, im; };
+    std::vector<Term> terms;
+    std::string cnd;
+    bool neg2 = false;
+    switch (op.kind) {
+      case HQ_GATE_RY:   // Re(λ1* ψ0) − Re(λ0* ψ1)
+        for (int i = 0; i < N; ++i) {
+          if (i >> a & 1) continue;
+          const int j = i | 1 << a;
+          terms.push_back({+1, j, i, 0});
+          terms.push_back({-1, i, j, 0});
+        }
+        break;
+      case HQ_GATE_RX:   // Im(λ0* ψ1) + Im(λ1* ψ0)
+        for (int i = 0; i < N; ++i) {
+          if (i >> a & 1) continue;
+          const int j = i | 1 << a;
+          terms.push_back({+1, i, j, 1});
+          terms.push_back({+1, j, i, 1});
+        }
+        break;
+      case HQ_GATE_RZ: case HQ_GATE_CR: {
+        int M = 0;
+        std::vector<int> codes = {a};
+        if (op.kind == HQ_GATE_CR) codes.push_back(op.b);
+        for (int code : codes) {
+          if (is_reg(code)) M |= 1 << code;
+          else cnd += (cnd.empty() ? "" : " && ") + cond(code);
+        }
+        for (int i = 0; i < N; ++i)
+          if ((i & M) == M) terms.push_back({+1, i, i, 1});
+        neg2 = true;
+        break;
+      }
+      default:
+        break;
+    }
+    const int nt = (int)terms.size();
+    const int nc = std::min(kChains, std::max(1, nt));
     if (packed) {
       // componentwise FFMA2 accumulators, combined once at the end:
-      //   Re-dot Σ(λ.x ψ.x + λ.y ψ.y) = ap.x + ap.y ;  Im-dot Σ(λ.x ψ.y − λ.y ψ.x) = ai.x − ai.y
-      o << "C ap_ = make_float2(0.f, 0.f), am_ = ap_, ai_ = ap_;\n";
-      switch (op.kind) {
-        case HQ_GATE_RY:   // Re(λ1* ψ0) − Re(λ0* ψ1)
-          for (int i = 0; i < N; ++i) {
-            if (i >> a & 1) continue;
-            const int j = i | 1 << a;
-            o << "ap_ = fma2(" << L(j) << ", " << P(i) << ", ap_); am_ = fma2(" << L(i) << ", " << P(j) << ", am_);\n";
-          }
-          o << "acc_ = (ap_.x + ap_.y) - (am_.x + am_.y);\n";
-          break;
-        case HQ_GATE_RX:   // Im(λ0* ψ1) + Im(λ1* ψ0)
-          for (int i = 0; i < N; ++i) {
-            if (i >> a & 1) continue;
-            const int j = i | 1 << a;
-            o << "ai_ = fma2(" << L(i) << ", swp2(" << P(j) << "), ai_); ai_ = fma2(" << L(j) << ", swp2(" << P(i)
-              << "), ai_);\n";
-          }
-          o << "acc_ = ai_.x - ai_.y;\n";
-          break;
-        case HQ_GATE_RZ: case HQ_GATE_CR: {
-          int M = 0;
-          std::string cnd;
-          std::vector<int> codes = {a};
-          if (op.kind == HQ_GATE_CR) codes.push_back(op.b);
-          for (int code : codes) {
-            if (is_reg(code)) M |= 1 << code;
-            else cnd += (cnd.empty() ? "" : " && ") + cond(code);
-          }
-          for (int i = 0; i < N; ++i)
-            if ((i & M) == M) o << "ai_ = fma2(" << L(i) << ", swp2(" << P(i) << "), ai_);\n";
-          o << "acc_ = ai_.x - ai_.y;\n";
-          if (!cnd.empty()) o << "if (!(" << cnd << ")) acc_ = (R)0;\n";
-          o << "acc_ *= (R)-2;\n";
-          break;
+      //   Re(λ*ψ) = λ.x ψ.x + λ.y ψ.y -> acc.x + acc.y ;  Im(λ*ψ) = λ.x ψ.y − λ.y ψ.x -> acc.x − acc.y
+      // (Im terms multiply λ by swp2(ψ)); chains hold one (sign, kind) class each
+      std::map<std::pair<int, int>, std::vector<int>> cls;
+      for (int k = 0; k < nt; ++k) cls[{terms[k].sg, terms[k].im}].push_back(k);
+      std::string comb;
+      int id = 0;
+      for (auto& kv : cls) {
+        const int sg = kv.first.first, im = kv.first.second;
+        const auto& ks = kv.second;
+        const int ncl = std::max(1, std::min<int>(nc / (int)cls.size(), (int)ks.size() / 4));
+        for (int c = 0; c < ncl; ++c) o << "C k" << id << "_" << c << " = make_float2(0.f, 0.f);\n";
+        for (size_t m = 0; m < ks.size(); ++m) {
+          const Term& t = terms[ks[m]];
+          const std::string acc = "k" + std::to_string(id) + "_" + std::to_string(m % ncl);
+          o << acc << " = fma2(" << L(t.li) << ", " << (im ? "swp2(" + P(t.pi) + ")" : P(t.pi)) << ", " << acc << ");\n";
         }
-        default:
-          break;
+        std::string sum = "k" + std::to_string(id) + "_0";
+        for (int c = 1; c < ncl; ++c) {
+          o << sum << " = add2(" << sum << ", k" << id << "_" << c << ");\n";
+        }
+        comb += std::string(sg > 0 ? " + " : " - ") + "(" + sum + ".x " + (im ? "-" : "+") + " " + sum + ".y)";
+        ++id;
       }
+      o << "acc_ = (R)0" << comb << ";\n";
     } else {
-      auto imd = [&](int i) {
-        return "acc_ = fmaf_r(" + L(i) + ".x, " + P(i) + ".y, acc_); acc_ = fmaf_r(-" + L(i) + ".y, " + P(i) + ".x, acc_)";
-      };
-      switch (op.kind) {
-        case HQ_GATE_RY:
-          for (int i = 0; i < N; ++i) {
-            if (i >> a & 1) continue;
-            const int j = i | 1 << a;
-            o << "acc_ = fmaf_r(" << L(j) << ".x, " << P(i) << ".x, acc_); acc_ = fmaf_r(" << L(j) << ".y, " << P(i)
-              << ".y, acc_); acc_ = fmaf_r(-" << L(i) << ".x, " << P(j) << ".x, acc_); acc_ = fmaf_r(-" << L(i)
-              << ".y, " << P(j) << ".y, acc_);\n";
-          }
-          break;
-        case HQ_GATE_RX:
-          for (int i = 0; i < N; ++i) {
-            if (i >> a & 1) continue;
-            const int j = i | 1 << a;
-            o << "acc_ = fmaf_r(" << L(i) << ".x, " << P(j) << ".y, acc_); acc_ = fmaf_r(-" << L(i) << ".y, " << P(j)
-              << ".x, acc_); acc_ = fmaf_r(" << L(j) << ".x, " << P(i) << ".y, acc_); acc_ = fmaf_r(-" << L(j)
-              << ".y, " << P(i) << ".x, acc_);\n";
-          }
-          break;
-        case HQ_GATE_RZ: case HQ_GATE_CR: {
-          int M = 0;
-          std::string cnd;
-          std::vector<int> codes = {a};
-          if (op.kind == HQ_GATE_CR) codes.push_back(op.b);
-          for (int code : codes) {
-            if (is_reg(code)) M |= 1 << code;
-            else cnd += (cnd.empty() ? "" : " && ") + cond(code);
-          }
-          for (int i = 0; i < N; ++i)
-            if ((i & M) == M) o << imd(i) << ";\n";
-          if (!cnd.empty()) o << "if (!(" << cnd << ")) acc_ = (R)0;\n";
-          o << "acc_ *= (R)-2;\n";
-          break;
-        }
-        default:
-          break;
+      for (int c = 0; c < nc; ++c) o << "R q" << c << "_ = (R)0;\n";
+      for (int k = 0; k < nt; ++k) {
+        const Term& t = terms[k];
+        const std::string acc = "q" + std::to_string(k % nc) + "_";
+        const std::string s1 = t.sg > 0 ? "" : "-";
+        const std::string s2 = t.sg > 0 ? "-" : "";
+        if (!t.im)
+          o << acc << " = fmaf_r(" << s1 << L(t.li) << ".x, " << P(t.pi) << ".x, " << acc << "); " << acc << " = fmaf_r("
+            << s1 << L(t.li) << ".y, " << P(t.pi) << ".y, " << acc << ");\n";
+        else
+          o << acc << " = fmaf_r(" << s1 << L(t.li) << ".x, " << P(t.pi) << ".y, " << acc << "); " << acc << " = fmaf_r("
+            << s2 << L(t.li) << ".y, " << P(t.pi) << ".x, " << acc << ");\n";
       }
+      o << "acc_ = q0_";
+      for (int c = 1; c < nc; ++c) o << " + q" << c << "_";
+      o << ";\n";
     }
-    if (per_thread) {
+    if (!cnd.empty()) o << "if (!(" << cnd << ")) acc_ = (R)0;\n";
+    if (neg2) o << "acc_ *= (R)-2;\n";
+    if (op.dl < reg_acc) {
+      o << "da" << op.dl << " += acc_; }\n";
+    } else if (per_thread) {
       o << "dacc[" << op.dl << " * T + tid] += acc_; }\n";
     } else {
       o << "acc_ = warp_sum_r(acc_); if ((tid & 31) == 0) dacc[" << op.dl << " * " << nw
@@ -760,6 +771,16 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       if (P.wins[w].op1 > stop_op) { stop_win = w; break; }
   }
 
+  // derivative accumulators in registers across the tile loop when the pass
+  // has few enough derivative slots (shared-memory partials otherwise)
+  int reg_acc = 0;
+  if (bwd) {
+    int cap = 24;
+    if (const char* e = std::getenv("HQ_REG_ACC")) cap = std::atoi(e);
+    if (P.n_dslots_pass <= cap && L.per_thread) reg_acc = P.n_dslots_pass;
+    for (int k = 0; k < reg_acc; ++k) o << "R da" << k << " = (R)0;\n";
+  }
+
   // ---- tile loop
   o << "for (int tt = 0; tt < ps.tpc; ++tt) {\n"
     << "const uint64_t t = (uint64_t)chunk * ps.tpc + tt;\n"
@@ -916,7 +937,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       g.pending = false;
       const int lo = std::max<int>(W.op0, first ? stop_op : 0);
       for (int k = W.op1 - 1; k >= lo; --k) {
-        g.dot(P.wops[k], L.per_thread, nw);
+        g.dot(P.wops[k], L.per_thread, nw, reg_acc);
         if (!(first && k == stop_op && P.wops[k].dl >= 0)) g.apply(P.wops[k], true, true);
       }
       g.flush_pending(true);
@@ -951,9 +972,12 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     o << "e = block_sum<R>(e, red, tid, T);\nif (tid == 0) ps.rpart[vl * ps.n_chunks + chunk] = e;\n";
   if (bwd) {
     const int stride = L.per_thread ? g.T : nw;
-    o << "__syncthreads();\nfor (int i = tid; i < " << P.n_dslots_pass << "; i += T) { double s = 0.0; "
-      << "for (int k = 0; k < " << stride << "; ++k) s += (double)dacc[i * " << stride << " + k]; "
-      << "a.dpart[((int64_t)v * p.n_adj + ps.dlist[i]) * a.n_parts + chunk] = s; }\n";
+    for (int k = 0; k < reg_acc; ++k) o << "dacc[" << k << " * T + tid] = da" << k << ";\n";
+    // one warp per slot: lanes sum strided partials in double, then a shuffle tree
+    o << "__syncthreads();\n{ const int lane_ = tid & 31;\nfor (int i = tid >> 5; i < " << P.n_dslots_pass
+      << "; i += " << nw << ") { double s = 0.0; for (int k = lane_; k < " << stride
+      << "; k += 32) s += (double)dacc[i * " << stride << " + k]; s = warp_sum<double>(s); "
+      << "if (lane_ == 0) a.dpart[((int64_t)v * p.n_adj + ps.dlist[i]) * a.n_parts + chunk] = s; } }\n";
   }
   o << "}\n";
   return o.str();
