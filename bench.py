@@ -54,6 +54,16 @@ def parse():
     return ap.parse_args()
 
 
+def fp_peak(prec):
+    """Measured FMA throughput (tools/fma_peak.cu -> profiles/r01_fma_peak.json)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "r01_fma_peak.json")) as f:
+            m = json.load(f)
+        return (m["fp32_ffma2_tflops"] if prec == "c64" else m["fp64_dfma_tflops"]), "measured (tools/fma_peak.cu)"
+    except Exception:
+        return (75.0 if prec == "c64" else 37.0), "datasheet"
+
+
 def peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -293,6 +303,23 @@ def run_ours(a):
                 "all_passes": {"achieved": alg_all / t_all / 1e9, "frac": alg_all / t_all / 1e9 / peak,
                                "algorithmic_bytes_per_sample": alg_all / (B * a.steps)},
                 "all_kernels_ms_per_step": {k: v["ms"] / a.steps for k, v in prof.items()}}
+        # SURVEY.md §8(d)'s per-unit model over all pass kernels: bytes assume
+        # S = d·ceil(n/13) sweeps (this plan executes S above, fewer bytes than
+        # the model), flops F = 2^n·(18R + 8D + 6) against the measured FFMA2 peak
+        R, D, _ = wl.gate_counts(cfg)
+        depth = 10 if cfg == "cfg4" else 20
+        S_model = depth * -(-n // (13 if prec == "c64" else 12))
+        bytes_unit = 2 * (1 << n) * b * (S_model + 2 * S_model)
+        flops_unit = (1 << n) * (18 * R + 8 * D + 6)
+        units_per_s = B * a.steps / t_all
+        fpeak, fkind = fp_peak(prec)
+        roof["survey_model"] = {
+            "sweeps_model": S_model, "sweeps_executed": S,
+            "bytes_per_unit": bytes_unit, "hbm_achieved_GBps": bytes_unit * units_per_s / 1e9,
+            "hbm_frac": bytes_unit * units_per_s / 1e9 / peak,
+            "flops_per_unit": flops_unit, "fp_achieved_TFLOPs": flops_unit * units_per_s / 1e12,
+            "fp_peak_TFLOPs": fpeak, "fp_peak_source": fkind,
+            "fp_frac": flops_unit * units_per_s / 1e12 / fpeak if fpeak else None}
     else:
         dom = prof["onchip"]
         R, D, G = wl.gate_counts(cfg)

@@ -370,7 +370,7 @@ struct Gen {
   // the register accumulator da<dl> (kept across the tile loop), otherwise
   // into the shared-memory partials.
   static constexpr int kChains = 4;
-  void dot(const WOp& op, bool per_thread, int nw, int reg_acc) {
+  void dot(const WOp& op, bool per_thread, int group, int nw, int reg_acc) {
     if (op.dl < 0) return;
     const int a = op.a;
     o << "{ R acc_ = (R)0;\n";
@@ -465,8 +465,9 @@ struct Gen {
     } else if (per_thread) {
       o << "dacc[" << op.dl << " * T + tid] += acc_; }\n";
     } else {
-      o << "acc_ = warp_sum_r(acc_); if ((tid & 31) == 0) dacc[" << op.dl << " * " << nw
-        << " + (tid >> 5)] += acc_; }\n";
+      for (int m = 16; m >= group; m >>= 1) o << "acc_ += __shfl_xor_sync(0xffffffffu, acc_, " << m << ");\n";
+      o << "if ((tid & 31) < " << group << ") dacc[(" << op.dl << " * " << nw << " + (tid >> 5)) * " << group
+        << " + (tid & 31)] += acc_; }\n";
     }
   }
 
@@ -586,9 +587,12 @@ JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd, bool fused) {
   L.trig = o; o = a16(o + P.slots.size() * 8 * rsz);
   L.extra = o;
   if (bwd) {
-    const size_t pt = (size_t)P.n_dslots_pass * T * rsz;
-    L.per_thread = pt <= 40 * 1024;
-    o = a16(o + (L.per_thread ? pt : (size_t)P.n_dslots_pass * (T / 32) * rsz));
+    // largest lane group whose partials fit: a dot costs log2(32/group)
+    // shuffles plus one shared read-modify-write per tile
+    L.group = 32;
+    while (L.group > 1 && (size_t)P.n_dslots_pass * (T / 32) * L.group * rsz > 40 * 1024) L.group >>= 1;
+    L.per_thread = L.group == 32;
+    o = a16(o + (size_t)P.n_dslots_pass * (T / 32) * L.group * rsz);
   }
   L.extra2 = o;
   if (!bwd || fused) o = a16(o + (96 + (size_t)(i == 0 ? ((pl->prep_total + 1) & ~1) : 0)) * 8);
@@ -725,7 +729,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   o << ";\n(void)ot;\n";
   if (bwd)
     o << "R* dacc = reinterpret_cast<R*>(smem + " << L.extra << ");\n"
-      << "for (int i = tid; i < " << P.n_dslots_pass * (L.per_thread ? g.T : nw) << "; i += T) dacc[i] = (R)0;\n";
+      << "for (int i = tid; i < " << P.n_dslots_pass * nw * L.group << "; i += T) dacc[i] = (R)0;\n";
   if (fwd)
     o << "double* dx = reinterpret_cast<double*>(smem + " << L.extra2 << ");\n"
       << "double* red = dx; double* inv = dx + 32; double* wt = dx + 64; double* sval = dx + 96;\n"
@@ -937,7 +941,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       g.pending = false;
       const int lo = std::max<int>(W.op0, first ? stop_op : 0);
       for (int k = W.op1 - 1; k >= lo; --k) {
-        g.dot(P.wops[k], L.per_thread, nw, reg_acc);
+        g.dot(P.wops[k], L.per_thread, L.group, nw, reg_acc);
         if (!(first && k == stop_op && P.wops[k].dl >= 0)) g.apply(P.wops[k], true, true);
       }
       g.flush_pending(true);
@@ -971,7 +975,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   if (fwd && last)
     o << "e = block_sum<R>(e, red, tid, T);\nif (tid == 0) ps.rpart[vl * ps.n_chunks + chunk] = e;\n";
   if (bwd) {
-    const int stride = L.per_thread ? g.T : nw;
+    const int stride = nw * L.group;
     for (int k = 0; k < reg_acc; ++k) o << "dacc[" << k << " * T + tid] = da" << k << ";\n";
     // one warp per slot: lanes sum strided partials in double, then a shuffle tree
     o << "__syncthreads();\n{ const int lane_ = tid & 31;\nfor (int i = tid >> 5; i < " << P.n_dslots_pass

@@ -11,7 +11,8 @@ namespace hq {
 
 struct JitLayout {
   size_t lut, trig, extra, extra2, total;
-  bool per_thread;  // bwd: per-thread derivative accumulators (else per warp)
+  bool per_thread;  // bwd: per-thread derivative accumulators (group == 32)
+  int group;        // bwd: derivative partials kept per group of 32/group lanes (1 = per warp)
 };
 
 JitLayout jit_layout(const hq_plan_s* pl, int pass, bool bwd, bool fused = false);
