@@ -280,7 +280,7 @@ uint16_t swz_host(uint32_t j) { return (uint16_t)(j ^ (((j >> 4) ^ (j >> 8)) & 1
 // Split one pass's ops (tile-bit operands) into register windows (see
 // hq_window.cuh): same greedy as the pass scheduler, capacity kRegBits, over
 // the exchange qubits; controls / diagonal qubits may be thread bits.
-void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB) {
+void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, int fixed) {
   auto exch = [](const hq::DOp& o) -> uint32_t {
     switch (o.kind) {
       case HQ_GATE_H: case HQ_GATE_X: case HQ_GATE_Y: case HQ_GATE_RX: case HQ_GATE_RY:
@@ -342,13 +342,29 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB) 
         progress = true;
       }
     }
-    // register bits, then thread bits: lanes first, covering all 4 bank classes
+    // register bits, then thread bits: lanes first, covering all 4 bank
+    // classes.  Controls of CNOTs whose control is not a register bit go to
+    // warp bits where possible (warp-uniform branch instead of FSEL swaps);
+    // bits below `fixed` keep their lane slots (direct HBM windows).
+    uint32_t ctl = 0;
+    for (size_t k : exec)
+      if (ops[k].kind == HQ_GATE_CNOT && ops[k].a >= 0 && !(Rm >> ops[k].a & 1u)) ctl |= 1u << ops[k].a;
     std::vector<int> R, S, rest;
     for (int b = 0; b < q; ++b) (Rm >> b & 1u ? R : rest).push_back(b);
     std::vector<char> used(rest.size(), 0);
-    for (int cls = 0; cls < 4 && (int)S.size() < 5; ++cls)
-      for (size_t i = 0; i < rest.size(); ++i)
-        if (!used[i] && (rest[i] & 3) == cls) { S.push_back(rest[i]); used[i] = 1; break; }
+    auto pick = [&](int cls) {   // lane bit of bank class cls (-1: any class)
+      int best = -1;
+      for (size_t i = 0; i < rest.size(); ++i) {
+        if (used[i] || (cls >= 0 && (rest[i] & 3) != cls)) continue;
+        if (rest[i] < fixed) { best = (int)i; break; }
+        const bool c = ctl >> rest[i] & 1u;
+        if (best < 0 || (!c && (ctl >> rest[best] & 1u))) best = (int)i;
+        if (!c) break;
+      }
+      if (best >= 0) { S.push_back(rest[best]); used[best] = 1; }
+    };
+    for (int cls = 0; cls < 4 && (int)S.size() < 5; ++cls) pick(cls);
+    while ((int)S.size() < 5 && S.size() < rest.size()) pick(-1);
     for (size_t i = 0; i < rest.size(); ++i)
       if (!used[i]) S.push_back(rest[i]);
     (void)all;
@@ -544,7 +560,7 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
         pl->dops.push_back(o);
         pops.push_back(o);
       }
-      plan_windows(ps, pops, pl->tile_bits, RB);
+      plan_windows(ps, pops, pl->tile_bits, RB, f);
       ps.n_dops = (int32_t)ps.op_ids.size();
       ps.n_dslots_pass = (int32_t)pass_dlist.size() - ps.first_dlist;
       ps.first_slotlist = (int32_t)pass_slots.size();

@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <thread>
@@ -516,6 +517,7 @@ typedef unsigned long size_t;
 )";
 
 const char* kHelpers = R"(
+__device__ __forceinline__ void bar_na() { asm volatile("barrier.sync 0;" ::: "memory"); }
 namespace hq {
 __device__ __forceinline__ uint32_t jpad(uint32_t j) { return j + (j >> 4) + (j >> 8); }
 // packed FP32x2 (sm_100 FFMA2/FMUL2/FADD2): a complex64 amplitude is one
@@ -785,6 +787,54 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     for (int k = 0; k < reg_acc; ++k) o << "R da" << k << " = (R)0;\n";
   }
 
+  // Window op emission.  A CNOT whose control is a CTA-uniform (tile bit
+  // outside the tile) or warp-uniform (warp-index bit) runtime bit becomes a
+  // branch: each side continues with its own compile-time register renaming
+  // down to the window's store, instead of FSEL-swapping every register pair.
+  // Barriers inside warp-uniform branches are the non-aligned form.
+  int ubudget = 2;
+  if (const char* e = std::getenv("HQ_UBRANCH")) ubudget = std::atoi(e);
+  if (fused) ubudget = 0;
+  bool na = false;
+  auto sync = [&]() { o << (na ? "bar_na();\n" : "__syncthreads();\n"); };
+  std::function<void(const std::vector<int>&, size_t, bool, const std::function<void()>&, int)> emit_steps;
+  emit_steps = [&](const std::vector<int>& ks, size_t i, bool adj, const std::function<void()>& tail, int budget) {
+    for (; i < ks.size(); ++i) {
+      const int k = ks[i];
+      const WOp& op = P.wops[k];
+      if (adj) {
+        g.dot(op, L.per_thread, L.group, nw, reg_acc);
+        if (first && k == stop_op && op.dl >= 0) continue;
+      }
+      const bool uni = op.kind == HQ_GATE_CNOT && !Gen::is_reg(op.a) && (op.a >= 64 || op.a - 16 >= 5);
+      if (budget > 0 && uni) {
+        const std::vector<int> map0 = g.map;
+        const bool pend0 = g.pending, na0 = na;
+        if (op.a < 64) na = true;
+        WOp x{};
+        x.kind = HQ_GATE_X;
+        x.a = op.b;
+        x.b = -1;
+        x.slot = -1;
+        x.dl = -1;
+        o << "if (" << Gen::cond(op.a) << ") {\n";
+        g.apply(x, adj, adj);
+        emit_steps(ks, i + 1, adj, tail, budget - 1);
+        o << "} else {\n";
+        g.map = map0;
+        g.pending = pend0;
+        emit_steps(ks, i + 1, adj, tail, budget - 1);
+        o << "}\n";
+        g.map = map0;
+        g.pending = pend0;
+        na = na0;
+        return;
+      }
+      g.apply(op, adj, adj);
+    }
+    tail();
+  };
+
   // ---- tile loop
   o << "for (int tt = 0; tt < ps.tpc; ++tt) {\n"
     << "const uint64_t t = (uint64_t)chunk * ps.tpc + tt;\n"
@@ -850,15 +900,23 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         g.load_regs(W, "p", "tp");
       }
       g.pending = false;
-      for (int k = W.op0; k < W.op1; ++k) g.apply(P.wops[k], false, false);
-      g.flush_pending(false);
+      std::vector<int> ks;
+      for (int k = W.op0; k < W.op1; ++k) ks.push_back(k);
       if (w < nwin - 1) {
-        o << "__syncthreads();\n";
-        g.store_regs(W, "p", "tp");
-        o << "__syncthreads();\n}\n";
+        emit_steps(ks, 0, false, [&] { g.flush_pending(false); sync(); g.store_regs(W, "p", "tp"); sync(); }, ubudget);
+        o << "}\n";
+      } else if (fused) {
+        for (int k : ks) g.apply(P.wops[k], false, false);
+        g.flush_pending(false);
+      } else if (last || !direct_ok(W)) {
+        emit_steps(ks, 0, false, [&] { g.flush_pending(false); sync(); g.store_regs(W, "p", "tp"); sync(); }, ubudget);
+        o << "}\n";
+      } else {
+        emit_steps(ks, 0, false, [&] { g.flush_pending(false); direct_store(W, false); }, ubudget);
+        o << "}\n";
       }
     }
-    // the last window's block is still open here
+    // fused: the last window's block is still open here
     const WinDev& WL = P.wins[nwin - 1];
     if (fused) {
       // readout + λ = wψ on the registers (tile index of logical register i =
@@ -878,9 +936,6 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       o << "}\n";
       regs_live = true;  // continue into the backward windows (block stays open)
     } else if (last) {
-      o << "__syncthreads();\n";
-      g.store_regs(WL, "p", "tp");
-      o << "__syncthreads();\n}\n";
       o << "{ double wb = 0.0; for (int i = 0; i < p.n_measured; ++i) if ((base >> p.measured[i]) & 1ull) "
            "wb += (double)(1ull << i);\n"
         << "for (int bb = 0; bb < Q - " << g.RB << "; ++bb) if ((tid >> bb) & 1) wb += wt[bb];\n";
@@ -896,13 +951,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
              "dst[2 * g2 + 1] = (double)z.x * gph[1] + (double)z.y * gph[0]; } }\n";
       }
       o << "}\n";
-    } else if (direct_ok(WL)) {
-      direct_store(WL, false);
-      o << "}\n";
-    } else {
-      o << "__syncthreads();\n";
-      g.store_regs(WL, "p", "tp");
-      o << "__syncthreads();\n}\n";
+    } else if (!direct_ok(WL)) {
       for (int i = 0; i < g.N; ++i)
         o << "gout[base | ot | " << hex64(hi_off(i)) << "] = tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u];\n";
     }
@@ -940,35 +989,38 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       }
       g.pending = false;
       const int lo = std::max<int>(W.op0, first ? stop_op : 0);
-      for (int k = W.op1 - 1; k >= lo; --k) {
-        g.dot(P.wops[k], L.per_thread, L.group, nw, reg_acc);
-        if (!(first && k == stop_op && P.wops[k].dl >= 0)) g.apply(P.wops[k], true, true);
-      }
-      g.flush_pending(true);
+      std::vector<int> ks;
+      for (int k = W.op1 - 1; k >= lo; --k) ks.push_back(k);
       const bool end = first ? (wi == nwin - 1 || w == stop_win) : (w == 0);
       if (end) {
-        if (!first) {
+        emit_steps(ks, 0, true, [&] {
+          g.flush_pending(true);
+          if (first) return;
           if (direct_ok(W)) {
             direct_store(W, true);
           } else {
-            o << "__syncthreads();\n";
+            sync();
             g.store_regs(W, "p", "tp");
             g.store_regs(W, "l", "tl");
-            o << "__syncthreads();\n";
+            sync();
             for (int i = 0; i < g.N; ++i) {
               o << "if (gout) gout[base | ot | " << hex64(hi_off(i)) << "] = tp[tpad + " << Gen::pad((uint32_t)(i * g.T))
                 << "u];\n";
               o << "glam[base | ot | " << hex64(hi_off(i)) << "] = tl[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u];\n";
             }
           }
-        }
+        }, ubudget);
         o << "}\n";
         break;
       }
-      o << "__syncthreads();\n";
-      g.store_regs(W, "p", "tp");
-      g.store_regs(W, "l", "tl");
-      o << "__syncthreads();\n}\n";
+      emit_steps(ks, 0, true, [&] {
+        g.flush_pending(true);
+        sync();
+        g.store_regs(W, "p", "tp");
+        g.store_regs(W, "l", "tl");
+        sync();
+      }, ubudget);
+      o << "}\n";
     }
   }
   o << "__syncthreads();\n}\n";  // tile loop
