@@ -88,6 +88,7 @@ struct hq_plan_s {
   int32_t n_inputs = 0, n_params = 0;
   bool onchip = true;
   int32_t tile_bits = 0;                  // streaming path
+  int32_t fixed_bits = 0;                 // low qubits always in the tile (contiguous HBM runs)
   int32_t reg_bits = 0;                   // amplitudes per thread = 2^reg_bits (register windows)
   int32_t n_adj = 0, n_tp = 0;
   std::vector<hq::DOp> dops;              // on-chip: the whole tape; streaming: per pass

@@ -518,6 +518,11 @@ typedef unsigned long size_t;
 
 const char* kHelpers = R"(
 __device__ __forceinline__ void bar_na() { asm volatile("barrier.sync 0;" ::: "memory"); }
+__device__ __forceinline__ void cp8(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"((unsigned)__cvta_generic_to_shared(s)), "l"(g) : "memory"); }
+__device__ __forceinline__ void cp16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"((unsigned)__cvta_generic_to_shared(s)), "l"(g) : "memory"); }
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 namespace hq {
 __device__ __forceinline__ uint32_t jpad(uint32_t j) { return j + (j >> 4) + (j >> 8); }
 // packed FP32x2 (sm_100 FFMA2/FMUL2/FADD2): a complex64 amplitude is one
@@ -629,7 +634,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   const int n = pl->n_qubits;
   const int np = (int)pl->passes.size();
   const bool first = pi == 0, last = pi == np - 1;
-  const int f = c64 ? 3 : 2;
+  const int f = pl->fixed_bits;
   const JitLayout L = jit_layout(pl, pi, bwd, fused);
   const int nw = g.T / 32;
   const int nwin = (int)P.wins.size();
@@ -792,6 +797,9 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   // branch: each side continues with its own compile-time register renaming
   // down to the window's store, instead of FSEL-swapping every register pair.
   // Barriers inside warp-uniform branches are the non-aligned form.
+  // HQ_ABLATE (timing experiments only, results are wrong): backward kernels
+  // without window transitions (1), gate math (2), derivative dots (4)
+  const int ablate = std::getenv("HQ_ABLATE") ? std::atoi(std::getenv("HQ_ABLATE")) : 0;
   int ubudget = 2;
   if (const char* e = std::getenv("HQ_UBRANCH")) ubudget = std::atoi(e);
   if (fused) ubudget = 0;
@@ -803,7 +811,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       const int k = ks[i];
       const WOp& op = P.wops[k];
       if (adj) {
-        g.dot(op, L.per_thread, L.group, nw, reg_acc);
+        if (!(ablate & 4)) g.dot(op, L.per_thread, L.group, nw, reg_acc);
         if (first && k == stop_op && op.dl >= 0) continue;
       }
       const bool uni = op.kind == HQ_GATE_CNOT && !Gen::is_reg(op.a) && (op.a >= 64 || op.a - 16 >= 5);
@@ -830,10 +838,37 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         na = na0;
         return;
       }
-      g.apply(op, adj, adj);
+      if (!(adj && (ablate & 2))) g.apply(op, adj, adj);
     }
     tail();
   };
+
+  // Tile prefetch (cp.async) into the transposition buffers: once the last
+  // window of a tile has read its registers from shared memory, the next
+  // tile's first window is copied into tp/tl asynchronously, overlapping that
+  // window's math and HBM store; the next tile then starts from shared memory.
+  // Needs direct (HBM-contiguous) first and last windows.
+  const WinDev& Wfirst = bwd ? P.wins[nwin - 1] : P.wins[0];
+  bool pf = !fused && !(fwd && first) && !(fwd && last) && direct_ok(Wfirst) &&
+            (bwd ? (first || direct_ok(P.wins[0])) : direct_ok(P.wins[nwin - 1]));
+  {
+    const char* e = std::getenv("HQ_PF");
+    if (!(e && e[0] == '1')) pf = false;
+  }
+  auto emit_tile_prefetch = [&](const char* texpr) {
+    o << "{ const uint64_t t2 = " << texpr << "; const uint64_t base2 = 0ull";
+    for (size_t i = 0; i < nonlocal.size(); ++i) o << " | (((t2 >> " << i << ") & 1ull) << " << nonlocal[i] << ")";
+    o << ";\n";
+    g.win_tb(Wfirst, tbits);
+    emit_tw(Wfirst);
+    for (int i = 0; i < g.N; ++i) {
+      const char* cp = c64 ? "cp8" : "cp16";
+      o << cp << "(&tp[tb + " << g.phys(Wfirst, i) << "u], gpsi + (base2 | tw | " << hex64(reg_goff(Wfirst, i)) << "));\n";
+      if (bwd) o << cp << "(&tl[tb + " << g.phys(Wfirst, i) << "u], glam + (base2 | tw | " << hex64(reg_goff(Wfirst, i)) << "));\n";
+    }
+    o << "}\n";
+  };
+  if (pf) emit_tile_prefetch("(uint64_t)chunk * ps.tpc");
 
   // ---- tile loop
   o << "for (int tt = 0; tt < ps.tpc; ++tt) {\n"
@@ -879,6 +914,8 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
            "init_amp(a, sval, inv, base | goff_j(j)); tp[jpad(j)].x = (R)z.x; tp[jpad(j)].y = (R)z.y; } }\n"
         << "else { for (uint32_t j = tid; j < (1u << Q); j += T) { tp[jpad(j)].x = (R)((base | goff_j(j)) == 0); "
            "tp[jpad(j)].y = (R)0; } } }\n__syncthreads();\n";
+    } else if (pf) {
+      o << "cp_wait();\n__syncthreads();\n";
     } else if (direct_ok(W0)) {
       o << "{ // window 0: direct load\n";
       direct_load(W0, false);
@@ -898,6 +935,10 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       if (!(w == 0 && regs_live)) {
         identity_map();
         g.load_regs(W, "p", "tp");
+      }
+      if (pf && w == nwin - 1) {
+        o << "__syncthreads();\nif (tt + 1 < ps.tpc) ";
+        emit_tile_prefetch("t + 1");
       }
       g.pending = false;
       std::vector<int> ks;
@@ -960,7 +1001,10 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     const WinDev& WL = P.wins[nwin - 1];
     if (!fused) {
       identity_map();
-      if (direct_ok(WL)) {
+      if (pf) {
+        o << "cp_wait();\n__syncthreads();\n";
+        regs_live = false;
+      } else if (direct_ok(WL)) {
         o << "{ // window " << nwin - 1 << " (adjoint): direct load\n";
         g.win_tb(WL, tbits);
         direct_load(WL, true);
@@ -984,8 +1028,14 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         o << "{ // window " << w << " (adjoint)\n";
         g.win_tb(W, tbits);
         identity_map();
-        g.load_regs(W, "p", "tp");
-        g.load_regs(W, "l", "tl");
+        if (!(ablate & 1)) {
+          g.load_regs(W, "p", "tp");
+          g.load_regs(W, "l", "tl");
+        }
+      }
+      if (pf && (first ? (wi == nwin - 1 || w == stop_win) : (w == 0))) {
+        o << "__syncthreads();\nif (tt + 1 < ps.tpc) ";
+        emit_tile_prefetch("t + 1");
       }
       g.pending = false;
       const int lo = std::max<int>(W.op0, first ? stop_op : 0);
@@ -1015,6 +1065,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       }
       emit_steps(ks, 0, true, [&] {
         g.flush_pending(true);
+        if (ablate & 1) return;
         sync();
         g.store_regs(W, "p", "tp");
         g.store_regs(W, "l", "tl");
