@@ -466,10 +466,60 @@ struct Gen {
     } else if (per_thread) {
       o << "dacc[" << op.dl << " * T + tid] += acc_; }\n";
     } else {
-      for (int m = 16; m >= group; m >>= 1) o << "acc_ += __shfl_xor_sync(0xffffffffu, acc_, " << m << ");\n";
-      o << "if ((tid & 31) < " << group << ") dacc[(" << op.dl << " * " << nw << " + (tid >> 5)) * " << group
-        << " + (tid & 31)] += acc_; }\n";
+      // batched: up to 8 dots are reduced across the warp together
+      o << "dq" << bq.size() << " = acc_; }\n";
+      bq.push_back(op.dl);
+      bgroup = group;
+      bnw = nw;
+      if (bq.size() == 8) flush_batch();
     }
+  }
+
+  // Transposed warp reduction of the pending dots dq0..dq(K-1): at each split
+  // level (lane masks 16, 8, 4) a lane keeps half of its values and trades the
+  // other half with its partner, so K dots cost K-1 shuffles instead of
+  // K·log2(32/G); the remaining lane bits above the group are summed, and each
+  // lane then updates one (slot, group) partial.
+  std::vector<int> bq;
+  int bgroup = 4, bnw = 8;
+  void flush_batch() {
+    if (bq.empty()) return;
+    const int K = (int)bq.size();
+    int Lv = 0;
+    while ((1 << Lv) < K) ++Lv;
+    const int split_m[3] = {16, 8, 4};
+    std::vector<std::string> vals;
+    for (int j = 0; j < (1 << Lv); ++j) vals.push_back(j < K ? "dq" + std::to_string(j) : std::string("(R)0"));
+    o << "{ const unsigned ln_ = tid & 31;\n";
+    int used = 0;
+    for (int lv = 0; lv < Lv; ++lv) {
+      const int m = split_m[lv];
+      used |= m;
+      const int half = (int)vals.size() / 2;
+      std::vector<std::string> nv;
+      for (int j = 0; j < half; ++j) {
+        const std::string nm = "t" + std::to_string(lv) + "_" + std::to_string(j) + "_";
+        o << "const R " << nm << " = ((ln_ & " << m << "u) ? " << vals[half + j] << " : " << vals[j]
+          << ") + __shfl_xor_sync(0xffffffffu, (ln_ & " << m << "u) ? " << vals[j] << " : " << vals[half + j] << ", "
+          << m << ");\n";
+        nv.push_back(nm);
+      }
+      vals = nv;
+    }
+    o << "R z_ = " << vals[0] << ";\n";
+    int red = 0;
+    for (int m = 16; m >= 1; m >>= 1)
+      if (!(used & m) && m >= bgroup) {
+        o << "z_ += __shfl_xor_sync(0xffffffffu, z_, " << m << ");\n";
+        red |= m;
+      }
+    o << "const int d_ = 0";
+    for (int lv = 0; lv < Lv; ++lv) o << " + ((ln_ & " << split_m[lv] << "u) ? " << (1 << (Lv - 1 - lv)) << " : 0)";
+    o << ";\nint s_ = " << bq[0] << ";";
+    for (int j = 1; j < K; ++j) o << " if (d_ == " << j << ") s_ = " << bq[j] << ";";
+    o << "\nif (d_ < " << K << " && (ln_ & " << red << "u) == 0) dacc[(s_ * " << bnw << " + (tid >> 5)) * " << bgroup
+      << " + (ln_ & " << (bgroup - 1) << "u)] += z_; }\n";
+    bq.clear();
   }
 
   // Padded shared layout: element j at pad(j) = j + (j>>4) + (j>>8).  pad is
@@ -599,6 +649,7 @@ JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd, bool fused) {
     L.group = 32;
     while (L.group > 1 && (size_t)P.n_dslots_pass * (T / 32) * L.group * rsz > 40 * 1024) L.group >>= 1;
     L.per_thread = L.group == 32;
+    if (!L.per_thread) L.group = std::min(L.group, 4);   // batched reduction keeps 4 partials per warp
     o = a16(o + (size_t)P.n_dslots_pass * (T / 32) * L.group * rsz);
   }
   L.extra2 = o;
@@ -790,6 +841,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     if (const char* e = std::getenv("HQ_REG_ACC")) cap = std::atoi(e);
     if (P.n_dslots_pass <= cap && L.per_thread) reg_acc = P.n_dslots_pass;
     for (int k = 0; k < reg_acc; ++k) o << "R da" << k << " = (R)0;\n";
+    if (!L.per_thread) o << "R dq0, dq1, dq2, dq3, dq4, dq5, dq6, dq7;\n";
   }
 
   // Window op emission.  A CNOT whose control is a CTA-uniform (tile bit
@@ -816,7 +868,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       }
       const bool uni = op.kind == HQ_GATE_CNOT && !Gen::is_reg(op.a) && (op.a >= 64 || op.a - 16 >= 5);
       if (budget > 0 && uni) {
-        const std::vector<int> map0 = g.map;
+        const std::vector<int> map0 = g.map, bq0 = g.bq;
         const bool pend0 = g.pending, na0 = na;
         if (op.a < 64) na = true;
         WOp x{};
@@ -830,10 +882,12 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         emit_steps(ks, i + 1, adj, tail, budget - 1);
         o << "} else {\n";
         g.map = map0;
+        g.bq = bq0;
         g.pending = pend0;
         emit_steps(ks, i + 1, adj, tail, budget - 1);
         o << "}\n";
         g.map = map0;
+        g.bq.clear();
         g.pending = pend0;
         na = na0;
         return;
@@ -1044,6 +1098,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       const bool end = first ? (wi == nwin - 1 || w == stop_win) : (w == 0);
       if (end) {
         emit_steps(ks, 0, true, [&] {
+          g.flush_batch();
           g.flush_pending(true);
           if (first) return;
           if (direct_ok(W)) {
@@ -1064,6 +1119,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         break;
       }
       emit_steps(ks, 0, true, [&] {
+        g.flush_batch();
         g.flush_pending(true);
         if (ablate & 1) return;
         sync();
