@@ -92,7 +92,7 @@ int64_t ws_budget() {
 
 struct Layout {
   int64_t V = 0;
-  size_t tp = 0, dpart = 0, psi = 0, lam = 0, rpart = 0, scratch = 0, total = 0;
+  size_t tp = 0, dpart = 0, psi = 0, lam = 0, rpart = 0, lamN = 0, scratch = 0, total = 0;
   int32_t n_parts = 1;
   hq::StreamWs sws;
 };
@@ -130,6 +130,7 @@ Layout layout_for(const hq_plan_s* pl, int64_t B, int32_t flags, bool need_state
     L.psi = off; off = align_up(off + (size_t)cs * per * (L.sws.ckpt ? L.sws.ckpt : 1));
     if (adj) { L.lam = off; off = align_up(off + (size_t)cs * per); }
     L.rpart = off; off = align_up(off + (size_t)cs * nc * 8);
+    if (adj && pl->fold_grad) { L.lamN = off; off = align_up(off + (size_t)cs * n_tiles * 16); }
   }
   (void)need_state_only;
   L.scratch = off; off = align_up(off + (size_t)B * 8 + 8);   // readout sink for hq_state
@@ -228,7 +229,9 @@ static hq_status validate(const hq_plan_desc* d) {
 namespace {
 
 // Greedy pass scheduler (see file comment).
-std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int q, int f) {
+// excl0: qubits that must stay out of the first pass's tile (their folded
+// gates' gradients are read from λ contracted over that tile)
+std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int q, int f, uint64_t excl0 = 0) {
   std::vector<hq::Pass> passes;
   std::vector<char> done(ops.size(), 0);
   size_t left = ops.size();
@@ -247,7 +250,8 @@ std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int 
         if (qs & blocked) { blocked |= qs; continue; }
         const uint64_t ex = exch_mask(ops[k]);
         if (ps.op_ids.size() >= kMaxPassOps) { blocked |= qs; continue; }
-        if ((ex & ~L) == 0 || popc(L | ex) <= q) {
+        const uint64_t excl = passes.empty() ? excl0 : 0;
+        if (!(ex & excl) && ((ex & ~L) == 0 || popc(L | ex) <= q)) {
           L |= ex;
           done[k] = 1;
           --left;
@@ -259,7 +263,8 @@ std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int 
       }
       if (first_scan) {
         // top up the tile with the lowest remaining qubits, then rescan
-        for (int b = 0; b < n && popc(L) < q; ++b) L |= 1ull << b;
+        for (int b = 0; b < n && popc(L) < q; ++b)
+          if (!((passes.empty() ? excl0 : 0) >> b & 1ull)) L |= 1ull << b;
         first_scan = false;
         progress = true;
       }
@@ -415,7 +420,63 @@ const T* rebase(const T* rel, char* base) {
 
 }  // namespace
 
+static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, bool allow_fold);
+
 extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
+  return plan_create_impl(d, out, true);
+}
+
+namespace {
+// Owning copy of a plan description (the unfolded twin is built lazily).
+struct DescCopy {
+  hq_plan_desc d{};
+  std::vector<hq_op> ops;
+  std::vector<double> sconst, scoef, gfactor;
+  std::vector<int32_t> sptr, svar, meas, pptr, pq, ps0, plen, gmode, gslot;
+  explicit DescCopy(const hq_plan_desc* s) : d(*s) {
+    const int nv = s->n_inputs + s->n_params;
+    const int nnz = s->n_slots ? s->slot_ptr[s->n_slots] : 0;
+    const int npq = s->n_preps ? s->prep_ptr[s->n_preps] : 0;
+    ops.assign(s->ops, s->ops + s->n_ops);
+    sconst.assign(s->slot_const, s->slot_const + s->n_slots);
+    if (s->n_slots) sptr.assign(s->slot_ptr, s->slot_ptr + s->n_slots + 1);
+    svar.assign(s->slot_var, s->slot_var + nnz);
+    scoef.assign(s->slot_coef, s->slot_coef + nnz);
+    if (s->n_measured) meas.assign(s->measured, s->measured + s->n_measured);
+    if (s->n_preps) {
+      pptr.assign(s->prep_ptr, s->prep_ptr + s->n_preps + 1);
+      pq.assign(s->prep_qubits, s->prep_qubits + npq);
+      ps0.assign(s->prep_slot0, s->prep_slot0 + s->n_preps);
+      plen.assign(s->prep_len, s->prep_len + s->n_preps);
+    }
+    if (s->grad_mode) {
+      gmode.assign(s->grad_mode, s->grad_mode + nv);
+      gslot.assign(s->grad_slot, s->grad_slot + nv);
+      gfactor.assign(s->grad_factor, s->grad_factor + nv);
+    }
+    d.ops = ops.data();
+    d.slot_const = sconst.data();
+    d.slot_ptr = sptr.data();
+    d.slot_var = svar.data();
+    d.slot_coef = scoef.data();
+    d.measured = meas.empty() ? nullptr : meas.data();
+    d.prep_ptr = pptr.data();
+    d.prep_qubits = pq.data();
+    d.prep_slot0 = ps0.data();
+    d.prep_len = plen.data();
+    d.grad_mode = s->grad_mode ? gmode.data() : nullptr;
+    d.grad_slot = s->grad_mode ? gslot.data() : nullptr;
+    d.grad_factor = s->grad_mode ? gfactor.data() : nullptr;
+  }
+};
+bool single_qubit(int k) {
+  return k == HQ_GATE_H || k == HQ_GATE_X || k == HQ_GATE_Y || k == HQ_GATE_Z || k == HQ_GATE_RX ||
+         k == HQ_GATE_RY || k == HQ_GATE_RZ;
+}
+constexpr int kMaxFoldPerQubit = 32;
+}  // namespace
+
+static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, bool allow_fold) {
   if (!out) return fail(HQ_E_CONFIG, "null output");
   *out = nullptr;
   hq_status st = validate(d);
@@ -538,6 +599,67 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
       return fail(HQ_E_CONFIG, "tile must hold 2^9..2^14 amplitudes");
     }
     pl->passes = schedule_passes(gates, n, pl->tile_bits, f);
+
+    // ---- fold leading single-qubit gates into the initial product state ----
+    // Qubits outside the first pass's tile: their whole single-qubit prefix
+    // (its gradients come from λ at the first pass's start, contracted over
+    // the tile: k_fold_grad).  Tile qubits: only the leading undifferentiated
+    // gates (the first backward pass differentiates the rest as usual).
+    const char* nofold = std::getenv("HQ_NO_FOLD");
+    if (allow_fold && !pl->has_preps && !(nofold && nofold[0] == '1')) {
+      uint64_t L0 = 0;
+      for (int b : pl->passes[0].local) L0 |= 1ull << b;
+      std::vector<char> open(n, 1), fold_it(gates.size(), 0);
+      std::vector<int> cnt(n, 0);
+      uint64_t excl = 0;
+      for (size_t k = 0; k < gates.size(); ++k) {
+        const hq_op& g = gates[k];
+        if (!single_qubit(g.kind)) {
+          for (int qb : {g.q0, g.q1})
+            if (qb >= 0) open[qb] = 0;
+          continue;
+        }
+        const int qb = g.q0;
+        if (!open[qb]) continue;
+        const bool local0 = L0 >> qb & 1ull;
+        if (cnt[qb] >= kMaxFoldPerQubit || (local0 && dslot_of(g) >= 0)) { open[qb] = 0; continue; }
+        fold_it[k] = 1;
+        ++cnt[qb];
+        if (dslot_of(g) >= 0) excl |= 1ull << qb;
+      }
+      std::vector<hq_op> kept;
+      pl->fold_ptr.assign(n + 1, 0);
+      for (int qb = 0; qb < n; ++qb) pl->fold_ptr[qb + 1] = pl->fold_ptr[qb] + cnt[qb];
+      pl->fold_kind.assign(pl->fold_ptr[n], 0);
+      pl->fold_slot.assign(pl->fold_ptr[n], -1);
+      pl->fold_dslot.assign(pl->fold_ptr[n], -1);
+      std::vector<int> fill(n, 0);
+      for (size_t k = 0; k < gates.size(); ++k) {
+        if (!fold_it[k]) { kept.push_back(gates[k]); continue; }
+        const hq_op& g = gates[k];
+        const int at = pl->fold_ptr[g.q0] + fill[g.q0]++;
+        pl->fold_kind[at] = g.kind;
+        pl->fold_slot[at] = g.slot;
+        pl->fold_dslot[at] = dslot_of(g);
+      }
+      if (pl->fold_ptr[n] > 0 && !kept.empty()) {
+        pl->fold = true;
+        pl->fold_grad = excl != 0;
+        pl->fold_ops = pl->fold_ptr[n];
+        gates.swap(kept);
+        pl->passes = schedule_passes(gates, n, pl->tile_bits, f, excl);
+        for (int b : pl->passes[0].local)
+          if (excl >> b & 1ull) {
+            delete pl;
+            return fail(HQ_E_CONFIG, "internal: folded qubit inside the first pass");
+          }
+      } else {
+        pl->fold_ptr.clear();
+        pl->fold_kind.clear();
+        pl->fold_slot.clear();
+        pl->fold_dslot.clear();
+      }
+    }
     for (auto& ps : pl->passes) {
       int pos[kMaxQubits];
       for (int b = 0; b < n; ++b) pos[b] = ~b;
@@ -581,10 +703,11 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
     }
   }
 
+  // gates whose dropped global phase / sign hq_state restores (folded gates are exact)
   std::vector<int32_t> rz_slots, rot_slots;
-  for (int i = 0; i < d->n_ops; ++i) {
-    if (d->ops[i].kind == HQ_GATE_RZ) rz_slots.push_back(d->ops[i].slot);
-    if (d->ops[i].kind == HQ_GATE_RX || d->ops[i].kind == HQ_GATE_RY) rot_slots.push_back(d->ops[i].slot);
+  for (const auto& g : gates) {
+    if (g.kind == HQ_GATE_RZ) rz_slots.push_back(g.slot);
+    if (g.kind == HQ_GATE_RX || g.kind == HQ_GATE_RY) rot_slots.push_back(g.slot);
   }
 
   if (!pl->onchip) {
@@ -593,6 +716,12 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
     if (js != HQ_OK && pl->reg_bits != reg_bits_for(d->precision)) {
       delete pl;
       return fail(HQ_E_CONFIG, "HQ_REG_BITS needs the specialised kernels: " + why);
+    }
+    if (js != HQ_OK && pl->fold) {
+      // folding needs the specialised kernels
+      delete pl;
+      if (std::getenv("HQ_JIT_COMPILE_ONLY")) return fail(HQ_E_CONFIG, why);
+      return plan_create_impl(d, out, false);
     }
     if (js != HQ_OK) {
       pl->jit.ok = false;
@@ -611,7 +740,8 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
     os << " path=onchip smem=" << hq::onchip_smem_bytes(pl);
   } else {
     os << " path=stream kernels=" << (pl->jit.ok ? "jit" : "generic") << " tile_bits=" << pl->tile_bits
-       << " reg_bits=" << pl->reg_bits << " passes=" << pl->passes.size() << " [";
+       << " reg_bits=" << pl->reg_bits << " folded=" << pl->fold_ops << (pl->fold_grad ? "(grad)" : "")
+       << " passes=" << pl->passes.size() << " [";
     for (size_t i = 0; i < pl->passes.size(); ++i)
       os << (i ? "," : "") << pl->passes[i].n_dops << "/" << pl->passes[i].wins.size() << "w";
     os << "]";
@@ -678,9 +808,19 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
   const hq::WOp* r_wops;
   put(blob, off, all_wins.data(), all_wins.size(), r_wins);
   put(blob, off, all_wops.data(), all_wops.size(), r_wops);
-  const int32_t *r_rz, *r_rot;
+  const int32_t *r_rz, *r_rot, *r_fptr, *r_fkind, *r_fslot, *r_fdsl, *r_fnl;
   put(blob, off, rz_slots.data(), rz_slots.size(), r_rz);
   put(blob, off, rot_slots.data(), rot_slots.size(), r_rot);
+  std::vector<int32_t> fold_nl;
+  if (pl->fold)
+    for (int b = 0; b < n; ++b)
+      if (std::find(pl->passes[0].local.begin(), pl->passes[0].local.end(), b) == pl->passes[0].local.end())
+        fold_nl.push_back(b);
+  put(blob, off, pl->fold_ptr.data(), pl->fold_ptr.size(), r_fptr);
+  put(blob, off, pl->fold_kind.data(), pl->fold_kind.size(), r_fkind);
+  put(blob, off, pl->fold_slot.data(), pl->fold_slot.size(), r_fslot);
+  put(blob, off, pl->fold_dslot.data(), pl->fold_dslot.size(), r_fdsl);
+  put(blob, off, fold_nl.data(), fold_nl.size(), r_fnl);
   blob.resize(align_up(std::max<size_t>(blob.size(), 16)));
   cudaError_t ce = cudaMalloc(&pl->dmem, blob.size());
   if (ce != cudaSuccess) {
@@ -730,7 +870,15 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
   dv.rz_slots = rebase(r_rz, base);
   dv.n_rot = (int32_t)rot_slots.size();
   dv.rot_slots = rebase(r_rot, base);
+  dv.n_fold = pl->fold ? (int32_t)pl->fold_ops : 0;
+  dv.fold_ptr = rebase(r_fptr, base);
+  dv.fold_kind = rebase(r_fkind, base);
+  dv.fold_slot = rebase(r_fslot, base);
+  dv.fold_dslot = rebase(r_fdsl, base);
+  dv.fold_nonlocal = rebase(r_fnl, base);
+  dv.n_fold_nonlocal = (int32_t)fold_nl.size();
   pl->dev = dv;
+  if (pl->fold) pl->desc_copy = std::make_shared<DescCopy>(d);
   pl->d_wops = rebase(r_wops, base);
 
   *out = pl;
@@ -739,6 +887,7 @@ extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
 
 extern "C" void hq_plan_destroy(hq_plan pl) {
   if (!pl) return;
+  if (pl->twin) hq_plan_destroy(pl->twin);
   for (auto& r : pl->prof.recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : pl->prof.pool) cudaEventDestroy(e);
   if (pl->dmem) cudaFree(pl->dmem);
@@ -762,6 +911,17 @@ static hq_status run(hq_plan pl, const double* x, int64_t ldx, const double* the
     return fail(HQ_E_DIMENSION, "input rows narrower than the circuit's inputs");
   if (pl->n_params > 0 && !theta) return fail(HQ_E_DIMENSION, "missing parameters");
   if (init && pl->has_preps) return fail(HQ_E_CIRCUIT, "initial state and state loads are exclusive");
+  if (init && pl->fold) {
+    // a caller-provided initial state replaces the folded product state: run
+    // the same tape unfolded (same workspace layout for hq_state)
+    if (!pl->twin) {
+      hq_plan tw = nullptr;
+      const hq_status st = plan_create_impl(&static_cast<DescCopy*>(pl->desc_copy.get())->d, &tw, false);
+      if (st != HQ_OK) return st;
+      pl->twin = tw;
+    }
+    return run(pl->twin, x, ldx, theta, batch, flags, out, jac, state, init, init_rows, ws, ws_bytes, stream);
+  }
   const Layout L = layout_for(pl, batch, flags);
   if (ws_bytes < L.total || (!ws && L.total > 256)) return fail(HQ_E_CONFIG, "workspace too small");
   char* w = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
@@ -785,6 +945,7 @@ static hq_status run(hq_plan pl, const double* x, int64_t ldx, const double* the
     in.sws.psi = w + L.psi;
     in.sws.lam = L.lam ? w + L.lam : nullptr;
     in.sws.rpart = reinterpret_cast<double*>(w + L.rpart);
+    in.sws.lamN = L.lamN ? w + L.lamN : nullptr;
   }
   cudaError_t e = hq::launch_forward(pl, in, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(HQ_E_CUDA, std::string("forward launch: ") + cudaGetErrorString(e));
@@ -845,7 +1006,7 @@ extern "C" hq_status hq_stats(hq_plan pl, int64_t batch, int32_t flags, hq_plan_
       const int64_t sh_chunks = (shifted + cs - 1) / cs;
       const bool adj = jac && pl->n_adj > 0;
       const bool fused = adj && pl->jit.ok && pl->jit.fused != nullptr;
-      launches = real_chunks * (np + 1 + (adj ? (fused ? np - 1 : np) : 0)) + sh_chunks * (np + 1);
+      launches = real_chunks * (np + 1 + (adj ? (fused ? np - 1 : np) + (pl->fold_grad ? 1 : 0) : 0)) + sh_chunks * (np + 1);
       s.chunk_samples = cs;
     }
     if (jac && (int64_t)batch * (pl->n_inputs + pl->n_params) > 0) launches += 1;

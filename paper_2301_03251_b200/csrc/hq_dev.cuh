@@ -183,6 +183,57 @@ __device__ __forceinline__ void load_trig8(const KArgs& a, const VSample& vs, co
   }
 }
 
+// Exact 2x2 single-qubit gate (qsim.py:25-45 conventions) on z = (a0, a1)
+// stored as {re0, im0, re1, im1}; inv applies the adjoint.
+__device__ inline void apply_1q(int kind, double ang, bool inv, double* z) {
+  const double r0 = z[0], i0 = z[1], r1 = z[2], i1 = z[3];
+  const double th = inv ? -ang : ang;
+  switch (kind) {
+    case HQ_GATE_H: {
+      const double h = 0.70710678118654752440;
+      z[0] = h * (r0 + r1); z[1] = h * (i0 + i1); z[2] = h * (r0 - r1); z[3] = h * (i0 - i1);
+      break;
+    }
+    case HQ_GATE_X: z[0] = r1; z[1] = i1; z[2] = r0; z[3] = i0; break;
+    case HQ_GATE_Y:   // [[0, -i], [i, 0]] (self-adjoint)
+      z[0] = i1; z[1] = -r1; z[2] = -i0; z[3] = r0;
+      break;
+    case HQ_GATE_Z: z[2] = -r1; z[3] = -i1; break;
+    case HQ_GATE_RX: {  // [[c, -is], [-is, c]]
+      double s, c;
+      sincos(0.5 * th, &s, &c);
+      z[0] = c * r0 + s * i1; z[1] = c * i0 - s * r1;
+      z[2] = c * r1 + s * i0; z[3] = c * i1 - s * r0;
+      break;
+    }
+    case HQ_GATE_RY: {  // [[c, -s], [s, c]]
+      double s, c;
+      sincos(0.5 * th, &s, &c);
+      z[0] = c * r0 - s * r1; z[1] = c * i0 - s * i1;
+      z[2] = s * r0 + c * r1; z[3] = s * i0 + c * i1;
+      break;
+    }
+    case HQ_GATE_RZ: {  // diag(e^{-iθ/2}, e^{iθ/2})
+      double s, c;
+      sincos(0.5 * th, &s, &c);
+      z[0] = c * r0 + s * i0; z[1] = c * i0 - s * r0;
+      z[2] = c * r1 - s * i1; z[3] = c * i1 + s * r1;
+      break;
+    }
+    default: break;
+  }
+}
+
+// Factor of qubit q in the initial product state: its folded gates on |0>.
+__device__ inline void fold_state(const DevPlan& p, const VSample& vs, const double* xr, const double* theta,
+                                  int q, double* z) {
+  z[0] = 1.0; z[1] = 0.0; z[2] = 0.0; z[3] = 0.0;
+  for (int k = p.fold_ptr[q]; k < p.fold_ptr[q + 1]; ++k) {
+    const int s = p.fold_slot[k];
+    apply_1q(p.fold_kind[k], s >= 0 ? eval_slot(p, s, xr, theta, vs.shvar, vs.shval) : 0.0, false, z);
+  }
+}
+
 __device__ __forceinline__ void load_prep_values(const KArgs& a, const VSample& vs, double* sval,
                                                  int tid, int T) {
   const double* xr = a.x + vs.b * a.ldx;

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -111,6 +112,15 @@ struct hq_plan_s {
   const hq::WinDev* d_wins = nullptr;
   const hq::WOp* d_wops = nullptr;
   mutable hq::Prof prof;                  // live per-launch timing (bench / profiling)
+  // leading single-qubit gates folded into the initial product state
+  // (fold_ptr[q]..fold_ptr[q+1] index fold_kind/slot/dslot); fold_grad: some
+  // folded gate is differentiated (gradient from λ at the first pass's start)
+  bool fold = false, fold_grad = false;
+  std::vector<int32_t> fold_ptr, fold_kind, fold_slot, fold_dslot;
+  int64_t fold_ops = 0;
+  // hq_state with a caller-provided initial state runs on an unfolded twin
+  std::shared_ptr<void> desc_copy;
+  hq_plan_s* twin = nullptr;
   struct Jit {
     bool ok = false;
     std::string why;                      // why the static kernels run instead

@@ -653,7 +653,10 @@ JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd, bool fused) {
     o = a16(o + (size_t)P.n_dslots_pass * (T / 32) * L.group * rsz);
   }
   L.extra2 = o;
-  if (!bwd || fused) o = a16(o + (96 + (size_t)(i == 0 ? ((pl->prep_total + 1) & ~1) : 0)) * 8);
+  if (!bwd || fused || (i == 0 && pl->fold_grad))
+    o = a16(o + (96 + (size_t)(i == 0 ? ((pl->prep_total + 1) & ~1) : 0)) * 8);
+  L.fz = o;
+  if (i == 0 && pl->fold) o = a16(o + ((size_t)pl->n_qubits * 2 + ((size_t)1 << RB)) * amp);
   L.total = o;
   return L;
 }
@@ -685,6 +688,9 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   const int n = pl->n_qubits;
   const int np = (int)pl->passes.size();
   const bool first = pi == 0, last = pi == np - 1;
+  // (a folding plan with folded gradients un-applies λ through the whole first
+  // pass: its start is where k_fold_grad reads λ)
+  const bool fold_end = bwd && first && pl->fold_grad;
   const int f = pl->fixed_bits;
   const JitLayout L = jit_layout(pl, pi, bwd, fused);
   const int nw = g.T / 32;
@@ -792,6 +798,16 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     o << "double* dx = reinterpret_cast<double*>(smem + " << L.extra2 << ");\n"
       << "double* red = dx; double* inv = dx + 32; double* wt = dx + 64; double* sval = dx + 96;\n"
       << "(void)red; (void)inv; (void)wt; (void)sval;\n";
+  if (bwd && !fwd && fold_end)
+    o << "double* red = reinterpret_cast<double*>(smem + " << L.extra2 << ");\n";
+  if (first && pl->fold) {
+    // initial product state: factor (a0, a1) of every qubit (its folded gates on |0>)
+    o << "C* fz = reinterpret_cast<C*>(smem + " << L.fz << ");\n"
+      << "if (tid < p.n_qubits) { double z[4]; fold_state(p, vs, a.x + vs.b * a.ldx, a.theta, tid, z); "
+         "fz[2 * tid].x = (R)z[0]; fz[2 * tid].y = (R)z[1]; fz[2 * tid + 1].x = (R)z[2]; fz[2 * tid + 1].y = (R)z[3]; }\n"
+      << "auto cm_ = [](C u, C w) { C r; r.x = u.x * w.x - u.y * w.y; r.y = u.x * w.y + u.y * w.x; return r; };\n"
+      << "(void)cm_;\n";
+  }
   o << "load_trig8<R>(a, vs, ps.slots, ps.n_slots, trig, tid, T);\n";
   if (fwd && first) o << "if (p.n_preps > 0) load_prep_values(a, vs, sval, tid, T);\n";
   if (mode == 0 && last)
@@ -804,6 +820,14 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
          "w = (double)(1ull << i); wt[tid] = w; }\n";
   o << "__syncthreads();\n";
   if (fwd && first) o << "if (p.n_preps > 0) prep_norms(a, sval, inv, tid);\n__syncthreads();\n";
+  if (fwd && first && pl->fold) {
+    // tile index j = tid + k·T: thread-bit factor per thread, high-bit factors in a table
+    o << "C fthr_; fthr_.x = (R)1; fthr_.y = (R)0;\n";
+    for (int b = 0; b < tbits; ++b) o << "fthr_ = cm_(fthr_, fz[" << 2 * P.local[b] << " + ((tid >> " << b << ") & 1)]);\n";
+    o << "C* fk_ = fz + 2 * p.n_qubits;\nif (tid < " << (1 << g.RB) << ") { C z; z.x = (R)1; z.y = (R)0;";
+    for (int b = tbits; b < g.Q; ++b) o << " z = cm_(z, fz[" << 2 * P.local[b] << " + ((tid >> " << b - tbits << ") & 1)]);";
+    o << " fk_[tid] = z; }\n__syncthreads();\n";
+  }
   o << "C* gpsi = reinterpret_cast<C*>(ps.psi) + (size_t)vl * ((size_t)1 << p.n_qubits);\n"
     << "C* gout = ps.psi_out ? reinterpret_cast<C*>(ps.psi_out) + (size_t)vl * ((size_t)1 << p.n_qubits) : nullptr;\n"
     << "C* glam = ps.lam ? reinterpret_cast<C*>(ps.lam) + (size_t)vl * ((size_t)1 << p.n_qubits) : nullptr;\n"
@@ -825,7 +849,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
 
   // first-pass backward: stop at the earliest derivative-bearing gate
   int stop_op = 0, stop_win = 0;
-  if (first) {
+  if (first && !fold_end) {
     stop_op = (int)P.wops.size();
     for (int k = 0; k < (int)P.wops.size(); ++k)
       if (P.wops[k].dl >= 0) { stop_op = k; break; }
@@ -864,7 +888,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       const WOp& op = P.wops[k];
       if (adj) {
         if (!(ablate & 4)) g.dot(op, L.per_thread, L.group, nw, reg_acc);
-        if (first && k == stop_op && op.dl >= 0) continue;
+        if (first && !fold_end && k == stop_op && op.dl >= 0) continue;
       }
       const bool uni = op.kind == HQ_GATE_CNOT && !Gen::is_reg(op.a) && (op.a >= 64 || op.a - 16 >= 5);
       if (budget > 0 && uni) {
@@ -966,8 +990,18 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
            "tp[jpad(j)].x = (R)src[2 * g2]; tp[jpad(j)].y = (R)src[2 * g2 + 1]; } }\n"
         << "else if (p.n_preps > 0) { for (uint32_t j = tid; j < (1u << Q); j += T) { const double2 z = "
            "init_amp(a, sval, inv, base | goff_j(j)); tp[jpad(j)].x = (R)z.x; tp[jpad(j)].y = (R)z.y; } }\n"
-        << "else { for (uint32_t j = tid; j < (1u << Q); j += T) { tp[jpad(j)].x = (R)((base | goff_j(j)) == 0); "
-           "tp[jpad(j)].y = (R)0; } } }\n__syncthreads();\n";
+        ;
+      if (pl->fold) {
+        // product state: Π over tile qubits (per amplitude) × Π over the tile id's qubits
+        o << "else { C fb; fb.x = (R)1; fb.y = (R)0;\n";
+        for (size_t i = 0; i < nonlocal.size(); ++i)
+          o << "fb = cm_(fb, fz[" << 2 * nonlocal[i] << " + ((t >> " << i << ") & 1)]);\n";
+        o << "const C f0_ = cm_(fthr_, fb);\nfor (int k = 0; k < " << (1 << g.RB)
+          << "; ++k) tp[jpad((uint32_t)(tid + k * T))] = cm_(f0_, fk_[k]); } }\n__syncthreads();\n";
+      } else {
+        o << "else { for (uint32_t j = tid; j < (1u << Q); j += T) { tp[jpad(j)].x = (R)((base | goff_j(j)) == 0); "
+             "tp[jpad(j)].y = (R)0; } } }\n__syncthreads();\n";
+      }
     } else if (pf) {
       o << "cp_wait();\n__syncthreads();\n";
     } else if (direct_ok(W0)) {
@@ -1100,6 +1134,31 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         emit_steps(ks, 0, true, [&] {
           g.flush_batch();
           g.flush_pending(true);
+          if (fold_end) {
+            // λ at the pass start contracted with the tile's initial factors:
+            // lamN[t] = Σ_i λ[t, i] conj(Π_b fz[LOCAL[b]][bit_b(i)])
+            const std::vector<int> S = Sbits(W), Rr = Rbits(W);
+            o << "{ C wt_; wt_.x = (R)1; wt_.y = (R)0;\n";
+            for (int s2 = 0; s2 < tbits; ++s2)
+              o << "wt_ = cm_(wt_, fz[" << 2 * P.local[S[s2]] << " + ((tid >> " << s2 << ") & 1)]);\n";
+            o << "double sx_ = 0.0, sy_ = 0.0;\n";
+            for (int i = 0; i < g.N; ++i) {
+              o << "{ C w_ = wt_;";
+              for (int r = 0; r < g.RB; ++r) o << " w_ = cm_(w_, fz[" << 2 * P.local[Rr[r]] + ((i >> r) & 1) << "]);";
+              const std::string L_ = g.L(i);
+              o << " sx_ += (double)(w_.x * " << L_ << ".x + w_.y * " << L_ << ".y); sy_ += (double)(w_.x * " << L_
+                << ".y - w_.y * " << L_ << ".x); }\n";
+            }
+            o << "sx_ = warp_sum<double>(sx_); sy_ = warp_sum<double>(sy_);\n";
+            sync();
+            o << "if ((tid & 31) == 0) { red[2 * (tid >> 5)] = sx_; red[2 * (tid >> 5) + 1] = sy_; }\n";
+            sync();
+            o << "if (tid == 0) { double ax = 0.0, ay = 0.0; for (int k = 0; k < " << nw
+              << "; ++k) { ax += red[2 * k]; ay += red[2 * k + 1]; } double* dst = a.lamN + 2 * (vl * ((int64_t)1 << "
+              << nonlocal.size() << ") + (int64_t)t); dst[0] = ax; dst[1] = ay; }\n";
+            sync();
+            o << "}\n";
+          }
           if (first) return;
           if (direct_ok(W)) {
             direct_store(W, true);

@@ -10,7 +10,7 @@
 namespace hq {
 
 struct JitLayout {
-  size_t lut, trig, extra, extra2, total;
+  size_t lut, trig, extra, extra2, fz, total;   // fz: first pass of a folding plan, [n][2] initial factors
   bool per_thread;  // bwd: per-thread derivative accumulators (group == 32)
   int group;        // bwd: derivative partials kept per group of 32/group lanes (1 = per warp)
 };

@@ -15,6 +15,7 @@ struct StreamWs {
   int64_t chunk_samples = 0;  // virtual samples resident per launch
   int32_t n_chunks = 1;       // CTAs per sample per pass
   int32_t ckpt = 0;           // >0: forward passes write ψ checkpoints C_1..C_ckpt out of place
+  void* lamN = nullptr;       // fold_grad: [chunk_samples, 2^(n-q)] complex128 (k_fold_grad input)
 };
 
 struct LaunchIn {

@@ -34,6 +34,14 @@ struct DevPlan {
   const int32_t* rz_slots;
   int32_t n_rot;               // RX/RY gates (their dropped global signs, specialised kernels)
   const int32_t* rot_slots;
+  // folded leading single-qubit gates per qubit (initial product state)
+  int32_t n_fold;
+  const int32_t* fold_ptr;     // [n_qubits + 1]
+  const int32_t* fold_kind;
+  const int32_t* fold_slot;
+  const int32_t* fold_dslot;
+  const int32_t* fold_nonlocal; // first pass's non-local qubits (tile-id bit i -> qubit)
+  int32_t n_fold_nonlocal;
 };
 
 struct KArgs {
@@ -53,6 +61,7 @@ struct KArgs {
   int64_t init_rows;
   const int32_t* prep_off;  // [n_preps] offsets of each prep's values in sval
   int32_t prep_total;
+  double* lamN;             // fold_grad: λ at the first pass's start contracted over its tile, [V, 2^(n-q)] complex
 };
 
 

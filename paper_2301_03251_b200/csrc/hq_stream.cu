@@ -328,6 +328,98 @@ __global__ void __launch_bounds__(256, 2) k_wbwd(KArgs a, SArgs sa) {
 }
 
 // ---------------------------------------------------------------------------
+// Gradients of folded gates (leading single-qubit gates of qubits outside the
+// first pass's tile, applied analytically in the initial product state).
+// With u_p the initial factor of qubit p and lamN[t] = λ at the circuit start
+// contracted over the first pass's tile (written by its backward kernel), the
+// reduced adjoint of folded qubit q is r_q[c] = Σ_{t: bit_q(t)=c} lamN[t]·
+// conj(Π_{p≠q} u_p[bit_p(t)]); for q's j-th folded gate G_j (state after it
+// a = G_j..G_1|0>, y = G_{j+1}^†..G_K^† r_q) the pairwise products are
+// X[b'][b] = a_b·conj(y_b'), and the derivative dot is the passes' formula
+// on X (RY: Re X10 − Re X01; RX: Im X01 + Im X10; RZ: −2 Im X11).
+// One CTA per sample; writes part 0 of each folded derivative slot.
+__global__ void __launch_bounds__(256) k_fold_grad(KArgs a, int64_t v0) {
+  const DevPlan& p = a.p;
+  const int tid = threadIdx.x, T = blockDim.x;
+  const int64_t vl = blockIdx.x, v = v0 + vl;
+  const VSample vs = decode_vsample(p, v, a.B);
+  const double* xr = a.x + vs.b * a.ldx;
+  __shared__ double u[64][4];
+  __shared__ double red[8][4];
+  for (int q = tid; q < p.n_qubits; q += T) fold_state(p, vs, xr, a.theta, q, u[q]);
+  __syncthreads();
+  const int m = p.n_fold_nonlocal;
+  const int64_t NT = 1ll << m;
+  const double* lam = a.lamN + 2 * vl * NT;
+  for (int k = 0; k < m; ++k) {
+    const int q = p.fold_nonlocal[k];
+    bool any = false;
+    for (int j = p.fold_ptr[q]; j < p.fold_ptr[q + 1]; ++j) any |= p.fold_dslot[j] >= 0;
+    if (!any) continue;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t t = tid; t < NT; t += T) {
+      double wr = 1.0, wi = 0.0;
+      for (int i = 0; i < m && (wr != 0.0 || wi != 0.0); ++i) {
+        if (i == k) continue;
+        const double* f = u[p.fold_nonlocal[i]] + 2 * ((t >> i) & 1);
+        const double nr = wr * f[0] - wi * f[1];
+        wi = wr * f[1] + wi * f[0];
+        wr = nr;
+      }
+      const double lr = lam[2 * t], li = lam[2 * t + 1];
+      const int c = (int)((t >> k) & 1);
+      acc[2 * c] += lr * wr + li * wi;
+      acc[2 * c + 1] += li * wr - lr * wi;
+    }
+    for (int c = 0; c < 4; ++c) {
+      double x = acc[c];
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if ((tid & 31) == 0) red[tid >> 5][c] = x;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double r[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int w = 0; w < (T >> 5); ++w)
+        for (int c = 0; c < 4; ++c) r[c] += red[w][c];
+      // states after each folded gate, then the adjoint walk back
+      const int j0 = p.fold_ptr[q], K = p.fold_ptr[q + 1] - j0;
+      double st[33][4];
+      st[0][0] = 1.0; st[0][1] = 0.0; st[0][2] = 0.0; st[0][3] = 0.0;
+      double ang[32];
+      for (int j = 0; j < K; ++j) {
+        const int s = p.fold_slot[j0 + j];
+        ang[j] = s >= 0 ? eval_slot(p, s, xr, a.theta, vs.shvar, vs.shval) : 0.0;
+        for (int c = 0; c < 4; ++c) st[j + 1][c] = st[j][c];
+        apply_1q(p.fold_kind[j0 + j], ang[j], false, st[j + 1]);
+      }
+      double y[4] = {r[0], r[1], r[2], r[3]};
+      for (int j = K - 1; j >= 0; --j) {
+        const int ds = p.fold_dslot[j0 + j];
+        if (ds >= 0) {
+          // X[b'][b] = a_b conj(y_b'), a = st[j + 1]
+          auto X = [&](int bp, int b, double* re, double* im) {
+            const double ar = st[j + 1][2 * b], ai = st[j + 1][2 * b + 1];
+            const double yr = y[2 * bp], yi = -y[2 * bp + 1];
+            *re = ar * yr - ai * yi;
+            *im = ar * yi + ai * yr;
+          };
+          double r10, i10, r01, i01, r11, i11;
+          X(1, 0, &r10, &i10);
+          X(0, 1, &r01, &i01);
+          X(1, 1, &r11, &i11);
+          const int kind = p.fold_kind[j0 + j];
+          const double dot = kind == HQ_GATE_RY ? r10 - r01 : kind == HQ_GATE_RX ? i01 + i10 : -2.0 * i11;
+          double* dst = a.dpart + ((int64_t)v * p.n_adj + ds) * a.n_parts;
+          dst[0] = dot;
+          for (int pp = 1; pp < a.n_parts; ++pp) dst[pp] = 0.0;
+        }
+        apply_1q(p.fold_kind[j0 + j], ang[j], true, y);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 static int rb_of(const hq_plan_s* pl) { return pl->reg_bits; }
 
 static WPass wpass(const hq_plan_s* pl, int i) {
@@ -471,6 +563,10 @@ static cudaError_t run_stream_t(const hq_plan_s* pl, const KArgs& a, const Strea
           } else {
             k_wbwd<R><<<(unsigned)(nv * n_chunks), T, sm, st>>>(a, sa);
           }
+        }
+        if (pl->fold_grad) {
+          ProfScope prof(pl, st, HQ_K_OTHER, (double)nv * 16.0 * (double)n_tiles);
+          k_fold_grad<<<(unsigned)nv, 256, 0, st>>>(a, v0);
         }
       }
       cudaError_t e = cudaGetLastError();
