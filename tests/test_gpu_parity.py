@@ -333,3 +333,105 @@ def test_layer_builds_output_in_the_inputs_graph_module():
     assert type(out) is fake.Tensor and all(type(nd) is fake.GraphNode for nd in out.nodes)
     fake.backward(fake.tsum(out))
     np.testing.assert_allclose(x.grad[:, 0], np.cos([0.4, 1.1]) / 2, atol=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# folded single-qubit prefixes (analytic initial product state, k_fold_grad)
+def _prefix_builder(n, seed, Circ=None):
+    """Random single-qubit prefixes (every rotation its own variable, so the
+    adjoint path differentiates them; inputs feed qubit 0 and qubit n-1), then
+    two RY layers + CNOT chains.  Returns (builder, n_params)."""
+    rng = np.random.default_rng(seed)
+    kinds = ["H", "X", "Y", "Z", "RX", "RY", "RZ"]
+    pre, nxt = [], 0
+    for q in range(n):
+        ops = []
+        for _ in range(int(rng.integers(1, 5))):
+            k = kinds[rng.integers(7)]
+            if k[0] == "R":
+                ops.append((k, nxt)); nxt += 1
+            else:
+                ops.append((k, None))
+        pre.append(ops)
+    n_params = nxt + 2 * n
+
+    def builder(inputs, params, Circ=Circ or Circuit):
+        c = Circ(n)
+        if True:
+            c.ry(0, inputs[0])
+            c.rx(n - 1, inputs[1])
+        for q in range(n):
+            for k, v in pre[q]:
+                if v is None:
+                    getattr(c, k.lower())(q)
+                else:
+                    getattr(c, k.lower())(q, params[v])
+        for layer in range(2):
+            for q in range(n):
+                c.ry(q, params[nxt + layer * n + q])
+            for q in range(n - 1):
+                c.cnot(q, q + 1)
+        c.measure(0, n - 1)
+        return c
+    return builder, n_params
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_folded_prefix_gradients_vs_oracle(prec, monkeypatch):
+    monkeypatch.setenv("HQ_FORCE_STREAM", "1")
+    monkeypatch.setenv("HQ_TILE_BITS", "9")
+    n = 14
+    b, P = _prefix_builder(n, 5)
+    rng = np.random.default_rng(2)
+    x = rng.uniform(-3, 3, (3, 2))
+    th = rng.uniform(0, 6, P)
+    res, jac, info = engine.run_batch(b, x, th, True, True, prec, cache=engine.PlanCache(2))
+    assert "(grad)" in info["plan"].description      # folded gates with derivatives
+    out, jx, jp, _, _ = O.layer(lambda i, p: b(i, p, Circ=O.Circuit), x, th)
+    check_vals(res, out, prec)
+    j = jac.cpu().numpy()
+    check_vals(j[:, :2], jx, prec, grad=True)
+    check_vals(j[:, 2:], jp, prec, grad=True)
+
+
+def test_folded_plan_with_initial_state(monkeypatch):
+    # a caller-provided initial state replaces the folded product state
+    monkeypatch.setenv("HQ_FORCE_STREAM", "1")
+    monkeypatch.setenv("HQ_TILE_BITS", "9")
+    n = 13
+    rng = np.random.default_rng(4)
+    ops = []
+    for q in range(n):
+        ops.append(("RY", (q,), float(rng.uniform(-3, 3))))
+        ops.append(("H", (q,), None))
+    for q in range(n - 1):
+        ops.append(("CNOT", (q, q + 1), None))
+        ops.append(("RZ", (q + 1,), float(rng.uniform(-3, 3))))
+    c = Circuit(n)
+    oc = O.Circuit(n)
+    for k, t, a in ops:
+        (getattr(c, k.lower())(*t, a) if a is not None else getattr(c, k.lower())(*t))
+        oc.add(O.Op(k, t, a))
+    init = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    init /= np.linalg.norm(init)
+    got = engine.final_states([c], "c128", init=init)[0]
+    np.testing.assert_allclose(got, O.simulate(oc, initial=init), atol=1e-10)
+    got0 = engine.final_states([c], "c128")[0]
+    np.testing.assert_allclose(got0, O.simulate(oc), atol=1e-10)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_folding_matches_unfolded(prec, monkeypatch):
+    monkeypatch.setenv("HQ_FORCE_STREAM", "1")
+    monkeypatch.setenv("HQ_TILE_BITS", "9")
+    b, P = _prefix_builder(14, 9)
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-3, 3, (4, 2))
+    th = rng.uniform(0, 6, P)
+    r1, j1, i1 = engine.run_batch(b, x, th, True, True, prec, cache=engine.PlanCache(2))
+    monkeypatch.setenv("HQ_NO_FOLD", "1")
+    r0, j0, i0 = engine.run_batch(b, x, th, True, True, prec, cache=engine.PlanCache(2))
+    assert "folded=0" in i0["plan"].description and "folded=0" not in i1["plan"].description
+    tol = 1e-10 if prec == "c128" else 2e-5
+    np.testing.assert_allclose(r1, r0, atol=tol)
+    np.testing.assert_allclose(j1.cpu().numpy(), j0.cpu().numpy(), atol=tol * 10)
