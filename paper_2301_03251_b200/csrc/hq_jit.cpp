@@ -471,7 +471,8 @@ struct Gen {
       bq.push_back(op.dl);
       bgroup = group;
       bnw = nw;
-      if (bq.size() == 8) flush_batch();
+      bstride = nw * group + 4;
+      if ((int)bq.size() == bmax) flush_batch();
     }
   }
 
@@ -481,7 +482,8 @@ struct Gen {
   // K·log2(32/G); the remaining lane bits above the group are summed, and each
   // lane then updates one (slot, group) partial.
   std::vector<int> bq;
-  int bgroup = 4, bnw = 8;
+  int bgroup = 4, bnw = 8, bstride = 36;
+  int bmax = std::getenv("HQ_DOT_BATCH") ? std::max(1, std::min(8, std::atoi(std::getenv("HQ_DOT_BATCH")))) : 8;
   void flush_batch() {
     if (bq.empty()) return;
     const int K = (int)bq.size();
@@ -517,7 +519,7 @@ struct Gen {
     for (int lv = 0; lv < Lv; ++lv) o << " + ((ln_ & " << split_m[lv] << "u) ? " << (1 << (Lv - 1 - lv)) << " : 0)";
     o << ";\nint s_ = " << bq[0] << ";";
     for (int j = 1; j < K; ++j) o << " if (d_ == " << j << ") s_ = " << bq[j] << ";";
-    o << "\nif (d_ < " << K << " && (ln_ & " << red << "u) == 0) dacc[(s_ * " << bnw << " + (tid >> 5)) * " << bgroup
+    o << "\nif (d_ < " << K << " && (ln_ & " << red << "u) == 0) dacc[s_ * " << bstride << " + (tid >> 5) * " << bgroup
       << " + (ln_ & " << (bgroup - 1) << "u)] += z_; }\n";
     bq.clear();
   }
@@ -650,7 +652,10 @@ JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd, bool fused) {
     while (L.group > 1 && (size_t)P.n_dslots_pass * (T / 32) * L.group * rsz > 40 * 1024) L.group >>= 1;
     L.per_thread = L.group == 32;
     if (!L.per_thread) L.group = std::min(L.group, 4);   // batched reduction keeps 4 partials per warp
-    o = a16(o + (size_t)P.n_dslots_pass * (T / 32) * L.group * rsz);
+    // group mode: a batch updates 8 slots at once; a stride of nw·G + 4 puts
+    // consecutive slots on different banks
+    L.slot_stride = L.per_thread ? T : (T / 32) * L.group + 4;
+    o = a16(o + (size_t)P.n_dslots_pass * L.slot_stride * rsz);
   }
   L.extra2 = o;
   if (!bwd || fused || (i == 0 && pl->fold_grad))
@@ -793,7 +798,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   o << ";\n(void)ot;\n";
   if (bwd)
     o << "R* dacc = reinterpret_cast<R*>(smem + " << L.extra << ");\n"
-      << "for (int i = tid; i < " << P.n_dslots_pass * nw * L.group << "; i += T) dacc[i] = (R)0;\n";
+      << "for (int i = tid; i < " << P.n_dslots_pass * L.slot_stride << "; i += T) dacc[i] = (R)0;\n";
   if (fwd)
     o << "double* dx = reinterpret_cast<double*>(smem + " << L.extra2 << ");\n"
       << "double* red = dx; double* inv = dx + 32; double* wt = dx + 64; double* sval = dx + 96;\n"
@@ -1193,12 +1198,12 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   if (fwd && last)
     o << "e = block_sum<R>(e, red, tid, T);\nif (tid == 0) ps.rpart[vl * ps.n_chunks + chunk] = e;\n";
   if (bwd) {
-    const int stride = nw * L.group;
+    const int width = nw * L.group;
     for (int k = 0; k < reg_acc; ++k) o << "dacc[" << k << " * T + tid] = da" << k << ";\n";
     // one warp per slot: lanes sum strided partials in double, then a shuffle tree
     o << "__syncthreads();\n{ const int lane_ = tid & 31;\nfor (int i = tid >> 5; i < " << P.n_dslots_pass
-      << "; i += " << nw << ") { double s = 0.0; for (int k = lane_; k < " << stride
-      << "; k += 32) s += (double)dacc[i * " << stride << " + k]; s = warp_sum<double>(s); "
+      << "; i += " << nw << ") { double s = 0.0; for (int k = lane_; k < " << width
+      << "; k += 32) s += (double)dacc[i * " << L.slot_stride << " + k]; s = warp_sum<double>(s); "
       << "if (lane_ == 0) a.dpart[((int64_t)v * p.n_adj + ps.dlist[i]) * a.n_parts + chunk] = s; } }\n";
   }
   o << "}\n";

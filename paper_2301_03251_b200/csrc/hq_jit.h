@@ -13,6 +13,7 @@ struct JitLayout {
   size_t lut, trig, extra, extra2, fz, total;   // fz: first pass of a folding plan, [n][2] initial factors
   bool per_thread;  // bwd: per-thread derivative accumulators (group == 32)
   int group;        // bwd: derivative partials kept per group of 32/group lanes (1 = per warp)
+  int slot_stride;  // bwd: floats between derivative slots' partials (padded in group mode: no bank conflicts)
 };
 
 JitLayout jit_layout(const hq_plan_s* pl, int pass, bool bwd, bool fused = false);
