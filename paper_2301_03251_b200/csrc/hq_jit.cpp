@@ -884,6 +884,11 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   int ubudget = 2;
   if (const char* e = std::getenv("HQ_UBRANCH")) ubudget = std::atoi(e);
   if (fused) ubudget = 0;
+  if (first) {
+    // the first pass is one long kernel: code size (instruction-cache misses) matters more
+    ubudget = std::min(ubudget, 1);
+    if (const char* e = std::getenv("HQ_UBRANCH0")) ubudget = std::atoi(e);
+  }
   bool na = false;
   auto sync = [&]() { o << (na ? "bar_na();\n" : "__syncthreads();\n"); };
   std::function<void(const std::vector<int>&, size_t, bool, const std::function<void()>&, int)> emit_steps;
