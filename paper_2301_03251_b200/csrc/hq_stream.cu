@@ -337,11 +337,13 @@ __global__ void __launch_bounds__(256, 2) k_wbwd(KArgs a, SArgs sa) {
 // a = G_j..G_1|0>, y = G_{j+1}^†..G_K^† r_q) the pairwise products are
 // X[b'][b] = a_b·conj(y_b'), and the derivative dot is the passes' formula
 // on X (RY: Re X10 − Re X01; RX: Im X01 + Im X10; RZ: −2 Im X11).
-// One CTA per sample; writes part 0 of each folded derivative slot.
+// One CTA per (sample, non-tile qubit); writes part 0 of each folded
+// derivative slot of that qubit.
 __global__ void __launch_bounds__(256) k_fold_grad(KArgs a, int64_t v0) {
   const DevPlan& p = a.p;
   const int tid = threadIdx.x, T = blockDim.x;
-  const int64_t vl = blockIdx.x, v = v0 + vl;
+  const int64_t vl = blockIdx.x / p.n_fold_nonlocal, v = v0 + vl;
+  const int kq = (int)(blockIdx.x - vl * p.n_fold_nonlocal);
   const VSample vs = decode_vsample(p, v, a.B);
   const double* xr = a.x + vs.b * a.ldx;
   __shared__ double u[64][4];
@@ -351,11 +353,12 @@ __global__ void __launch_bounds__(256) k_fold_grad(KArgs a, int64_t v0) {
   const int m = p.n_fold_nonlocal;
   const int64_t NT = 1ll << m;
   const double* lam = a.lamN + 2 * vl * NT;
-  for (int k = 0; k < m; ++k) {
+  {
+    const int k = kq;
     const int q = p.fold_nonlocal[k];
     bool any = false;
     for (int j = p.fold_ptr[q]; j < p.fold_ptr[q + 1]; ++j) any |= p.fold_dslot[j] >= 0;
-    if (!any) continue;
+    if (!any) return;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t t = tid; t < NT; t += T) {
       double wr = 1.0, wi = 0.0;
@@ -566,7 +569,7 @@ static cudaError_t run_stream_t(const hq_plan_s* pl, const KArgs& a, const Strea
         }
         if (pl->fold_grad) {
           ProfScope prof(pl, st, HQ_K_OTHER, (double)nv * 16.0 * (double)n_tiles);
-          k_fold_grad<<<(unsigned)nv, 256, 0, st>>>(a, v0);
+          k_fold_grad<<<(unsigned)(nv * pl->dev.n_fold_nonlocal), 256, 0, st>>>(a, v0);
         }
       }
       cudaError_t e = cudaGetLastError();
