@@ -74,7 +74,10 @@ int popc(uint64_t m) { return __builtin_popcountll(m); }
 
 size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
 
-int onchip_max_qubits(int precision) { return precision == HQ_C64 ? 13 : 12; }
+int onchip_max_qubits(int precision) {
+  if (const char* e = std::getenv("HQ_ONCHIP_MAX")) return std::atoi(e);   // test hook
+  return precision == HQ_C64 ? 13 : 12;
+}
 int tile_bits_for(int precision) { return precision == HQ_C64 ? 12 : 11; }
 int fixed_bits_for(int precision) {
   if (const char* e = std::getenv("HQ_FIXED_BITS")) return std::atoi(e);   // test hook
@@ -433,10 +436,13 @@ const T* rebase(const T* rel, char* base) {
 
 }  // namespace
 
-static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, bool allow_fold);
+// opts: kNoFold (no folded prefixes), kOnchipOk (small circuits may use the
+// shared-memory interpreter when the specialised kernels are unavailable)
+enum { kNoFold = 1, kPreferOnchip = 2 };
+static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts);
 
 extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
-  return plan_create_impl(d, out, true);
+  return plan_create_impl(d, out, 0);
 }
 
 namespace {
@@ -489,7 +495,8 @@ bool single_qubit(int k) {
 constexpr int kMaxFoldPerQubit = 32;
 }  // namespace
 
-static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, bool allow_fold) {
+static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts) {
+  const bool allow_fold = !(opts & kNoFold);
   if (!out) return fail(HQ_E_CONFIG, "null output");
   *out = nullptr;
   hq_status st = validate(d);
@@ -566,7 +573,14 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, bool allo
   // the multi-pass HBM path (parity of the pass planner against the oracle)
   const char* force = std::getenv("HQ_FORCE_STREAM");
   const char* tb_env = std::getenv("HQ_TILE_BITS");
-  pl->onchip = n <= onchip_max_qubits(d->precision) && !(force && force[0] == '1');
+  // Shared-memory interpreter (k_onchip) only for circuits too small for the
+  // specialised streaming kernels (tile >= 2^(RB+5) amplitudes): from 9 (c64) /
+  // 8 (c128) qubits the whole state is one tile of a single fused
+  // forward+backward kernel, 3-7x faster than the interpreter (n = 9..13,
+  // tools/onchip_vs_stream.py).  Without NVRTC the interpreter takes over.
+  const int stream_min = reg_bits_for(d->precision) + 5;
+  pl->onchip = n <= onchip_max_qubits(d->precision) && !(force && force[0] == '1') &&
+               (n < stream_min || (opts & kPreferOnchip));
   std::vector<int32_t> pass_slots, pass_dlist, pass_local;
   if (pl->onchip) {
     pl->tile_bits = n;
@@ -585,7 +599,7 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, bool allo
     pl->dops.clear();
     pl->tile_bits = tile_bits_for(d->precision);
     if (tb_env) pl->tile_bits = std::max(3, std::min(14, std::atoi(tb_env)));
-    if (n <= pl->tile_bits) pl->tile_bits = n - 1;
+    if (n < pl->tile_bits) pl->tile_bits = n;   // whole state in one tile
     if (pl->tile_bits < 2) {
       delete pl;
       return fail(HQ_E_CONFIG, "circuit too small for the streaming path");
@@ -730,11 +744,11 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, bool allo
       delete pl;
       return fail(HQ_E_CONFIG, "HQ_REG_BITS needs the specialised kernels: " + why);
     }
-    if (js != HQ_OK && pl->fold) {
-      // folding needs the specialised kernels
+    if (js != HQ_OK && !(opts & kPreferOnchip) && (pl->fold || n <= onchip_max_qubits(d->precision))) {
+      // folding needs the specialised kernels; small circuits fall back to the interpreter
       delete pl;
       if (std::getenv("HQ_JIT_COMPILE_ONLY")) return fail(HQ_E_CONFIG, why);
-      return plan_create_impl(d, out, false);
+      return plan_create_impl(d, out, opts | kNoFold | kPreferOnchip);
     }
     if (js != HQ_OK) {
       pl->jit.ok = false;
@@ -929,7 +943,7 @@ static hq_status run(hq_plan pl, const double* x, int64_t ldx, const double* the
     // the same tape unfolded (same workspace layout for hq_state)
     if (!pl->twin) {
       hq_plan tw = nullptr;
-      const hq_status st = plan_create_impl(&static_cast<DescCopy*>(pl->desc_copy.get())->d, &tw, false);
+      const hq_status st = plan_create_impl(&static_cast<DescCopy*>(pl->desc_copy.get())->d, &tw, kNoFold);
       if (st != HQ_OK) return st;
       pl->twin = tw;
     }
