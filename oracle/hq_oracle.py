@@ -21,6 +21,10 @@ Restated pieces (file:line in the reference):
 * ``QuantumLayer.forward`` + df_x/df_p  qnn.py:123-154
 * templates (embeddings, cry/crz, ccz/toffoli/cswap)   templates.py:16-143
 * ``Circuit`` builder API + validation  qsim.py:48-140
+* SHOT_SAMPLING draws (Philox4x64-10 per shot)          qsim.py:222-248
+* NOISY trajectories: channels, NoiseModel, apply_channel, run_trajectory,
+  simulate_noisy, NoiseQuantumLayer values + shift-rule gradients
+                                        noise.py:23-153, qnn.py:107-111,157-166
 
 The reference has no compiled code (it is pure Python + NumPy),
 so there is no ``oracle/_ref`` build; ``oracle/Makefile`` is a no-op.
@@ -402,3 +406,143 @@ def shot_expectation(circuit, shots, seed):
     qubits = list(circuit.measured_qubits) or list(range(circuit.n_qubits))
     counts = measure_shots(simulate(circuit), circuit.n_qubits, qubits, shots, seed)
     return sum(int(k, 2) * c for k, c in counts.items()) / shots
+
+
+# ---------------------------------------------------------------------------
+# NOISY machine type: per-shot Kraus trajectories (noise.py:1-153)
+def philox_draw(seed, shot, k):
+    """k-th ``random()`` of np.random.Generator(np.random.Philox(key=[seed, shot])):
+    block b = k // 4 uses counter b + 1 (the counter is bumped before every
+    block), output word k % 4, (w >> 11)·2^-53 (numpy philox4x64 buffering)."""
+    b, wsel = divmod(int(k), 4)
+    c = [(b + 1) & _MASK, 0, 0, 0]
+    key = [seed & _MASK, shot & _MASK]
+    for r in range(10):
+        if r:
+            key = [(key[0] + _W0) & _MASK, (key[1] + _W1) & _MASK]
+        p0, p1 = _M0 * c[0], _M1 * c[2]
+        c = [(p1 >> 64) ^ c[1] ^ key[0], p1 & _MASK, (p0 >> 64) ^ c[3] ^ key[1], p0 & _MASK]
+    return (c[wsel] >> 11) * (1.0 / 9007199254740992.0)
+
+
+CHANNEL_NAMES = ("bit_flip", "phase_flip", "depolarizing", "amplitude_damping")
+
+
+@dataclass(frozen=True)
+class Channel:
+    """noise.py:23-34."""
+    name: str
+    param: float
+
+    def __post_init__(self):
+        if self.name not in CHANNEL_NAMES:
+            raise OracleError(f"unknown channel {self.name!r}")
+        if not 0.0 <= self.param <= 1.0:
+            raise OracleError(f"{self.name} parameter {self.param} outside [0, 1]")
+
+
+class NoiseModel:
+    """Gate kind (optionally per qubit) -> channel list (noise.py:54-78)."""
+
+    def __init__(self):
+        self.by_kind, self.by_kind_qubit = {}, {}
+
+    def add(self, kind, channel, qubit=None):
+        if qubit is None:
+            self.by_kind.setdefault(kind, []).append(channel)
+        else:
+            self.by_kind_qubit.setdefault((kind, int(qubit)), []).append(channel)
+        return self
+
+    def channels_for(self, kind, qubit):
+        ov = self.by_kind_qubit.get((kind, qubit))
+        return ov if ov is not None else self.by_kind.get(kind, [])
+
+
+class _ShotStream:
+    """Sequential draws of one shot's Philox substream (qsim.py:222-224)."""
+
+    def __init__(self, seed, shot):
+        self.seed, self.shot, self.k = seed, shot, 0
+
+    def random(self):
+        u = philox_draw(self.seed, self.shot, self.k)
+        self.k += 1
+        return u
+
+
+def apply_channel(psi, n, qubit, ch, rng):
+    """One Kraus jump in place; zero-parameter channels draw nothing (noise.py:93-127)."""
+    p = ch.param
+    if p == 0.0:
+        return
+    if ch.name == "bit_flip":
+        if rng.random() < p:
+            apply_gate(psi, n, Op("X", (qubit,)))
+    elif ch.name == "phase_flip":
+        if rng.random() < p:
+            apply_gate(psi, n, Op("Z", (qubit,)))
+    elif ch.name == "depolarizing":
+        u = rng.random()
+        if u < 0.75 * p:
+            apply_gate(psi, n, Op("XYZ"[int(u // (0.25 * p))], (qubit,)))
+    else:  # amplitude_damping
+        v = _pair_view(psi, n, qubit)
+        p_jump = p * float((np.abs(v[:, 1, :]) ** 2).sum())
+        if rng.random() < p_jump:
+            v[:, 0, :] = np.sqrt(p) * v[:, 1, :]
+            v[:, 1, :] = 0.0
+            norm = np.sqrt(p_jump)
+        else:
+            v[:, 1, :] = np.sqrt(1.0 - p) * v[:, 1, :]
+            norm = np.sqrt(1.0 - p_jump)
+        if norm > 0:
+            psi /= norm
+
+
+def run_trajectory(circuit, noise, rng):
+    """noise.py:130-138: channels act after each gate on every qubit it touched."""
+    n = int(circuit.n_qubits)
+    psi = np.zeros(1 << n, dtype=np.complex128)
+    psi[0] = 1.0
+    for op in circuit.ops:
+        apply_gate(psi, n, op)
+        for q in op.targets:
+            for ch in noise.channels_for(op.kind, q):
+                apply_channel(psi, n, q, ch, rng)
+    return psi
+
+
+def simulate_noisy(circuit, noise, shots, seed):
+    """Counts dict of per-shot trajectories, one final draw each (noise.py:141-153)."""
+    qubits = list(circuit.measured_qubits) or list(range(circuit.n_qubits))
+    tally = {}
+    for s in range(shots):
+        rng = _ShotStream(seed, s)
+        psi = run_trajectory(circuit, noise, rng)
+        cum = np.cumsum(probabilities(psi, circuit.n_qubits, qubits))
+        idx = min(int(np.searchsorted(cum, rng.random(), side="right")), len(cum) - 1)
+        key = format(idx, f"0{len(qubits)}b")
+        tally[key] = tally.get(key, 0) + 1
+    return tally
+
+
+def noisy_expectation(circuit, noise, shots, seed):
+    """qnn.py:107-111 + expectation_from_counts (qnn.py:27-32)."""
+    counts = simulate_noisy(circuit, noise, shots, seed)
+    return sum(int(k, 2) * c for k, c in counts.items()) / shots
+
+
+def noisy_layer(builder, x, theta, noise, shots, seed, want_x=True, want_p=True,
+                shift=math.pi / 2, grad_scale=0.5):
+    """NoiseQuantumLayer forward + shift-rule jacobians (qnn.py:123-166)."""
+    x = np.asarray(x, dtype=np.float64)
+    theta = np.asarray(theta, dtype=np.float64)
+    ex = lambda i, p: noisy_expectation(builder([float(v) for v in i], [float(v) for v in p]),
+                                        noise, shots, seed)
+    out = np.array([ex(x[i], theta) for i in range(len(x))])
+    jx = np.array([parameter_shift_grad(lambda v: ex(v, theta), x[i], shift, grad_scale, 1.0)
+                   if want_x else np.zeros(x.shape[1]) for i in range(len(x))])
+    jp = np.array([parameter_shift_grad(lambda v: ex(x[i], v), theta, shift, grad_scale, 1.0)
+                   if want_p and theta.size else np.zeros(theta.size) for i in range(len(x))])
+    return out, jx, jp

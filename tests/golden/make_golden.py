@@ -196,8 +196,81 @@ def embedding_case():
          sizes=np.array([v.size for v in vecs]), states=np.array(out))
 
 
+def noise_cases():
+    # simulate_noisy counts (noise.py:141-153) and NoiseQuantumLayer values /
+    # shift-rule gradients (qnn.py:157-166) for mixed channel models
+    import hyqnet.noise as rn
+    from hyqnet.qnn import NoiseQuantumLayer
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from conftest import random_circuit
+    rng = np.random.default_rng(2024)
+    models = []
+
+    def model(spec):
+        m = rn.NoiseModel()
+        for kind, name, p, q in spec:
+            m.add(kind, rn.Channel(name, p), q)
+        return m
+    specs = [
+        [("H", "bit_flip", 0.2, None), ("CNOT", "phase_flip", 0.3, None), ("RY", "depolarizing", 0.4, None)],
+        [("RX", "amplitude_damping", 0.35, None), ("RY", "amplitude_damping", 0.5, None),
+         ("CNOT", "depolarizing", 0.25, None), ("X", "bit_flip", 0.0, None)],
+        [("RZ", "phase_flip", 0.15, None), ("H", "depolarizing", 1.0, None), ("CZ", "bit_flip", 0.4, 0),
+         ("CZ", "amplitude_damping", 0.6, None), ("SWAP", "bit_flip", 0.1, None)],
+        [("RY", "depolarizing", 0.3, 1), ("RY", "bit_flip", 0.05, None), ("CR", "amplitude_damping", 0.2, None),
+         ("Y", "phase_flip", 0.5, None), ("Z", "depolarizing", 0.6, None), ("RX", "bit_flip", 0.3, None)],
+    ]
+    kinds, q0, q1, ang, starts, nq, shots, seeds, midx = [], [], [], [], [0], [], [], [], []
+    extra = {}
+    k = 0
+    for trial in range(8):
+        n = int(rng.integers(1, 6))
+        c = random_circuit(rng, n, int(rng.integers(3, 20)))
+        for op in c.ops:
+            kinds.append(op.kind)
+            q0.append(op.targets[0])
+            q1.append(op.targets[1] if len(op.targets) > 1 else -1)
+            ang.append(np.nan if op.angle is None else op.angle)
+        starts.append(len(kinds))
+        nq.append(n)
+        S, seed = int(rng.integers(50, 300)), int(rng.integers(0, 1000))
+        mi = trial % len(specs)
+        shots.append(S); seeds.append(seed); midx.append(mi)
+        counts = rn.simulate_noisy(c, model(specs[mi]), S, seed)
+        extra[f"keys{trial}"] = np.array(list(counts.keys()))
+        extra[f"vals{trial}"] = np.array(list(counts.values()))
+    spec_arr = np.array([(i, kd, nm, p, -1 if q is None else q) for i, sp in enumerate(specs)
+                         for kd, nm, p, q in sp], dtype=object)
+
+    def builder(inputs, params):
+        c = rq.Circuit(3)
+        c.ry(0, inputs[0])
+        c.rx(1, inputs[1])
+        c.h(2)
+        c.cnot(0, 1)
+        c.ry(1, params[0])
+        c.rz(2, params[1])
+        c.cnot(1, 2)
+        c.rx(0, params[2])
+        c.measure(0, 2)
+        return c
+    x = rng.uniform(-2, 2, (3, 2))
+    theta = rng.uniform(0, 6, 3)
+    lay = NoiseQuantumLayer(builder, 3, model(specs[1]), shots=64, seed=11, param_init=theta)
+    xt = Tensor(x, requires_grad=True, dtype=np.float64)
+    g = rng.uniform(0.5, 1.5, (3, 1))
+    out = lay(xt)
+    backward(tsum(out * Tensor(g, dtype=np.float64)))
+    save("noise", kinds=np.array(kinds), q0=np.array(q0), q1=np.array(q1), angle=np.array(ang),
+         starts=np.array(starts), n_qubits=np.array(nq), shots=np.array(shots), seed=np.array(seeds),
+         model=np.array(midx), specs=spec_arr.astype(str), layer_x=x, layer_theta=theta,
+         layer_upstream=g[:, 0], layer_out=out.numpy()[:, 0], layer_grad_x=xt.grad,
+         layer_grad_p=lay.params.grad, **extra)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "cfg4", "random", "reupload", "qae", "embed", "shots"]
+    which = sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "cfg4", "random", "reupload", "qae", "embed", "shots",
+                             "noise"]
     if "cfg1" in which:
         layer_case("cfg1", "cfg1", 16, True)
     if "cfg2" in which:
@@ -216,3 +289,5 @@ if __name__ == "__main__":
         embedding_case()
     if "shots" in which:
         shots_case()
+    if "noise" in which:
+        noise_cases()

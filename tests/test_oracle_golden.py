@@ -145,3 +145,54 @@ def _hry(theta):
 
 def _circuits_from(g):
     return _circuits({k: g[k] for k in ("kinds", "q0", "q1", "angle", "starts", "n_qubits")})
+
+
+# ---------------------------------------------------------------------------
+# NOISY trajectories (noise.py) — counts and NoiseQuantumLayer values/gradients
+def noise_models(g):
+    models = {}
+    for i, kind, name, p, q in g["specs"]:
+        m = models.setdefault(int(i), O.NoiseModel())
+        m.add(str(kind), O.Channel(str(name), float(p)), None if int(q) < 0 else int(q))
+    return models
+
+
+def noise_layer_builder(Circ):
+    def builder(inputs, params):
+        c = Circ(3)
+        c.ry(0, inputs[0])
+        c.rx(1, inputs[1])
+        c.h(2)
+        c.cnot(0, 1)
+        c.ry(1, params[0])
+        c.rz(2, params[1])
+        c.cnot(1, 2)
+        c.rx(0, params[2])
+        c.measure(0, 2)
+        return c
+    return builder
+
+
+def test_philox_stream_matches_numpy():
+    for seed, shot in ((0, 0), (7, 3), (2**40 + 5, 123456)):
+        gen = np.random.Generator(np.random.Philox(key=[seed, shot]))
+        assert [gen.random() for _ in range(13)] == [O.philox_draw(seed, shot, k) for k in range(13)]
+
+
+def test_noisy_counts_golden():
+    g = golden("noise")
+    models = noise_models(g)
+    for k, c in enumerate(_circuits_from(g)):
+        counts = O.simulate_noisy(c, models[int(g["model"][k])], int(g["shots"][k]), int(g["seed"][k]))
+        want = {str(key): int(v) for key, v in zip(g[f"keys{k}"], g[f"vals{k}"])}
+        assert counts == want, k
+
+
+def test_noisy_layer_golden():
+    g = golden("noise")
+    m = noise_models(g)[1]
+    out, jx, jp = O.noisy_layer(noise_layer_builder(O.Circuit), g["layer_x"], g["layer_theta"], m, 64, 11)
+    up = g["layer_upstream"]
+    assert list(out) == list(g["layer_out"])
+    np.testing.assert_allclose(jx * up[:, None], g["layer_grad_x"], atol=1e-14)
+    np.testing.assert_allclose((jp * up[:, None]).sum(0), g["layer_grad_p"], atol=1e-13)
