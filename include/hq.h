@@ -20,6 +20,10 @@
  *                    df_x / df_p (qnn.py:137-152).
  *   hq_state         replaces simulate() returning the amplitudes
  *                    (qsim.py:179-191), for StateVector-level parity tests.
+ *   hq_sample        replaces measure_shots (qsim.py:236-248) / SHOT_SAMPLING.
+ *   hq_noisy         replaces simulate_noisy (noise.py:141-153) / the NOISY
+ *                    machine type (qnn.py:109-111, NoiseQuantumLayer
+ *                    qnn.py:157-166) with its shift-rule gradients.
  *
  * Conventions (all pinned by the reference tests): qubit k is
  * bit k of the amplitude index; rotations are half-angle; CR(θ) multiplies
@@ -43,7 +47,7 @@
 extern "C" {
 #endif
 
-#define HQ_ABI_VERSION 1
+#define HQ_ABI_VERSION 2
 
 typedef struct hq_plan_s* hq_plan;
 
@@ -158,6 +162,34 @@ hq_status hq_sample(const double* state, int64_t rows, int32_t n_qubits, const i
 
 /* u_s for s in [shot0, shot0 + count): the per-shot uniform stream of shot_rng (qsim.py:222-224) */
 hq_status hq_shot_uniforms(uint64_t seed, int64_t shot0, int64_t count, double* out, void* stream);
+
+/* ---- NOISY machine type: per-shot Kraus trajectories (noise.py) ---------- */
+
+enum { HQ_CH_BIT_FLIP = 0, HQ_CH_PHASE_FLIP = 1, HQ_CH_DEPOLARIZING = 2, HQ_CH_AMP_DAMPING = 3 };
+
+/* One channel application: after tape op `op`, on `qubit` (one of the op's
+ * targets), in the order the reference visits them (noise.py:130-138: op order,
+ * then the op's targets, then the model's channel list).  Sites with param 0
+ * draw nothing (noise.py:99) and may be omitted. */
+typedef struct {
+  int32_t op, qubit, channel;
+  double param;
+} hq_noise_site;
+
+size_t hq_noisy_workspace_bytes(hq_plan plan, int64_t batch, int32_t flags, int32_t n_sites);
+
+/* simulate_noisy for every (virtual) sample (noise.py:141-153): `shots`
+ * trajectories from |0...0>, shot s drawing from Philox4x64-10(key=[seed, s])
+ * (one draw per non-zero channel application, one final outcome draw).
+ * out[b] = Σ outcome / shots (qnn.py:27-32); HQ_WANT_JAC: jac rows by the
+ * two-point rule on the same streams (every differentiated variable must be
+ * HQ_GRAD_TWOPOINT); counts (optional) [batch, 2^m] uint64.  Complex128
+ * state; circuits up to 13 qubits without state loads.
+ * Replaces: qnn.py:109-111 (NOISY _execute) and its shift-rule closures. */
+hq_status hq_noisy(hq_plan plan, const double* x, int64_t ldx, const double* theta, int64_t batch,
+                   int32_t flags, const hq_noise_site* sites, int32_t n_sites, int64_t shots, uint64_t seed,
+                   double* out, double* jac, uint64_t* counts, void* workspace, size_t workspace_bytes,
+                   void* stream);
 
 /* ---- introspection / measurement ---------------------------------------- */
 

@@ -15,7 +15,9 @@ from .qsim import (MAX_QUBITS, Circuit, Counts, GateOp, StatePrepOp, StateVector
                    format_circuit_text, gate_matrix, parse_circuit_text, probabilities, simulate)
 from .templates import (amplitude_embedding, angle_embedding, basis_embedding, ccz, cry, crz,
                         cswap, toffoli)
-from .qnn import (EXACT_PROB, NOISY, SHOT_SAMPLING, QAELayer, QuantumLayer,
+from .qnn import (EXACT_PROB, NOISY, SHOT_SAMPLING, NoiseQuantumLayer, QAELayer, QuantumLayer,
                   expectation_from_counts, measure_shots, parameter_shift_grad, shot_rng)
+from .noise import (CHANNEL_NAMES, Channel, NoiseModel, amplitude_damping, bit_flip, depolarizing,
+                    phase_flip, simulate_noisy)
 
 __version__ = "0.1.0"

@@ -22,7 +22,7 @@ KIND_CODE = {"H": 0, "X": 1, "Y": 2, "Z": 3, "RX": 4, "RY": 5, "RZ": 6, "CNOT": 
 EXPORTS = ("hq_abi_version", "hq_last_error", "hq_plan_create", "hq_plan_destroy",
            "hq_plan_describe", "hq_workspace_bytes", "hq_forward", "hq_vjp", "hq_state",
            "hq_stats", "hq_profile_enable", "hq_profile_read", "hq_sample_workspace_bytes", "hq_sample",
-           "hq_shot_uniforms")
+           "hq_shot_uniforms", "hq_noisy_workspace_bytes", "hq_noisy")
 K_CLASSES = ("onchip", "pass_fwd", "pass_bwd", "other")
 
 
@@ -47,6 +47,14 @@ class HqPlanDesc(ctypes.Structure):
         ("grad_mode", _P), ("grad_slot", _P), ("grad_factor", _P),
         ("shift", ctypes.c_double), ("grad_scale", ctypes.c_double),
     ]
+
+
+class HqNoiseSite(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int32), ("qubit", ctypes.c_int32), ("channel", ctypes.c_int32),
+                ("param", ctypes.c_double)]
+
+
+CHANNEL_CODE = {"bit_flip": 0, "phase_flip": 1, "depolarizing": 2, "amplitude_damping": 3}
 
 
 class HqStats(ctypes.Structure):
@@ -103,8 +111,13 @@ def lib():
     h.hq_sample.restype = ctypes.c_int
     h.hq_shot_uniforms.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, _P, _P]
     h.hq_shot_uniforms.restype = ctypes.c_int
-    if h.hq_abi_version() != 1:
-        raise NativeError(f"libhq ABI {h.hq_abi_version()} != 1")
+    h.hq_noisy_workspace_bytes.argtypes = [_P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32]
+    h.hq_noisy_workspace_bytes.restype = ctypes.c_size_t
+    h.hq_noisy.argtypes = [_P, _P, ctypes.c_int64, _P, ctypes.c_int64, ctypes.c_int32, _P, ctypes.c_int32,
+                           ctypes.c_int64, ctypes.c_uint64, _P, _P, _P, _P, ctypes.c_size_t, _P]
+    h.hq_noisy.restype = ctypes.c_int
+    if h.hq_abi_version() != 2:
+        raise NativeError(f"libhq ABI {h.hq_abi_version()} != 2")
     _lib = h
     return h
 

@@ -160,6 +160,10 @@ Layout layout_for(const hq_plan_s* pl, int64_t B, int32_t flags, bool need_state
 
 }  // namespace
 
+namespace hq {
+hq_status fail_status(hq_status s, const std::string& msg) { return fail(s, msg); }
+}  // namespace hq
+
 extern "C" int hq_abi_version(void) { return HQ_ABI_VERSION; }
 extern "C" const char* hq_last_error(void) { return g_err.c_str(); }
 
@@ -835,6 +839,8 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
   const hq::WOp* r_wops;
   put(blob, off, all_wins.data(), all_wins.size(), r_wins);
   put(blob, off, all_wops.data(), all_wops.size(), r_wops);
+  const hq_op* r_tape;
+  put(blob, off, d->ops, (size_t)d->n_ops, r_tape);
   const int32_t *r_rz, *r_rot, *r_fptr, *r_fkind, *r_fslot, *r_fdsl, *r_fnl;
   put(blob, off, rz_slots.data(), rz_slots.size(), r_rz);
   put(blob, off, rot_slots.data(), rot_slots.size(), r_rot);
@@ -905,6 +911,8 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
   dv.fold_nonlocal = rebase(r_fnl, base);
   dv.n_fold_nonlocal = (int32_t)fold_nl.size();
   pl->dev = dv;
+  pl->d_tape = rebase(r_tape, base);
+  pl->n_tape = d->n_ops;
   if (pl->fold) pl->desc_copy = std::make_shared<DescCopy>(d);
   pl->d_wops = rebase(r_wops, base);
 

@@ -83,6 +83,11 @@ struct Prof {
 
 }  // namespace hq
 
+namespace hq {
+// sets hq_last_error() and returns s (for entry points outside hq_api.cpp)
+hq_status fail_status(hq_status s, const std::string& msg);
+}  // namespace hq
+
 struct hq_plan_s {
   int32_t n_qubits = 0;
   int32_t precision = HQ_C128;
@@ -109,6 +114,8 @@ struct hq_plan_s {
   const int32_t* d_pass_dlist = nullptr;
   const int32_t* d_pass_local = nullptr;  // [n_passes][n] (local then nonlocal)
   const int32_t* d_prep_off = nullptr;    // [n_preps]
+  const hq_op* d_tape = nullptr;          // the plan's tape as given (NOISY trajectories)
+  int32_t n_tape = 0;
   const hq::WinDev* d_wins = nullptr;
   const hq::WOp* d_wops = nullptr;
   mutable hq::Prof prof;                  // live per-launch timing (bench / profiling)

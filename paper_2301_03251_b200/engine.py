@@ -120,6 +120,7 @@ class Plan:
         self._h = h
         self._lib = L
         self.description = L.hq_plan_describe(h).decode()
+        self.measured = list(tape.measured) or list(range(tape.n_qubits))
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -188,6 +189,30 @@ class Plan:
                                      _ptr(theta), B, _ptr(init), rows, _ptr(st_out), _ptr(ws),
                                      ws.numel(), st), "state")
         return st_out
+
+
+    def noisy(self, x, theta, sites, shots: int, seed: int, want_jac: bool, want_counts: bool = False):
+        """NOISY trajectories (hq_noisy): -> (E [B], jac [B, nv] | None, counts [B, 2^m] | None)."""
+        torch = _torch()
+        B = int(x.shape[0])
+        dev = f"cuda:{self.device}"
+        flags = nat.HQ_WANT_JAC if want_jac else 0
+        n_sites = len(sites)
+        arr = (nat.HqNoiseSite * max(1, n_sites))()
+        for i, (op, q, code, prm) in enumerate(sites):
+            arr[i] = nat.HqNoiseSite(op, q, code, prm)
+        nb = int(self._lib.hq_noisy_workspace_bytes(self._h, B, flags, n_sites))
+        ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=dev)
+        out = torch.empty(B, dtype=torch.float64, device=dev)
+        jac = torch.empty((B, self.n_vars), dtype=torch.float64, device=dev) if want_jac else None
+        m = len(self.measured)
+        counts = torch.empty((B, 1 << m), dtype=torch.int64, device=dev) if want_counts else None
+        st = torch.cuda.current_stream().cuda_stream
+        nat.check(self._lib.hq_noisy(self._h, _ptr(x), int(x.stride(0)) if x.dim() == 2 else 0, _ptr(theta), B,
+                                     flags, ctypes.cast(arr, ctypes.c_void_p), n_sites, int(shots),
+                                     ctypes.c_uint64(int(seed) & ((1 << 64) - 1)), _ptr(out), _ptr(jac),
+                                     _ptr(counts), _ptr(ws), ws.numel(), st), "noisy")
+        return out, jac, counts
 
 
 # ------------------------------------------------------------------------------
@@ -475,3 +500,80 @@ def run_batch_shots(builder, xd, pd, want_x, want_p, shots, seed, precision="c12
             J[:, j] = (ep - em) * grad_scale
         jac = torch.from_numpy(J).to("cuda")
     return out, jac
+
+
+# ------------------------------------------------------------------------------
+# NOISY machine type (noise.py, qnn.py:109-111,157-166)
+def _twopoint_spec(nv: int, wanted):
+    return ([2 if w else 0 for w in wanted], [-1] * nv, [0.0] * nv)
+
+
+def run_batch_noisy(builder, xd, pd, want_x, want_p, noise, shots, seed, shift=math.pi / 2,
+                    grad_scale=0.5):
+    """Per-shot noise trajectories for every sample and every shifted
+    evaluation (same seed, same per-shot streams: qnn.py:35-52,109-111).
+    Returns (E [B] numpy, jac [B, d+P] cuda | None)."""
+    from .noise import noise_sites
+    torch = _torch()
+    B, d = xd.shape
+    P = pd.shape[0]
+    want = (want_x and d > 0) or (want_p and P > 0)
+    tape, ok = tr.trace(builder, xd, pd)
+    if ok and not tape.preps:
+        wanted = [want_x] * d + [want_p] * P
+        spec = _twopoint_spec(d + P, wanted) if want else None
+        plan = _global_cache.get(tape, d, P, "c128", spec, shift, grad_scale)
+        dev = f"cuda:{plan.device}"
+        xt = torch.from_numpy(xd).to(dev) if d else torch.zeros((B, 1), dtype=torch.float64, device=dev)
+        pt = torch.from_numpy(pd).to(dev) if P else torch.zeros(1, dtype=torch.float64, device=dev)
+        e, jac, _ = plan.noisy(xt, pt, noise_sites(tape.ops, noise), shots, seed, want)
+        return e.cpu().numpy(), jac
+    # per-circuit path (data-dependent builders / state loads): every base and
+    # shifted evaluation is a concrete circuit; circuits sharing a structure
+    # share one plan with their angles as per-row inputs
+    from .qnn import build_circuit
+    ext = np.hstack([xd, np.broadcast_to(pd, (B, P))])
+    rows, index = [ext], []
+    if want:
+        for j in range(d + P):
+            if (j < d and not want_x) or (j >= d and not want_p):
+                continue
+            for sgn in (1.0, -1.0):
+                r = ext.copy()
+                r[:, j] = ext[:, j] + sgn * shift
+                rows.append(r)
+                index.append(j)
+    allrows = np.concatenate(rows)
+    vals = noisy_circuit_values([build_circuit(builder, r[:d], r[d:]) for r in allrows], noise, shots, seed)
+    jac = None
+    if index:
+        J = np.zeros((B, d + P))
+        for k in range(0, len(index), 2):
+            ep = vals[B * (1 + k):B * (2 + k)]
+            em = vals[B * (2 + k):B * (3 + k)]
+            J[:, index[k]] = (ep - em) * grad_scale
+        jac = torch.from_numpy(J).to("cuda")
+    return vals[:B], jac
+
+
+def noisy_circuit_values(circuits, noise, shots, seed, want_counts=False):
+    """E (and optionally counts) of concrete circuits under ``noise``."""
+    from .noise import noise_sites
+    torch = _torch()
+    vals = np.empty(len(circuits))
+    counts = [None] * len(circuits)
+    for tape, rows in _circuit_rows(circuits).values():
+        A = len(tape.slot_const)
+        plan = _global_cache.get(tape, A, 0, "c128", None, math.pi / 2, 0.5)
+        dev = f"cuda:{plan.device}"
+        x = np.array([r[1] for r in rows], dtype=np.float64).reshape(len(rows), A)
+        xt = torch.from_numpy(x).to(dev) if A else torch.zeros((len(rows), 1), dtype=torch.float64, device=dev)
+        pt = torch.zeros(1, dtype=torch.float64, device=dev)
+        e, _, cnt = plan.noisy(xt, pt, noise_sites(tape.ops, noise), shots, seed, False, want_counts)
+        idx = [r[0] for r in rows]
+        vals[idx] = e.cpu().numpy()
+        if want_counts:
+            c = cnt.cpu().numpy()
+            for k, i in enumerate(idx):
+                counts[i] = c[k]
+    return (vals, counts) if want_counts else vals

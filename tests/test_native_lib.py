@@ -28,7 +28,7 @@ def test_library_exports_header_symbols():
     assert set(syms) == set(nat.EXPORTS)
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.hq_abi_version() == 1
+    assert lib.hq_abi_version() == 2
 
 
 def _desc(n=2, ops=((4, 0, -1, 0),), n_slots=1, measured=(), preps=None):
