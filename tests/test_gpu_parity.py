@@ -435,3 +435,44 @@ def test_folding_matches_unfolded(prec, monkeypatch):
     tol = 1e-10 if prec == "c128" else 2e-5
     np.testing.assert_allclose(r1, r0, atol=tol)
     np.testing.assert_allclose(j1.cpu().numpy(), j0.cpu().numpy(), atol=tol * 10)
+
+
+# ---------------------------------------------------------------------------
+# fallback kernels and workspace variants stay on the same numbers
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("force", [False, True])
+def test_generic_kernels_without_nvrtc_vs_oracle(prec, force, monkeypatch):
+    # HQ_JIT=0: interpreter (small circuits) or the generic window kernels (forced streaming)
+    monkeypatch.setenv("HQ_JIT", "0")
+    if force:
+        monkeypatch.setenv("HQ_FORCE_STREAM", "1")
+        monkeypatch.setenv("HQ_TILE_BITS", "9")
+    n = 11
+    b = _random_layer_builder(n, 60, seed=77)
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-3, 3, (3, 2))
+    th = rng.uniform(0, 6, 4)
+    res, jac, info = engine.run_batch(b, x, th, True, True, prec, cache=engine.PlanCache(2))
+    desc = info["plan"].description
+    assert ("kernels=generic" in desc) if force else ("path=onchip" in desc)
+    out, jx, jp, _, _ = O.layer(lambda i, p: b(i, p, Circ=O.Circuit), x, th)
+    check_vals(res, out, prec)
+    j = jac.cpu().numpy()
+    check_vals(j[:, :2], jx, prec, grad=True)
+    check_vals(j[:, 2:], jp, prec, grad=True)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_checkpoints_off_matches(prec, monkeypatch):
+    monkeypatch.setenv("HQ_FORCE_STREAM", "1")
+    monkeypatch.setenv("HQ_TILE_BITS", "9")
+    b, P = _prefix_builder(13, 21)
+    rng = np.random.default_rng(6)
+    x = rng.uniform(-3, 3, (4, 2))
+    th = rng.uniform(0, 6, P)
+    r1, j1, _ = engine.run_batch(b, x, th, True, True, prec, cache=engine.PlanCache(2))
+    monkeypatch.setenv("HQ_NO_CKPT", "1")
+    r0, j0, _ = engine.run_batch(b, x, th, True, True, prec, cache=engine.PlanCache(2))
+    tol = 1e-12 if prec == "c128" else 2e-5       # ψ re-derived from different checkpoints
+    np.testing.assert_allclose(r1, r0, atol=tol)
+    np.testing.assert_allclose(j1.cpu().numpy(), j0.cpu().numpy(), atol=tol * 10)
