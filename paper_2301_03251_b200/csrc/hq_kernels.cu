@@ -22,6 +22,11 @@
 namespace hq {
 
 // ---------------------------------------------------------------------------
+// the op list is staged in shared memory when it fits (one dependent global
+// load per gate step otherwise dominated small circuits: cfg1 48 us/step)
+constexpr size_t kOnchipOpsSmem = 32 * 1024;
+__host__ __device__ inline bool onchip_ops_in_smem(int n_ops) { return (size_t)n_ops * sizeof(DOp) <= kOnchipOpsSmem; }
+
 template <typename R>
 __global__ void __launch_bounds__(256) k_onchip(KArgs a, const DOp* __restrict__ ops, int n_ops) {
   using C = typename Cx<R>::T;
@@ -37,6 +42,12 @@ __global__ void __launch_bounds__(256) k_onchip(KArgs a, const DOp* __restrict__
   double* inv = red + 32;
   C* psi = reinterpret_cast<C*>(inv + 32);
   C* lam = psi + N;
+  if (onchip_ops_in_smem(n_ops)) {
+    DOp* sops = reinterpret_cast<DOp*>(lam + N);
+    for (int k = tid; k < n_ops; k += T) sops[k] = ops[k];
+    ops = sops;
+    __syncthreads();
+  }
 
   for (int64_t v = blockIdx.x; v < a.V; v += gridDim.x) {
     const VSample vs = decode_vsample(p, v, a.B);
@@ -162,7 +173,9 @@ namespace hq {
 static size_t onchip_smem(const hq_plan_s* pl, bool c64) {
   const size_t amp = c64 ? 8 : 16;
   const size_t prep = ((size_t)pl->dev.n_preps ? (size_t)pl->prep_total + 1 : 0) & ~(size_t)1;
-  return (size_t)pl->n_slots * 16 + prep * 8 + 64 * 8 + 2 * ((size_t)1 << pl->n_qubits) * amp;
+  const int n_ops = (int)pl->dops.size();
+  return (size_t)pl->n_slots * 16 + prep * 8 + 64 * 8 + 2 * ((size_t)1 << pl->n_qubits) * amp +
+         (onchip_ops_in_smem(n_ops) ? (size_t)n_ops * sizeof(DOp) : 0);
 }
 
 size_t onchip_smem_bytes(const hq_plan_s* pl) { return onchip_smem(pl, pl->precision == HQ_C64); }

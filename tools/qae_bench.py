@@ -1,0 +1,24 @@
+"""QAELayer (the reference's own autoencoder) forward +
+parameter gradient throughput on one GPU, EXACT_PROB, complex128."""
+import json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_2301_03251_b200 import QAELayer, Tensor, backward, tsum, workloads as wl
+
+for trash, total, B in ((2, 7, 256), (2, 12, 64)):
+    layer = QAELayer(trash, total, machine_type="exact_prob")
+    dim = 1 << (total - 1 - trash)
+    x = wl.qae_vectors(B, dim, min(dim, 128), seed=0)
+    def step():
+        out = layer(Tensor(x, dtype=np.float64))
+        backward(tsum(out))
+        layer.params.zero_grad()
+    step(); torch.cuda.synchronize()
+    t0 = time.perf_counter(); k = 3
+    for _ in range(k): step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / k
+    info = getattr(layer, "last_info", None)
+    print(json.dumps({"trash": trash, "total": total, "batch": B, "params": int(layer.params.data.size),
+                      "s_per_step": dt, "samples_per_s": B / dt,
+                      "plan": (info["plan"].description[:160] if info and "plan" in info else None)}), flush=True)
