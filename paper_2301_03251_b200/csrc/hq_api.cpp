@@ -108,7 +108,7 @@ int64_t ws_budget() {
 
 struct Layout {
   int64_t V = 0;
-  size_t tp = 0, dpart = 0, psi = 0, lam = 0, rpart = 0, lamN = 0, scratch = 0, total = 0;
+  size_t tp = 0, dpart = 0, psi = 0, lam = 0, rpart = 0, lamN = 0, locpart = 0, scratch = 0, total = 0;
   int32_t n_parts = 1;
   hq::StreamWs sws;
 };
@@ -147,6 +147,10 @@ Layout layout_for(const hq_plan_s* pl, int64_t B, int32_t flags, bool need_state
     if (adj) { L.lam = off; off = align_up(off + (size_t)cs * per); }
     L.rpart = off; off = align_up(off + (size_t)cs * nc * 8);
     if (adj && pl->fold_grad) { L.lamN = off; off = align_up(off + (size_t)cs * n_tiles * 16); }
+    if (adj && !pl->fold_local.empty()) {
+      L.locpart = off;
+      off = align_up(off + (size_t)cs * nc * pl->fold_local.size() * 32);
+    }
   }
   (void)need_state_only;
   L.scratch = off; off = align_up(off + (size_t)B * 8 + 8);   // readout sink for hq_state
@@ -637,6 +641,11 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
     // the tile: k_fold_grad).  Tile qubits: only the leading undifferentiated
     // gates (the first backward pass differentiates the rest as usual).
     const char* nofold = std::getenv("HQ_NO_FOLD");
+    // differentiated prefixes of tile qubits fold too with HQ_FOLD_LOCAL=1
+    const char* fl_env = std::getenv("HQ_FOLD_LOCAL");
+    // (opt-in: on cfg4 the first backward pass got 2 more register windows and
+    // ran slower, 3.31 -> 3.49 ms, than with those gates kept)
+    const bool fold_local_grad = fl_env && fl_env[0] == '1';
     if (allow_fold && !pl->has_preps && !(nofold && nofold[0] == '1')) {
       uint64_t L0 = 0;
       for (int b : pl->passes[0].local) L0 |= 1ull << b;
@@ -653,7 +662,10 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
         const int qb = g.q0;
         if (!open[qb]) continue;
         const bool local0 = L0 >> qb & 1ull;
-        if (cnt[qb] >= kMaxFoldPerQubit || (local0 && dslot_of(g) >= 0)) { open[qb] = 0; continue; }
+        if (cnt[qb] >= kMaxFoldPerQubit || (local0 && dslot_of(g) >= 0 && !fold_local_grad)) {
+          open[qb] = 0;
+          continue;
+        }
         fold_it[k] = 1;
         ++cnt[qb];
         if (dslot_of(g) >= 0) excl |= 1ull << qb;
@@ -678,11 +690,16 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
         pl->fold_grad = excl != 0;
         pl->fold_ops = pl->fold_ptr[n];
         gates.swap(kept);
-        pl->passes = schedule_passes(gates, n, pl->tile_bits, f, excl);
+        // folded qubits with gradients: outside the first tile through λ contracted
+        // over the tile (lamN), inside it through the tile-level contraction (locpart)
+        pl->passes = schedule_passes(gates, n, pl->tile_bits, f, fold_local_grad ? 0 : excl);
         for (int b : pl->passes[0].local)
           if (excl >> b & 1ull) {
-            delete pl;
-            return fail(HQ_E_CONFIG, "internal: folded qubit inside the first pass");
+            if (!fold_local_grad) {
+              delete pl;
+              return fail(HQ_E_CONFIG, "internal: folded qubit inside the first pass");
+            }
+            pl->fold_local.push_back(b);
           }
       } else {
         pl->fold_ptr.clear();
@@ -854,6 +871,8 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
   put(blob, off, pl->fold_slot.data(), pl->fold_slot.size(), r_fslot);
   put(blob, off, pl->fold_dslot.data(), pl->fold_dslot.size(), r_fdsl);
   put(blob, off, fold_nl.data(), fold_nl.size(), r_fnl);
+  const int32_t* r_floc;
+  put(blob, off, pl->fold_local.data(), pl->fold_local.size(), r_floc);
   blob.resize(align_up(std::max<size_t>(blob.size(), 16)));
   cudaError_t ce = cudaMalloc(&pl->dmem, blob.size());
   if (ce != cudaSuccess) {
@@ -910,6 +929,8 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
   dv.fold_dslot = rebase(r_fdsl, base);
   dv.fold_nonlocal = rebase(r_fnl, base);
   dv.n_fold_nonlocal = (int32_t)fold_nl.size();
+  dv.fold_local = rebase(r_floc, base);
+  dv.n_fold_local = (int32_t)pl->fold_local.size();
   pl->dev = dv;
   pl->d_tape = rebase(r_tape, base);
   pl->n_tape = d->n_ops;
@@ -981,6 +1002,7 @@ static hq_status run(hq_plan pl, const double* x, int64_t ldx, const double* the
     in.sws.lam = L.lam ? w + L.lam : nullptr;
     in.sws.rpart = reinterpret_cast<double*>(w + L.rpart);
     in.sws.lamN = L.lamN ? w + L.lamN : nullptr;
+    in.sws.locpart = L.locpart ? w + L.locpart : nullptr;
   }
   cudaError_t e = hq::launch_forward(pl, in, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(HQ_E_CUDA, std::string("forward launch: ") + cudaGetErrorString(e));

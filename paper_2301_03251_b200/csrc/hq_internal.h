@@ -124,6 +124,7 @@ struct hq_plan_s {
   // folded gate is differentiated (gradient from λ at the first pass's start)
   bool fold = false, fold_grad = false;
   std::vector<int32_t> fold_ptr, fold_kind, fold_slot, fold_dslot;
+  std::vector<int32_t> fold_local;        // first-tile qubits with differentiated folded gates
   int64_t fold_ops = 0;
   // hq_state with a caller-provided initial state runs on an unfolded twin
   std::shared_ptr<void> desc_copy;

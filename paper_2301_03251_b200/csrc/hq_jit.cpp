@@ -658,8 +658,10 @@ JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd, bool fused) {
     o = a16(o + (size_t)P.n_dslots_pass * L.slot_stride * rsz);
   }
   L.extra2 = o;
-  if (!bwd || fused || (i == 0 && pl->fold_grad))
+  if (!bwd || fused)
     o = a16(o + (96 + (size_t)(i == 0 ? ((pl->prep_total + 1) & ~1) : 0)) * 8);
+  L.fred = o;   // first backward pass of a plan with folded gradients: per-warp tile contractions
+  if (bwd && i == 0 && pl->fold_grad) o = a16(o + (size_t)(T / 32) * (2 + 4 * pl->fold_local.size()) * 8);
   L.fz = o;
   if (i == 0 && pl->fold) o = a16(o + ((size_t)pl->n_qubits * 2 + ((size_t)1 << RB)) * amp);
   L.total = o;
@@ -803,8 +805,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     o << "double* dx = reinterpret_cast<double*>(smem + " << L.extra2 << ");\n"
       << "double* red = dx; double* inv = dx + 32; double* wt = dx + 64; double* sval = dx + 96;\n"
       << "(void)red; (void)inv; (void)wt; (void)sval;\n";
-  if (bwd && !fwd && fold_end)
-    o << "double* red = reinterpret_cast<double*>(smem + " << L.extra2 << ");\n";
+  if (fold_end) o << "double* fred = reinterpret_cast<double*>(smem + " << L.fred << ");\n";
   if (first && pl->fold) {
     // initial product state: factor (a0, a1) of every qubit (its folded gates on |0>)
     o << "C* fz = reinterpret_cast<C*>(smem + " << L.fz << ");\n"
@@ -871,6 +872,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     if (P.n_dslots_pass <= cap && L.per_thread) reg_acc = P.n_dslots_pass;
     for (int k = 0; k < reg_acc; ++k) o << "R da" << k << " = (R)0;\n";
     if (!L.per_thread) o << "R dq0, dq1, dq2, dq3, dq4, dq5, dq6, dq7;\n";
+    if (fold_end && !pl->fold_local.empty()) o << "double lacc_x = 0.0, lacc_y = 0.0;\n";
   }
 
   // Window op emission.  A CNOT whose control is a CTA-uniform (tile bit
@@ -1145,27 +1147,84 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
           g.flush_batch();
           g.flush_pending(true);
           if (fold_end) {
-            // λ at the pass start contracted with the tile's initial factors:
-            // lamN[t] = Σ_i λ[t, i] conj(Π_b fz[LOCAL[b]][bit_b(i)])
+            // λ at the circuit start (all first-pass gates un-applied), contracted
+            // with the tile's initial factors z_q (fz):
+            //   lamN[t] = Σ_i λ[t, i] conj(Π_b z_{local[b]}[bit_b(i)])      (non-tile folded qubits)
+            //   A_q[c](t) = Σ_{i: bit_q(i)=c} λ[t, i] conj(Π_{b≠q} z[..])   (tile folded qubits q)
+            // per register window: i = (register index r, thread index) with
+            // W_R(r) = Π over register qubits, wt_ = Π over thread qubits
             const std::vector<int> S = Sbits(W), Rr = Rbits(W);
-            o << "{ C wt_; wt_.x = (R)1; wt_.y = (R)0;\n";
+            const int nlq = (int)pl->fold_local.size();
+            const int NV = 2 + 4 * nlq;   // doubles reduced per tile
+            auto fzr = [&](int tilebit, const std::string& bit) {
+              return "fz[" + std::to_string(2 * P.local[tilebit]) + " + (" + bit + ")]";
+            };
+            auto wreg = [&](int i, int skip) {   // product of register factors of index i, skipping register bit skip
+              std::string e = "one_";
+              for (int r = 0; r < g.RB; ++r)
+                if (r != skip) e = "cm_(" + e + ", " + fzr(Rr[r], std::to_string((i >> r) & 1)) + ")";
+              return e;
+            };
+            auto cjacc = [&](const std::string& acc, const std::string& w, const std::string& l) {
+              return acc + ".x += " + w + ".x * " + l + ".x + " + w + ".y * " + l + ".y; " + acc + ".y += " + w +
+                     ".x * " + l + ".y - " + w + ".y * " + l + ".x;";
+            };
+            o << "{ C one_; one_.x = (R)1; one_.y = (R)0;\nC wt_ = one_;\n";
             for (int s2 = 0; s2 < tbits; ++s2)
-              o << "wt_ = cm_(wt_, fz[" << 2 * P.local[S[s2]] << " + ((tid >> " << s2 << ") & 1)]);\n";
-            o << "double sx_ = 0.0, sy_ = 0.0;\n";
-            for (int i = 0; i < g.N; ++i) {
-              o << "{ C w_ = wt_;";
-              for (int r = 0; r < g.RB; ++r) o << " w_ = cm_(w_, fz[" << 2 * P.local[Rr[r]] + ((i >> r) & 1) << "]);";
-              const std::string L_ = g.L(i);
-              o << " sx_ += (double)(w_.x * " << L_ << ".x + w_.y * " << L_ << ".y); sy_ += (double)(w_.x * " << L_
-                << ".y - w_.y * " << L_ << ".x); }\n";
+              o << "wt_ = cm_(wt_, " << fzr(S[s2], "(tid >> " + std::to_string(s2) + ") & 1") << ");\n";
+            o << "C T_; T_.x = (R)0; T_.y = (R)0;\n";
+            for (int i = 0; i < g.N; ++i) o << "{ const C w_ = " << wreg(i, -1) << "; " << cjacc("T_", "w_", g.L(i)) << " }\n";
+            o << "double vv_[" << NV << "];\n"
+              << "vv_[0] = (double)(wt_.x * T_.x + wt_.y * T_.y); vv_[1] = (double)(wt_.x * T_.y - wt_.y * T_.x);\n";
+            for (int k2 = 0; k2 < nlq; ++k2) {
+              const int q = pl->fold_local[k2];
+              int tb = -1;
+              for (int b2 = 0; b2 < g.Q; ++b2)
+                if (P.local[b2] == q) tb = b2;
+              int rpos = -1, spos = -1;
+              for (int r = 0; r < g.RB; ++r)
+                if (Rr[r] == tb) rpos = r;
+              for (int s2 = 0; s2 < tbits; ++s2)
+                if (S[s2] == tb) spos = s2;
+              const int v0 = 2 + 4 * k2;
+              if (rpos >= 0) {
+                for (int c = 0; c < 2; ++c) {
+                  o << "{ C a_; a_.x = (R)0; a_.y = (R)0;\n";
+                  for (int i = 0; i < g.N; ++i)
+                    if (((i >> rpos) & 1) == c)
+                      o << "{ const C w_ = " << wreg(i, rpos) << "; " << cjacc("a_", "w_", g.L(i)) << " }\n";
+                  o << "vv_[" << v0 + 2 * c << "] = (double)(wt_.x * a_.x + wt_.y * a_.y); vv_[" << v0 + 2 * c + 1
+                    << "] = (double)(wt_.x * a_.y - wt_.y * a_.x); }\n";
+                }
+              } else {
+                o << "{ C e_ = one_;";
+                for (int s2 = 0; s2 < tbits; ++s2)
+                  if (s2 != spos) o << " e_ = cm_(e_, " << fzr(S[s2], "(tid >> " + std::to_string(s2) + ") & 1") << ");";
+                o << "\nconst double xr_ = (double)(e_.x * T_.x + e_.y * T_.y), xi_ = (double)(e_.x * T_.y - e_.y * T_.x);\n"
+                  << "const bool b_ = (tid >> " << spos << ") & 1;\n"
+                  << "vv_[" << v0 << "] = b_ ? 0.0 : xr_; vv_[" << v0 + 1 << "] = b_ ? 0.0 : xi_; vv_[" << v0 + 2
+                  << "] = b_ ? xr_ : 0.0; vv_[" << v0 + 3 << "] = b_ ? xi_ : 0.0; }\n";
+              }
             }
-            o << "sx_ = warp_sum<double>(sx_); sy_ = warp_sum<double>(sy_);\n";
+            o << "#pragma unroll\nfor (int k_ = 0; k_ < " << NV << "; ++k_) vv_[k_] = warp_sum<double>(vv_[k_]);\n";
             sync();
-            o << "if ((tid & 31) == 0) { red[2 * (tid >> 5)] = sx_; red[2 * (tid >> 5) + 1] = sy_; }\n";
+            o << "if ((tid & 31) == 0) { for (int k_ = 0; k_ < " << NV << "; ++k_) fred[(tid >> 5) * " << NV
+              << " + k_] = vv_[k_]; }\n";
             sync();
-            o << "if (tid == 0) { double ax = 0.0, ay = 0.0; for (int k = 0; k < " << nw
-              << "; ++k) { ax += red[2 * k]; ay += red[2 * k + 1]; } double* dst = a.lamN + 2 * (vl * ((int64_t)1 << "
-              << nonlocal.size() << ") + (int64_t)t); dst[0] = ax; dst[1] = ay; }\n";
+            o << "if (tid < " << NV / 2 << ") { double ax = 0.0, ay = 0.0; for (int k = 0; k < " << nw
+              << "; ++k) { ax += fred[k * " << NV << " + 2 * tid]; ay += fred[k * " << NV << " + 2 * tid + 1]; }\n"
+              << "if (tid == 0) { double* dst = a.lamN + 2 * (vl * ((int64_t)1 << " << nonlocal.size()
+              << ") + (int64_t)t); dst[0] = ax; dst[1] = ay; }\n";
+            if (nlq) {
+              // weight the tile by conj(Π over its tile-id qubits of z) and keep per CTA
+              o << "else { double fx = 1.0, fy = 0.0;";
+              for (size_t i2 = 0; i2 < nonlocal.size(); ++i2)
+                o << " { const C z_ = fz[" << 2 * nonlocal[i2] << " + ((t >> " << i2
+                  << ") & 1)]; const double nx = fx * (double)z_.x - fy * (double)z_.y; fy = fx * (double)z_.y + fy * (double)z_.x; fx = nx; }";
+              o << "\nlacc_x += fx * ax + fy * ay; lacc_y += fx * ay - fy * ax; } }\n";
+            } else {
+              o << "}\n";
+            }
             sync();
             o << "}\n";
           }
@@ -1202,6 +1261,9 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   o << "__syncthreads();\n}\n";  // tile loop
   if (fwd && last)
     o << "e = block_sum<R>(e, red, tid, T);\nif (tid == 0) ps.rpart[vl * ps.n_chunks + chunk] = e;\n";
+  if (fold_end && !pl->fold_local.empty())
+    o << "if (tid >= 1 && tid < " << 1 + 2 * pl->fold_local.size() << ") { double* dst = a.locpart + 2 * ((vl * ps.n_chunks + "
+         "chunk) * " << 2 * pl->fold_local.size() << " + (tid - 1)); dst[0] = lacc_x; dst[1] = lacc_y; }\n";
   if (bwd) {
     const int width = nw * L.group;
     for (int k = 0; k < reg_acc; ++k) o << "dacc[" << k << " * T + tid] = da" << k << ";\n";

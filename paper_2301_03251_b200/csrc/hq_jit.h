@@ -10,7 +10,7 @@
 namespace hq {
 
 struct JitLayout {
-  size_t lut, trig, extra, extra2, fz, total;   // fz: first pass of a folding plan, [n][2] initial factors
+  size_t lut, trig, extra, extra2, fz, fred, total;   // fz: first pass of a folding plan, [n][2] initial factors
   bool per_thread;  // bwd: per-thread derivative accumulators (group == 32)
   int group;        // bwd: derivative partials kept per group of 32/group lanes (1 = per warp)
   int slot_stride;  // bwd: floats between derivative slots' partials (padded in group mode: no bank conflicts)

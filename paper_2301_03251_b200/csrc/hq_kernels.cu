@@ -224,6 +224,7 @@ cudaError_t launch_forward(const hq_plan_s* pl, const LaunchIn& in, cudaStream_t
   a.prep_off = pl->d_prep_off;
   a.prep_total = pl->prep_total;
   a.lamN = static_cast<double*>(in.sws.lamN);
+  a.locpart = static_cast<double*>(in.sws.locpart);
   cudaError_t e;
   const bool c64 = pl->precision == HQ_C64;
   if (pl->onchip) e = c64 ? run_onchip<float>(pl, a, st) : run_onchip<double>(pl, a, st);

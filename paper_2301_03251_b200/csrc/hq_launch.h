@@ -16,6 +16,7 @@ struct StreamWs {
   int32_t n_chunks = 1;       // CTAs per sample per pass
   int32_t ckpt = 0;           // >0: forward passes write ψ checkpoints C_1..C_ckpt out of place
   void* lamN = nullptr;       // fold_grad: [chunk_samples, 2^(n-q)] complex128 (k_fold_grad input)
+  void* locpart = nullptr;    // [chunk_samples, n_chunks, n_fold_local, 2] complex128
 };
 
 struct LaunchIn {

@@ -42,6 +42,8 @@ struct DevPlan {
   const int32_t* fold_dslot;
   const int32_t* fold_nonlocal; // first pass's non-local qubits (tile-id bit i -> qubit)
   int32_t n_fold_nonlocal;
+  const int32_t* fold_local;    // first-tile qubits with differentiated folded gates
+  int32_t n_fold_local;
 };
 
 struct KArgs {
@@ -62,6 +64,7 @@ struct KArgs {
   const int32_t* prep_off;  // [n_preps] offsets of each prep's values in sval
   int32_t prep_total;
   double* lamN;             // fold_grad: λ at the first pass's start contracted over its tile, [V, 2^(n-q)] complex
+  double* locpart;          // [V, n_chunks, n_fold_local, 2] complex: tile-qubit reduced adjoints per CTA
 };
 
 

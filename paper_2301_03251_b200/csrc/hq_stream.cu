@@ -339,26 +339,41 @@ __global__ void __launch_bounds__(256, 2) k_wbwd(KArgs a, SArgs sa) {
 // on X (RY: Re X10 − Re X01; RX: Im X01 + Im X10; RZ: −2 Im X11).
 // One CTA per (sample, non-tile qubit); writes part 0 of each folded
 // derivative slot of that qubit.
-__global__ void __launch_bounds__(256) k_fold_grad(KArgs a, int64_t v0) {
+__global__ void __launch_bounds__(256) k_fold_grad(KArgs a, int64_t v0, int32_t n_chunks) {
   const DevPlan& p = a.p;
   const int tid = threadIdx.x, T = blockDim.x;
-  const int64_t vl = blockIdx.x / p.n_fold_nonlocal, v = v0 + vl;
-  const int kq = (int)(blockIdx.x - vl * p.n_fold_nonlocal);
+  const int nq = p.n_fold_nonlocal + p.n_fold_local;
+  const int64_t vl = blockIdx.x / nq, v = v0 + vl;
+  const int kq = (int)(blockIdx.x - vl * nq);
   const VSample vs = decode_vsample(p, v, a.B);
   const double* xr = a.x + vs.b * a.ldx;
+  const bool local = kq >= p.n_fold_nonlocal;
+  const int q = local ? p.fold_local[kq - p.n_fold_nonlocal] : p.fold_nonlocal[kq];
+  bool any = false;
+  for (int j = p.fold_ptr[q]; j < p.fold_ptr[q + 1]; ++j) any |= p.fold_dslot[j] >= 0;
+  if (!any) return;
   __shared__ double u[64][4];
   __shared__ double red[8][4];
-  for (int q = tid; q < p.n_qubits; q += T) fold_state(p, vs, xr, a.theta, q, u[q]);
+  __shared__ double r[4];
+  for (int qq = tid; qq < p.n_qubits; qq += T) fold_state(p, vs, xr, a.theta, qq, u[qq]);
   __syncthreads();
-  const int m = p.n_fold_nonlocal;
-  const int64_t NT = 1ll << m;
-  const double* lam = a.lamN + 2 * vl * NT;
-  {
-    const int k = kq;
-    const int q = p.fold_nonlocal[k];
-    bool any = false;
-    for (int j = p.fold_ptr[q]; j < p.fold_ptr[q + 1]; ++j) any |= p.fold_dslot[j] >= 0;
-    if (!any) return;
+  if (local) {
+    // tile qubit: Σ over this sample's CTAs of the per-CTA reduced adjoints
+    if (tid == 0) {
+      const int j = kq - p.n_fold_nonlocal, nlq = p.n_fold_local;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int ch = 0; ch < n_chunks; ++ch)
+        for (int c = 0; c < 2; ++c) {
+          const double* src = a.locpart + 2 * (((int64_t)vl * n_chunks + ch) * 2 * nlq + 2 * j + c);
+          acc[2 * c] += src[0];
+          acc[2 * c + 1] += src[1];
+        }
+      for (int c = 0; c < 4; ++c) r[c] = acc[c];
+    }
+  } else {
+    const int k = kq, m = p.n_fold_nonlocal;
+    const int64_t NT = 1ll << m;
+    const double* lam = a.lamN + 2 * vl * NT;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t t = tid; t < NT; t += T) {
       double wr = 1.0, wi = 0.0;
@@ -380,46 +395,49 @@ __global__ void __launch_bounds__(256) k_fold_grad(KArgs a, int64_t v0) {
       if ((tid & 31) == 0) red[tid >> 5][c] = x;
     }
     __syncthreads();
-    if (tid == 0) {
-      double r[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int w = 0; w < (T >> 5); ++w)
-        for (int c = 0; c < 4; ++c) r[c] += red[w][c];
-      // states after each folded gate, then the adjoint walk back
-      const int j0 = p.fold_ptr[q], K = p.fold_ptr[q + 1] - j0;
-      double st[33][4];
-      st[0][0] = 1.0; st[0][1] = 0.0; st[0][2] = 0.0; st[0][3] = 0.0;
-      double ang[32];
-      for (int j = 0; j < K; ++j) {
-        const int s = p.fold_slot[j0 + j];
-        ang[j] = s >= 0 ? eval_slot(p, s, xr, a.theta, vs.shvar, vs.shval) : 0.0;
-        for (int c = 0; c < 4; ++c) st[j + 1][c] = st[j][c];
-        apply_1q(p.fold_kind[j0 + j], ang[j], false, st[j + 1]);
+    if (tid == 0)
+      for (int c = 0; c < 4; ++c) {
+        double x = 0.0;
+        for (int w = 0; w < (T >> 5); ++w) x += red[w][c];
+        r[c] = x;
       }
-      double y[4] = {r[0], r[1], r[2], r[3]};
-      for (int j = K - 1; j >= 0; --j) {
-        const int ds = p.fold_dslot[j0 + j];
-        if (ds >= 0) {
-          // X[b'][b] = a_b conj(y_b'), a = st[j + 1]
-          auto X = [&](int bp, int b, double* re, double* im) {
-            const double ar = st[j + 1][2 * b], ai = st[j + 1][2 * b + 1];
-            const double yr = y[2 * bp], yi = -y[2 * bp + 1];
-            *re = ar * yr - ai * yi;
-            *im = ar * yi + ai * yr;
-          };
-          double r10, i10, r01, i01, r11, i11;
-          X(1, 0, &r10, &i10);
-          X(0, 1, &r01, &i01);
-          X(1, 1, &r11, &i11);
-          const int kind = p.fold_kind[j0 + j];
-          const double dot = kind == HQ_GATE_RY ? r10 - r01 : kind == HQ_GATE_RX ? i01 + i10 : -2.0 * i11;
-          double* dst = a.dpart + ((int64_t)v * p.n_adj + ds) * a.n_parts;
-          dst[0] = dot;
-          for (int pp = 1; pp < a.n_parts; ++pp) dst[pp] = 0.0;
-        }
-        apply_1q(p.fold_kind[j0 + j], ang[j], true, y);
-      }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // states after each folded gate, then the adjoint walk back
+    const int j0 = p.fold_ptr[q], K = p.fold_ptr[q + 1] - j0;
+    double st[33][4];
+    st[0][0] = 1.0; st[0][1] = 0.0; st[0][2] = 0.0; st[0][3] = 0.0;
+    double ang[32];
+    for (int j = 0; j < K; ++j) {
+      const int s = p.fold_slot[j0 + j];
+      ang[j] = s >= 0 ? eval_slot(p, s, xr, a.theta, vs.shvar, vs.shval) : 0.0;
+      for (int c = 0; c < 4; ++c) st[j + 1][c] = st[j][c];
+      apply_1q(p.fold_kind[j0 + j], ang[j], false, st[j + 1]);
     }
-    __syncthreads();
+    double y[4] = {r[0], r[1], r[2], r[3]};
+    for (int j = K - 1; j >= 0; --j) {
+      const int ds = p.fold_dslot[j0 + j];
+      if (ds >= 0) {
+        // X[b'][b] = a_b conj(y_b'), a = st[j + 1]
+        auto X = [&](int bp, int b, double* re, double* im) {
+          const double ar = st[j + 1][2 * b], ai = st[j + 1][2 * b + 1];
+          const double yr = y[2 * bp], yi = -y[2 * bp + 1];
+          *re = ar * yr - ai * yi;
+          *im = ar * yi + ai * yr;
+        };
+        double r10, i10, r01, i01, r11, i11;
+        X(1, 0, &r10, &i10);
+        X(0, 1, &r01, &i01);
+        X(1, 1, &r11, &i11);
+        const int kind = p.fold_kind[j0 + j];
+        const double dot = kind == HQ_GATE_RY ? r10 - r01 : kind == HQ_GATE_RX ? i01 + i10 : -2.0 * i11;
+        double* dst = a.dpart + ((int64_t)v * p.n_adj + ds) * a.n_parts;
+        dst[0] = dot;
+        for (int pp = 1; pp < a.n_parts; ++pp) dst[pp] = 0.0;
+      }
+      apply_1q(p.fold_kind[j0 + j], ang[j], true, y);
+    }
   }
 }
 
@@ -569,7 +587,8 @@ static cudaError_t run_stream_t(const hq_plan_s* pl, const KArgs& a, const Strea
         }
         if (pl->fold_grad) {
           ProfScope prof(pl, st, HQ_K_OTHER, (double)nv * 16.0 * (double)n_tiles);
-          k_fold_grad<<<(unsigned)(nv * pl->dev.n_fold_nonlocal), 256, 0, st>>>(a, v0);
+          const int nq = pl->dev.n_fold_nonlocal + pl->dev.n_fold_local;
+          k_fold_grad<<<(unsigned)(nv * nq), 256, 0, st>>>(a, v0, n_chunks);
         }
       }
       cudaError_t e = cudaGetLastError();

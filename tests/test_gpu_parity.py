@@ -377,9 +377,11 @@ def _prefix_builder(n, seed, Circ=None):
 
 
 @pytest.mark.parametrize("prec", PRECS)
-def test_folded_prefix_gradients_vs_oracle(prec, monkeypatch):
+@pytest.mark.parametrize("fold_local", ["0", "1"])
+def test_folded_prefix_gradients_vs_oracle(prec, fold_local, monkeypatch):
     monkeypatch.setenv("HQ_FORCE_STREAM", "1")
     monkeypatch.setenv("HQ_TILE_BITS", "9")
+    monkeypatch.setenv("HQ_FOLD_LOCAL", fold_local)   # tile qubits' differentiated prefixes too
     n = 14
     b, P = _prefix_builder(n, 5)
     rng = np.random.default_rng(2)
