@@ -338,8 +338,61 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
   std::vector<char> done(ops.size(), 0);
   size_t left = ops.size();
   const uint32_t all = (q >= 32) ? ~0u : ((1u << q) - 1);
+  // Register set of a window: every RB-subset of the exchange qubits the next
+  // ops need is tried and the one that admits the most ops wins (first-come
+  // greedy as the fallback: HQ_WIN_GREEDY=1).  Sets that would take every tile
+  // bit of a bank class out of the thread bits are skipped.
+  const char* wg = std::getenv("HQ_WIN_GREEDY");
+  const bool lookahead = !(wg && wg[0] == '1');
+  auto class_ok = [&](uint32_t m) {
+    for (int cls = 0; cls < 4; ++cls) {
+      int c = 0, tot = 0;
+      for (int b = 0; b < q; ++b)
+        if ((b & 3) == cls) { ++tot; if (!(m >> b & 1u)) ++c; }
+      if (tot > 0 && c == 0) return false;
+    }
+    return true;
+  };
+  auto admitted = [&](uint32_t R) {
+    int cnt = 0;
+    uint32_t blocked = 0;
+    for (size_t k = 0; k < ops.size(); ++k) {
+      if (done[k]) continue;
+      const uint32_t qs = qmask(ops[k]);
+      if (qs & blocked) { blocked |= qs; continue; }
+      if ((exch(ops[k]) & ~R) == 0) ++cnt;
+      else blocked |= qs;
+    }
+    return cnt;
+  };
   do {
     uint32_t Rm = 0;
+    if (lookahead) {
+      uint32_t cand = 0;
+      int seen = 0;
+      for (size_t k = 0; k < ops.size() && seen < 48; ++k)
+        if (!done[k]) { cand |= exch(ops[k]); ++seen; }
+      std::vector<int> cb;
+      for (int b = 0; b < q; ++b)
+        if (cand >> b & 1u) cb.push_back(b);
+      if ((int)cb.size() > RB && cb.size() <= 16) {
+        int best = -1;
+        uint32_t bestR = 0;
+        const int nc = (int)cb.size();
+        for (uint32_t sel = 0; sel < (1u << nc); ++sel) {
+          if (popc(sel) != RB) continue;
+          uint32_t R = 0;
+          for (int i = 0; i < nc; ++i)
+            if (sel >> i & 1u) R |= 1u << cb[i];
+          if (!class_ok(R)) continue;
+          // ties: keep the fixed low bits (HBM-contiguous lanes) out of the registers
+          const uint32_t fmask = fixed >= 32 ? ~0u : ((1u << fixed) - 1u);
+          const int sc = 2 * admitted(R) + ((R & fmask) ? 0 : 1);
+          if (sc > best) { best = sc; bestR = R; }
+        }
+        if (best > 1) Rm = bestR;
+      }
+    }
     std::vector<size_t> exec;
     bool progress = true, first_scan = true;
     while (progress) {
@@ -758,6 +811,11 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
     if (g.kind == HQ_GATE_RX || g.kind == HQ_GATE_RY) rot_slots.push_back(g.slot);
   }
 
+  if (!pl->onchip && std::getenv("HQ_PLAN_WINDOWS")) {
+    std::fprintf(stderr, "hq windows:");
+    for (const auto& ps : pl->passes) std::fprintf(stderr, " %d/%zu", ps.n_dops, ps.wins.size());
+    std::fprintf(stderr, "\n");
+  }
   if (!pl->onchip) {
     std::string why;
     const hq_status js = hq::jit_build(pl, why);
