@@ -273,53 +273,53 @@ def run_ours(a):
     S = int(st["n_passes"])
     fwd, bwd = prof["pass_fwd"], prof["pass_bwd"]
     if st["path"] == 1:
-        # dominant kernel class: the backward passes (hq_b*, incl. the fused
-        # last-forward+first-backward kernel).  SURVEY.md §8(d): a backward pass
-        # moves 4·2^n·b bytes per sample (ψ and λ, read + write).
+        # Dominant kernel class: the backward passes (hq_b*, incl. the fused
+        # last-forward+first-backward kernel).  Algorithmic bytes per unit
+        # (one sample's forward + full gradient) follow SURVEY.md §8(d), which
+        # defines roofline.achieved: 2·2^n·b·(S_f + 2·S_b) with the model's
+        # sweep count S = d·ceil(n/q_model) (q_model = 13 c64 / 12 c128); the
+        # backward class carries the 2·S_b part (ψ and λ, read + write).  This
+        # plan executes fewer sweeps (S below): "executed" reports the bytes of
+        # the sweeps actually run, "traffic" the ncu-measured DRAM bytes.
+        R, D, _ = wl.gate_counts(cfg)
+        depth = 10 if cfg == "cfg4" else 20
+        S_model = depth * -(-n // (13 if prec == "c64" else 12))
         name = "hq_b* (backward passes)" if bwd["ms"] >= fwd["ms"] else "hq_f* (forward passes)"
         dom = bwd if bwd["ms"] >= fwd["ms"] else fwd
-        per_pass = (4 if dom is bwd else 2) * (1 << n) * b
-        alg = per_pass * S * B * a.steps
+        units = B * a.steps
+        alg = (4 if dom is bwd else 2) * (1 << n) * b * S_model * units
         achieved = alg / (dom["ms"] / 1e3) / 1e9
-        # all amplitude-update kernels together: 2·2^n·b·(S_f + 2·S_b)
-        alg_all = 2 * (1 << n) * b * (S + 2 * S) * B * a.steps
+        alg_exec = (4 if dom is bwd else 2) * (1 << n) * b * S * units
         t_all = (fwd["ms"] + bwd["ms"]) / 1e3
         traffic = None
         try:
             with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
                 ref = json.load(f)["hq_b" if dom is bwd else "hq_f"]
-            traffic = ref["dram_bytes_per_launch"] / ref["algorithmic_bytes_per_launch"] * (alg / max(dom["launches"], 1))
+            traffic = ref["dram_bytes_per_launch"] / ref["algorithmic_bytes_per_launch"] * (alg_exec / max(dom["launches"], 1))
         except Exception:
             pass
+        bytes_unit = 2 * (1 << n) * b * (S_model + 2 * S_model)
+        flops_unit = (1 << n) * (18 * R + 8 * D + 6)
+        units_per_s = units / t_all
+        fpeak, fkind = fp_peak(prec)
         roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "traffic_note": "ncu dram__bytes_read+write per launch, ratio to algorithmic bytes from "
-                                "profiles/ncu_traffic.json scaled to this launch size",
+                "traffic_note": "ncu dram__bytes_read+write per launch (ratio to executed-sweep bytes from "
+                                "profiles/ncu_traffic.json, scaled to this launch size)",
                 "peak_source": peak_kind,
                 "launches": dom["launches"], "avg_launch_ms": dom["ms"] / max(dom["launches"], 1),
                 "algorithmic_bytes_per_launch": alg / max(dom["launches"], 1),
-                "passes_per_direction": S,
+                "sweeps_model": S_model, "sweeps_executed": S,
+                "executed": {"achieved": alg_exec / (dom["ms"] / 1e3) / 1e9,
+                             "frac": alg_exec / (dom["ms"] / 1e3) / 1e9 / peak,
+                             "bytes_per_launch": alg_exec / max(dom["launches"], 1)},
                 "share_of_step": dom["ms"] / (ms * a.steps),
-                "all_passes": {"achieved": alg_all / t_all / 1e9, "frac": alg_all / t_all / 1e9 / peak,
-                               "algorithmic_bytes_per_sample": alg_all / (B * a.steps)},
+                "all_passes": {"bytes_per_unit": bytes_unit, "achieved": bytes_unit * units_per_s / 1e9,
+                               "frac": bytes_unit * units_per_s / 1e9 / peak},
+                "fp32": {"flops_per_unit": flops_unit, "achieved_TFLOPs": flops_unit * units_per_s / 1e12,
+                         "peak_TFLOPs": fpeak, "peak_source": fkind,
+                         "frac": flops_unit * units_per_s / 1e12 / fpeak if fpeak else None},
                 "all_kernels_ms_per_step": {k: v["ms"] / a.steps for k, v in prof.items()}}
-        # SURVEY.md §8(d)'s per-unit model over all pass kernels: bytes assume
-        # S = d·ceil(n/13) sweeps (this plan executes S above, fewer bytes than
-        # the model), flops F = 2^n·(18R + 8D + 6) against the measured FFMA2 peak
-        R, D, _ = wl.gate_counts(cfg)
-        depth = 10 if cfg == "cfg4" else 20
-        S_model = depth * -(-n // (13 if prec == "c64" else 12))
-        bytes_unit = 2 * (1 << n) * b * (S_model + 2 * S_model)
-        flops_unit = (1 << n) * (18 * R + 8 * D + 6)
-        units_per_s = B * a.steps / t_all
-        fpeak, fkind = fp_peak(prec)
-        roof["survey_model"] = {
-            "sweeps_model": S_model, "sweeps_executed": S,
-            "bytes_per_unit": bytes_unit, "hbm_achieved_GBps": bytes_unit * units_per_s / 1e9,
-            "hbm_frac": bytes_unit * units_per_s / 1e9 / peak,
-            "flops_per_unit": flops_unit, "fp_achieved_TFLOPs": flops_unit * units_per_s / 1e12,
-            "fp_peak_TFLOPs": fpeak, "fp_peak_source": fkind,
-            "fp_frac": flops_unit * units_per_s / 1e12 / fpeak if fpeak else None}
     else:
         dom = prof["onchip"]
         R, D, G = wl.gate_counts(cfg)

@@ -260,11 +260,60 @@ std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int 
   std::vector<char> done(ops.size(), 0);
   size_t left = ops.size();
   const uint64_t fixed = (f >= 64) ? ~0ull : ((1ull << f) - 1);
+  // Tile choice by lookahead (HQ_PASS_LOOKAHEAD=0: first-come greedy + lowest-
+  // qubit top-up): cfg4 17 -> 8 passes, 4,676 -> 5,646 samples/s
+  const char* pla = std::getenv("HQ_PASS_LOOKAHEAD");
+  const bool lookahead = !(pla && pla[0] == '0');
   while (left > 0) {
     uint64_t L = fixed;
     hq::Pass ps;
     bool progress = true;
     bool first_scan = true;
+    if (lookahead) {
+      // tile = fixed bits + the (q - f)-subset of the next ops' exchange qubits
+      // admitting the most ops (single scan, first-come blocking)
+      const uint64_t excl = passes.empty() ? excl0 : 0;
+      // candidates: exchange qubits of the next ops, in order, up to 16
+      uint64_t cand = 0;
+      for (size_t k = 0; k < ops.size() && popc(cand) < 16; ++k) {
+        if (done[k]) continue;
+        const uint64_t ex = exch_mask(ops[k]) & ~fixed & ~excl;
+        if (popc(cand | ex) > 16) break;
+        cand |= ex;
+      }
+      std::vector<int> cb;
+      for (int b = 0; b < n; ++b)
+        if (cand >> b & 1ull) cb.push_back(b);
+      const int need = q - popc(fixed);
+      if ((int)cb.size() > need && cb.size() <= 18) {
+        long best = -1;
+        uint64_t bestL = 0;
+        const int nc = (int)cb.size();
+        std::vector<int> idx(need);
+        for (int i = 0; i < need; ++i) idx[i] = i;
+        while (true) {
+          uint64_t Lc = fixed;
+          for (int i : idx) Lc |= 1ull << cb[i];
+          long cnt = 0;
+          uint64_t blocked = 0;
+          const uint64_t allq = n >= 64 ? ~0ull : ((1ull << n) - 1);
+          for (size_t k = 0; k < ops.size() && blocked != allq; ++k) {
+            if (done[k]) continue;
+            const uint64_t qs = op_mask(ops[k]);
+            if (qs & blocked) { blocked |= qs; continue; }
+            if ((exch_mask(ops[k]) & ~Lc) == 0) ++cnt;
+            else blocked |= qs;
+          }
+          if (cnt > best) { best = cnt; bestL = Lc; }
+          int i = need - 1;
+          while (i >= 0 && idx[i] == nc - need + i) --i;
+          if (i < 0) break;
+          ++idx[i];
+          for (int j = i + 1; j < need; ++j) idx[j] = idx[j - 1] + 1;
+        }
+        if (best > 0) { L = bestL; first_scan = false; }
+      }
+    }
     while (progress) {
       progress = false;
       uint64_t blocked = 0;
