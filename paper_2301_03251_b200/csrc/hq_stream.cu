@@ -372,22 +372,42 @@ __global__ void __launch_bounds__(256) k_fold_grad(KArgs a, int64_t v0, int32_t 
     }
   } else {
     const int k = kq, m = p.n_fold_nonlocal;
-    const int64_t NT = 1ll << m;
-    const double* lam = a.lamN + 2 * vl * NT;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int64_t t = tid; t < NT; t += T) {
+    const double* lam = a.lamN + 2 * vl * (1ll << m);
+    // weight(t) = Π_{i≠k} u_i[bit_i(t)] = W_hi(t >> Lb) · W_lo(t mod 2^Lb)
+    const int Lb = m < 9 ? m : 9;
+    __shared__ double2 wlo[512];
+    for (int lo = tid; lo < (1 << Lb); lo += T) {
       double wr = 1.0, wi = 0.0;
-      for (int i = 0; i < m && (wr != 0.0 || wi != 0.0); ++i) {
+      for (int i = 0; i < Lb; ++i) {
         if (i == k) continue;
-        const double* f = u[p.fold_nonlocal[i]] + 2 * ((t >> i) & 1);
+        const double* f = u[p.fold_nonlocal[i]] + 2 * ((lo >> i) & 1);
         const double nr = wr * f[0] - wi * f[1];
         wi = wr * f[1] + wi * f[0];
         wr = nr;
       }
-      const double lr = lam[2 * t], li = lam[2 * t + 1];
-      const int c = (int)((t >> k) & 1);
-      acc[2 * c] += lr * wr + li * wi;
-      acc[2 * c + 1] += li * wr - lr * wi;
+      wlo[lo] = make_double2(wr, wi);
+    }
+    __syncthreads();
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t hi = 0; hi < (1ll << (m - Lb)); ++hi) {
+      double hr = 1.0, hm = 0.0;
+      for (int i = Lb; i < m; ++i) {
+        if (i == k) continue;
+        const double* f = u[p.fold_nonlocal[i]] + 2 * ((hi >> (i - Lb)) & 1);
+        const double nr = hr * f[0] - hm * f[1];
+        hm = hr * f[1] + hm * f[0];
+        hr = nr;
+      }
+      if (hr == 0.0 && hm == 0.0) continue;
+      for (int lo = tid; lo < (1 << Lb); lo += T) {
+        const int64_t t = (hi << Lb) | lo;
+        const double2 w = wlo[lo];
+        const double wr = hr * w.x - hm * w.y, wi = hr * w.y + hm * w.x;
+        const double lr = lam[2 * t], li = lam[2 * t + 1];
+        const int c = (int)((t >> k) & 1);
+        acc[2 * c] += lr * wr + li * wi;
+        acc[2 * c + 1] += li * wr - lr * wi;
+      }
     }
     for (int c = 0; c < 4; ++c) {
       double x = acc[c];
