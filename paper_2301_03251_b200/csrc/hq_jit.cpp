@@ -867,7 +867,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   // has few enough derivative slots (shared-memory partials otherwise)
   int reg_acc = 0;
   if (bwd) {
-    int cap = 24;
+    int cap = 56;
     if (const char* e = std::getenv("HQ_REG_ACC")) cap = std::atoi(e);
     if (P.n_dslots_pass <= cap && L.per_thread) reg_acc = P.n_dslots_pass;
     for (int k = 0; k < reg_acc; ++k) o << "R da" << k << " = (R)0;\n";
