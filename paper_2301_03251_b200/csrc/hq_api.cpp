@@ -1040,6 +1040,7 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
   dv.n_fold_local = (int32_t)pl->fold_local.size();
   pl->dev = dv;
   pl->d_tape = rebase(r_tape, base);
+  pl->host_measured = meas;
   pl->n_tape = d->n_ops;
   if (pl->fold) pl->desc_copy = std::make_shared<DescCopy>(d);
   pl->d_wops = rebase(r_wops, base);

@@ -115,6 +115,7 @@ struct hq_plan_s {
   const int32_t* d_pass_local = nullptr;  // [n_passes][n] (local then nonlocal)
   const int32_t* d_prep_off = nullptr;    // [n_preps]
   const hq_op* d_tape = nullptr;          // the plan's tape as given (NOISY trajectories)
+  std::vector<int32_t> host_measured;     // readout qubits (host copy)
   int32_t n_tape = 0;
   const hq::WinDev* d_wins = nullptr;
   const hq::WOp* d_wops = nullptr;

@@ -310,11 +310,9 @@ extern "C" hq_status hq_noisy(hq_plan pl, const double* x, int64_t ldx, const do
   na.seed = seed;
   na.n = n;
   na.m = pl->dev.n_measured;
-  std::vector<int32_t> meas(na.m);
   if (na.m > 16) return hq::fail_status(HQ_E_CONFIG, "too many measured qubits");
-  cudaError_t e = cudaMemcpy(meas.data(), pl->dev.measured, na.m * sizeof(int32_t), cudaMemcpyDeviceToHost);
-  if (e != cudaSuccess) return hq::fail_status(HQ_E_CUDA, cudaGetErrorString(e));
-  for (int t = 0; t < na.m; ++t) na.measured[t] = meas[t];
+  for (int t = 0; t < na.m; ++t) na.measured[t] = pl->host_measured[t];
+  cudaError_t e;
   na.warp_bytes = ((size_t)16 << n) + ((size_t)8 << na.m);
   na.warps = (int32_t)std::max<size_t>(1, std::min<size_t>(8, (size_t)(96 * 1024) / na.warp_bytes));
   const size_t smem = (size_t)na.warps * na.warp_bytes;
