@@ -134,3 +134,56 @@ def test_cfg5_shape_schedule_swap_count_bounded():
         c.add(O.Op(kind, t, a))
     c.measure(0)
     assert E == pytest.approx(O.expectation(c), abs=1e-12)
+
+
+def _shard_worker(rank, world, port, n, seed, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = world.bit_length() - 1
+        rng = np.random.default_rng(seed)
+        ops = _random_ops(n, 60, rng)
+        measured = [int(x) for x in rng.choice(n, 2, replace=False)]
+        sch = S.schedule(n, g, ops, measured)
+        L = n - g
+        oracle_apply = _oracle_apply(L)
+
+        def apply_local_dev(shard, lops):   # CPU executor standing in for the GPU plan
+            out = oracle_apply(shard.numpy(), lops)
+            return torch.from_numpy(np.ascontiguousarray(out))
+        shard, E = S.run_nccl(sch, apply_local_dev, rank, world, torch.device("cpu"))
+        q.put((rank, shard.numpy(), E, sch.final_layout))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_amplitude_sharding_real_processes_gloo(world):
+    # run_nccl's exchange path (pairwise isend/irecv of half shards, per-rank
+    # phases, all-reduced readout) with real processes over gloo
+    import torch.multiprocessing as mp
+    n, seed = 7, 11 + world
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + (os.getpid() % 500) + world
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, n, seed, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in procs], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+    rng = np.random.default_rng(seed)
+    ops = _random_ops(n, 60, rng)
+    measured = [int(x) for x in rng.choice(n, 2, replace=False)]
+    full = O.Circuit(n)
+    for kind, t, a in ops:
+        full.add(O.Op(kind, t, a))
+    full.measure(*measured)
+    want = O.simulate(full)
+    L = n - (world.bit_length() - 1)
+    got = S.gather_state([r[1] for r in res], L, res[0][3])
+    np.testing.assert_allclose(got, want, atol=1e-12)
+    for r in res:
+        assert r[2] == pytest.approx(O.expectation(full), abs=1e-12)
