@@ -478,3 +478,21 @@ def test_checkpoints_off_matches(prec, monkeypatch):
     tol = 1e-12 if prec == "c128" else 2e-5       # ψ re-derived from different checkpoints
     np.testing.assert_allclose(r1, r0, atol=tol)
     np.testing.assert_allclose(j1.cpu().numpy(), j0.cpu().numpy(), atol=tol * 10)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_natural_multi_pass_circuit_vs_oracle(prec):
+    # n = 21 at the production tile size: several passes, 9 (c64) / 10 (c128)
+    # tile-id qubits, folded prefixes, lookahead tiles and windows
+    n = 21
+    b = _random_layer_builder(n, 45, seed=2121)
+    rng = np.random.default_rng(21)
+    x = rng.uniform(-3, 3, (2, 2))
+    th = rng.uniform(0, 6, 4)
+    res, jac, info = engine.run_batch(b, x, th, True, True, prec, cache=engine.PlanCache(2))
+    assert "path=stream" in info["plan"].description
+    out, jx, jp, _, _ = O.layer(lambda i, p: b(i, p, Circ=O.Circuit), x, th)
+    check_vals(res, out, prec)
+    j = jac.cpu().numpy()
+    check_vals(j[:, :2], jx, prec, grad=True)
+    check_vals(j[:, 2:], jp, prec, grad=True)
