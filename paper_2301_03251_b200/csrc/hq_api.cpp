@@ -136,6 +136,11 @@ Layout layout_for(const hq_plan_s* pl, int64_t B, int32_t flags, bool need_state
     if (cs < 1) cs = 1;
     if (cs > L.V) cs = L.V;
     if (cs < 1) cs = 1;
+    // equal launches instead of a small tail chunk
+    if (L.V > cs) {
+      const int64_t nl = (L.V + cs - 1) / cs;
+      cs = (L.V + nl - 1) / nl;
+    }
     int64_t want = (1184 + cs - 1) / cs;  // >= ~8 CTAs per SM per launch
     int64_t nc = 16;
     while (nc < want) nc <<= 1;
