@@ -6,11 +6,15 @@
 // HBM path schedules gates into passes:
 //
 //   * a pass = one read + one write of the state, tile = 2^q amplitudes over q
-//     "local" qubits, the low f qubits always local (contiguous 64 B runs);
+//     "local" qubits, the low f qubits always local (contiguous 128 B runs);
 //   * a gate joins the current pass when no earlier unscheduled gate shares a
 //     qubit with it and its exchange qubits (targets of non-diagonal kinds) are
 //     local; diagonal kinds and controls may sit on non-local qubits because
-//     their bit is constant over a tile.
+//     their bit is constant over a tile;
+//   * each pass's tile and each register window's register set are chosen by
+//     lookahead (the subset admitting the most upcoming gates);
+//   * leading single-qubit gates fold into an analytic initial product state
+//     (their gradients come from λ at the circuit start, k_fold_grad).
 //
 // Everything device-side of a plan lives in one cudaMalloc.
 #include <cuda_runtime.h>

@@ -674,7 +674,7 @@ JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd, bool fused) {
 //
 // Everything about the pass is known here, so global offsets are literals:
 // tile bit b sits at global bit local[b].  When a window's first f lane bits
-// are tile bits {0..f-1} (one contiguous 64 B run per 2^f lanes), its
+// are tile bits {0..f-1} (one contiguous 128 B run per 2^f lanes), its
 // registers are loaded from / stored to HBM directly, skipping the
 // shared-memory staging round trip at that end of the tile.
 static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
