@@ -275,52 +275,124 @@ std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int 
   if (const char* e = std::getenv("HQ_MAX_PASS_OPS")) max_ops = std::max<size_t>(8, std::min<size_t>(kMaxPassOps, std::atoll(e)));
   const char* pla = std::getenv("HQ_PASS_LOOKAHEAD");
   const bool lookahead = !(pla && pla[0] == '0');
+  const bool depth2 = pla && pla[0] == '2';
+  const int need = q - popc(fixed);
+  const uint64_t allq = n >= 64 ? ~0ull : ((1ull << n) - 1);
+  // ops admitted by tile Lc given the finished set d (first-come blocking)
+  auto admit = [&](uint64_t Lc, std::vector<char>& d, bool mark) {
+    long cnt = 0;
+    uint64_t blocked = 0;
+    for (size_t k = 0; k < ops.size() && blocked != allq; ++k) {
+      if (d[k]) continue;
+      const uint64_t qs = op_mask(ops[k]);
+      if (qs & blocked) { blocked |= qs; continue; }
+      if ((exch_mask(ops[k]) & ~Lc) == 0) {
+        ++cnt;
+        if (mark) d[k] = 1;
+      } else {
+        blocked |= qs;
+      }
+    }
+    return cnt;
+  };
+  // every candidate tile (fixed + (q-f)-subset of the next ops' exchange qubits,
+  // up to 16 candidates) with its admitted count, best first
+  auto tiles = [&](std::vector<char>& d, uint64_t ex0) {
+    std::vector<std::pair<long, uint64_t>> out;
+    uint64_t cand = 0;
+    for (size_t k = 0; k < ops.size() && popc(cand) < 16; ++k) {
+      if (d[k]) continue;
+      const uint64_t ex = exch_mask(ops[k]) & ~fixed & ~ex0;
+      if (popc(cand | ex) > 16) break;
+      cand |= ex;
+    }
+    std::vector<int> cb;
+    for (int b = 0; b < n; ++b)
+      if (cand >> b & 1ull) cb.push_back(b);
+    const int nc = (int)cb.size();
+    if (nc <= need || nc > 18) return out;
+    std::vector<int> idx(need);
+    for (int i = 0; i < need; ++i) idx[i] = i;
+    while (true) {
+      uint64_t Lc = fixed;
+      for (int i : idx) Lc |= 1ull << cb[i];
+      out.push_back({admit(Lc, d, false), Lc});
+      int i = need - 1;
+      while (i >= 0 && idx[i] == nc - need + i) --i;
+      if (i < 0) break;
+      ++idx[i];
+      for (int j = i + 1; j < need; ++j) idx[j] = idx[j - 1] + 1;
+    }
+    std::stable_sort(out.begin(), out.end(), [](const std::pair<long, uint64_t>& x,
+                                                 const std::pair<long, uint64_t>& y) { return x.first > y.first; });
+    return out;
+  };
+  // Beam search over whole tile sequences (width 4, 6 expansions per state):
+  // the schedule with the fewest passes wins (the tail of a staircase otherwise
+  // ends in nearly empty passes that still stream the whole state).
+  std::vector<uint64_t> beam_tiles;
+  const char* pb = std::getenv("HQ_PASS_BEAM");
+  if (lookahead && !(pb && pb[0] == '0') && max_ops >= ops.size()) {
+    struct St { std::vector<char> d; size_t left; std::vector<uint64_t> t; };
+    std::vector<St> beam{St{done, left, {}}};
+    bool ok = true;
+    for (int level = 0; ok && level < 64; ++level) {
+      bool all_done = true;
+      std::vector<St> nxt;
+      for (auto& st : beam) {
+        if (st.left == 0) { nxt.push_back(st); continue; }
+        all_done = false;
+        auto cands = tiles(st.d, level == 0 ? excl0 : 0);
+        if (cands.empty()) { ok = false; break; }
+        for (size_t c = 0; c < cands.size() && c < 6; ++c) {
+          St ns{st.d, st.left, st.t};
+          ns.left -= (size_t)admit(cands[c].second, ns.d, true);
+          ns.t.push_back(cands[c].second);
+          nxt.push_back(std::move(ns));
+        }
+      }
+      if (!ok || all_done) break;
+      std::stable_sort(nxt.begin(), nxt.end(), [](const St& a, const St& b) { return a.left < b.left; });
+      beam.clear();
+      for (auto& st : nxt) {
+        bool dup = false;
+        for (auto& b2 : beam) dup |= b2.d == st.d;
+        if (!dup) beam.push_back(std::move(st));
+        if (beam.size() == 4) break;
+      }
+    }
+    if (ok) {
+      size_t bi = 0;
+      for (size_t i = 0; i < beam.size(); ++i)
+        if (beam[i].left == 0 && (beam[bi].left != 0 || beam[i].t.size() < beam[bi].t.size())) bi = i;
+      if (beam[bi].left == 0) beam_tiles = beam[bi].t;
+    }
+  }
   while (left > 0) {
     uint64_t L = fixed;
     hq::Pass ps;
     bool progress = true;
     bool first_scan = true;
-    if (lookahead) {
-      // tile = fixed bits + the (q - f)-subset of the next ops' exchange qubits
-      // admitting the most ops (single scan, first-come blocking)
+    if (passes.size() < beam_tiles.size()) {
+      L = beam_tiles[passes.size()];
+      first_scan = false;
+    } else if (lookahead) {
+      // tile = fixed bits + the candidate subset admitting the most ops; depth 2
+      // (HQ_PASS_LOOKAHEAD=2) adds the best follow-up pass's count for the top 6
       const uint64_t excl = passes.empty() ? excl0 : 0;
-      // candidates: exchange qubits of the next ops, in order, up to 16
-      uint64_t cand = 0;
-      for (size_t k = 0; k < ops.size() && popc(cand) < 16; ++k) {
-        if (done[k]) continue;
-        const uint64_t ex = exch_mask(ops[k]) & ~fixed & ~excl;
-        if (popc(cand | ex) > 16) break;
-        cand |= ex;
-      }
-      std::vector<int> cb;
-      for (int b = 0; b < n; ++b)
-        if (cand >> b & 1ull) cb.push_back(b);
-      const int need = q - popc(fixed);
-      if ((int)cb.size() > need && cb.size() <= 18) {
-        long best = -1;
-        uint64_t bestL = 0;
-        const int nc = (int)cb.size();
-        std::vector<int> idx(need);
-        for (int i = 0; i < need; ++i) idx[i] = i;
-        while (true) {
-          uint64_t Lc = fixed;
-          for (int i : idx) Lc |= 1ull << cb[i];
-          long cnt = 0;
-          uint64_t blocked = 0;
-          const uint64_t allq = n >= 64 ? ~0ull : ((1ull << n) - 1);
-          for (size_t k = 0; k < ops.size() && blocked != allq; ++k) {
-            if (done[k]) continue;
-            const uint64_t qs = op_mask(ops[k]);
-            if (qs & blocked) { blocked |= qs; continue; }
-            if ((exch_mask(ops[k]) & ~Lc) == 0) ++cnt;
-            else blocked |= qs;
+      auto lv1 = tiles(done, excl);
+      if (!lv1.empty()) {
+        long best = lv1[0].first;
+        uint64_t bestL = lv1[0].second;
+        if (depth2) {
+          long best_tot = -1;
+          for (size_t c = 0; c < lv1.size() && c < 6; ++c) {
+            std::vector<char> d2 = done;
+            const long s1 = admit(lv1[c].second, d2, true);
+            long s2 = 0;
+            for (const auto& t : tiles(d2, 0)) s2 = std::max(s2, t.first);
+            if (s1 + s2 > best_tot) { best_tot = s1 + s2; best = s1; bestL = lv1[c].second; }
           }
-          if (cnt > best) { best = cnt; bestL = Lc; }
-          int i = need - 1;
-          while (i >= 0 && idx[i] == nc - need + i) --i;
-          if (i < 0) break;
-          ++idx[i];
-          for (int j = i + 1; j < need; ++j) idx[j] = idx[j - 1] + 1;
         }
         if (best > 0) { L = bestL; first_scan = false; }
       }
@@ -875,6 +947,17 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
     std::fprintf(stderr, "hq windows:");
     for (const auto& ps : pl->passes) std::fprintf(stderr, " %d/%zu", ps.n_dops, ps.wins.size());
     std::fprintf(stderr, "\n");
+    if (std::getenv("HQ_PLAN_WINDOWS")[0] == '2')
+      for (const auto& ps : pl->passes) {
+        std::fprintf(stderr, "  local:");
+        for (int b : ps.local) std::fprintf(stderr, " %d", b);
+        std::fprintf(stderr, "  ops:");
+        for (int k : ps.op_ids) {
+          const hq_op& g = gates[k];
+          std::fprintf(stderr, " %d(%d%s%d)", k, g.kind, two_qubit(g.kind) ? "," : "", two_qubit(g.kind) ? g.q1 : g.q0);
+        }
+        std::fprintf(stderr, "\n");
+      }
   }
   if (!pl->onchip) {
     std::string why;

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from collections import OrderedDict
 
 import numpy as np
@@ -278,6 +279,9 @@ def run_batch(builder, xd: np.ndarray, pd: np.ndarray, want_x: bool, want_p: boo
         return run_per_sample(builder, xd, pd, want_x, want_p, precision, shift, grad_scale)
     if tape.preps:
         _check_preps(tape, xd, pd)
+    if os.environ.get("HQ_LIGHTCONE") == "1":
+        # opt-in: drop gates outside the readout's backward light cone (identical E and gradients)
+        tape = tr.light_cone(tape) or tape
     wanted = [want_x] * d + [want_p] * P
     grad = tr.classify(tape, d + P, wanted, shift, grad_scale) if (want_x or want_p) else None
     cache = cache or _global_cache

@@ -313,3 +313,48 @@ def classify(tape: Tape, n_vars: int, wanted, shift: float, grad_scale: float):
         else:
             mode[v] = MODE_TWOPOINT
     return mode, vslot, factor
+
+
+_DIAGONAL = ("Z", "RZ", "CZ", "CR")
+
+
+def light_cone(tape: Tape):
+    """Backward light cone of the EXACT_PROB readout (opt-in, ``HQ_LIGHTCONE=1``).
+
+    E = Σ_i w(i)|ψ_i|² with w depending only on the measured qubits M.  Walking
+    the tape backwards with K = qubits of the gates kept so far, a gate is
+    dropped when it cannot change E:
+      * it touches none of M ∪ K (a unitary on qubits the readout never sees);
+      * it is diagonal (Z/RZ/CZ/CR) on qubits outside K (commutes with the
+        diagonal readout and nothing later acts on them);
+      * CNOT(c, t) with t outside M ∪ K and c outside K (it only permutes a
+        traced-out bit, conditioned on a bit the readout reads diagonally).
+    The kept gates act on M ∪ K only; the other qubits stay in |0> and are
+    removed (qubits renumbered, measured order kept).  Variables left only in
+    dropped gates get a zero derivative, which is also what the reference's
+    two-point rule returns for them (E does not depend on them).
+    Returns the reduced tape, or None when nothing can be removed or the tape
+    has state loads."""
+    if tape.preps or not tape.affine:
+        return None
+    M = set(tape.measured) if tape.measured else set(range(tape.n_qubits))
+    K = set()
+    kept = []
+    for kind, tg, slot in reversed(tape.ops):
+        qs = set(tg)
+        if not (qs & (M | K)):
+            continue
+        if kind in _DIAGONAL and not (qs & K):
+            continue
+        if kind == "CNOT" and tg[1] not in (M | K) and tg[0] not in K:
+            continue
+        kept.append((kind, tg, slot))
+        K |= qs
+    kept.reverse()
+    active = sorted(M | K)
+    if len(kept) == len(tape.ops) and len(active) == tape.n_qubits:
+        return None
+    new = {q: i for i, q in enumerate(active)}
+    out = Tape(len(active), [new[q] for q in tape.measured], [(k, tuple(new[q] for q in tg), s) for k, tg, s in kept],
+               [], list(tape.slot_const), list(tape.slot_terms), True)
+    return out

@@ -496,3 +496,18 @@ def test_natural_multi_pass_circuit_vs_oracle(prec):
     j = jac.cpu().numpy()
     check_vals(j[:, :2], jx, prec, grad=True)
     check_vals(j[:, 2:], jp, prec, grad=True)
+
+
+def test_light_cone_cfg4_matches_full(monkeypatch):
+    # opt-in light-cone pruning (HQ_LIGHTCONE=1): the 10-qubit reduced circuit
+    # gives the full 20-qubit circuit's outputs and gradients
+    from paper_2301_03251_b200 import workloads as wl
+    b = wl.make_builder("cfg4", qsim, T)
+    x = wl.inputs_for("cfg4", 6)
+    th = wl.params_for("cfg4")
+    r0, j0, i0 = engine.run_batch(b, x, th, True, True, "c128", cache=engine.PlanCache(2))
+    monkeypatch.setenv("HQ_LIGHTCONE", "1")
+    r1, j1, i1 = engine.run_batch(b, x, th, True, True, "c128", cache=engine.PlanCache(2))
+    assert i1["plan"].description.startswith("n=10 ")
+    np.testing.assert_allclose(r1, r0, atol=1e-12)
+    np.testing.assert_allclose(j1.cpu().numpy(), j0.cpu().numpy(), atol=1e-11)

@@ -190,3 +190,59 @@ class TestAutogradBoundary:
         y = tsum(x * 3.0 - 1.0)
         backward(y)
         np.testing.assert_array_equal(x.grad, [[3.0, 3.0]])
+
+
+# ---------------------------------------------------------------------------
+def _tape_expectation(tape, x_row, theta):
+    """Oracle EXACT_PROB of a traced tape at concrete values."""
+    from oracle import hq_oracle as Ora
+    vals = list(x_row) + list(theta)
+    c = Ora.Circuit(tape.n_qubits)
+    for kind, tg, slot in tape.ops:
+        ang = None
+        if slot >= 0:
+            ang = tape.slot_const[slot] + sum(coef * vals[v] for v, coef in tape.slot_terms[slot].items())
+        c.add(Ora.Op(kind, tg, ang))
+    if tape.measured:
+        c.measure(*tape.measured)
+    return Ora.expectation(c)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_light_cone_keeps_expectation(seed):
+    from paper_2301_03251_b200 import tracer as tr
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(3, 9))
+    kinds = ["H", "X", "Y", "Z", "RX", "RY", "RZ", "CNOT", "CZ", "CR", "SWAP"]
+    plan = []
+    for _ in range(40):
+        k = kinds[rng.integers(len(kinds))]
+        two = k in ("CNOT", "CZ", "CR", "SWAP")
+        tg = tuple(int(q) for q in rng.choice(n, 2 if two else 1, replace=False))
+        plan.append((k, tg, int(rng.integers(0, 5))))
+    meas = [int(q) for q in rng.choice(n, int(rng.integers(1, 3)), replace=False)]
+
+    def builder(inputs, params):
+        c = Circuit(n)
+        for k, tg, v in plan:
+            ang = (inputs[v] if v < 2 else params[v - 2]) if k in ("RX", "RY", "RZ", "CR") else None
+            getattr(c, k.lower())(*tg) if ang is None else getattr(c, k.lower())(*tg, ang)
+        c.measure(*meas)
+        return c
+    x = rng.uniform(-3, 3, (2, 2))
+    th = rng.uniform(0, 6, 3)
+    tape, ok = tr.trace(builder, x, th)
+    assert ok
+    lc = tr.light_cone(tape) or tape
+    for trial in range(3):
+        xr = rng.uniform(-3, 3, 2)
+        tr_ = rng.uniform(0, 6, 3)
+        assert _tape_expectation(lc, xr, tr_) == pytest.approx(_tape_expectation(tape, xr, tr_), abs=1e-12)
+
+
+def test_light_cone_cfg4_shrinks():
+    from paper_2301_03251_b200 import tracer as tr, workloads as wl, qsim, templates as T
+    b = wl.make_builder("cfg4", qsim, T)
+    tape, ok = tr.trace(b, wl.inputs_for("cfg4", 2), wl.params_for("cfg4"))
+    lc = tr.light_cone(tape)
+    assert lc.n_qubits == 10 and len(lc.ops) == 164 and lc.measured == [0]
