@@ -328,11 +328,12 @@ std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int 
     return out;
   };
   // Beam search over whole tile sequences (width 4, 6 expansions per state):
-  // the schedule with the fewest passes wins (the tail of a staircase otherwise
-  // ends in nearly empty passes that still stream the whole state).
+  // the schedule with the fewest passes wins.
   std::vector<uint64_t> beam_tiles;
+  // opt-in (HQ_PASS_BEAM=1): on cfg4 / cfg5 it finds the greedy lookahead's
+  // schedule again at 1.5-2.5x the planning time
   const char* pb = std::getenv("HQ_PASS_BEAM");
-  if (lookahead && !(pb && pb[0] == '0') && max_ops >= ops.size()) {
+  if (lookahead && pb && pb[0] == '1' && max_ops >= ops.size()) {
     struct St { std::vector<char> d; size_t left; std::vector<uint64_t> t; };
     std::vector<St> beam{St{done, left, {}}};
     bool ok = true;
