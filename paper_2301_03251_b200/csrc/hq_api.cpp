@@ -703,6 +703,9 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
   pl->n_inputs = d->n_inputs;
   pl->n_params = d->n_params;
   pl->n_slots = d->n_slots;
+  for (int i = 0; i < d->n_measured; ++i) pl->host_measured.push_back(d->measured[i]);
+  if (pl->host_measured.empty())
+    for (int qb = 0; qb < n; ++qb) pl->host_measured.push_back(qb);
 
   // ---- state loads must precede every gate on their qubits ----------------
   std::vector<hq_op> gates;
@@ -818,6 +821,30 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
     if (pl->tile_bits - RB < 5 || pl->tile_bits - RB > 10) {
       delete pl;
       return fail(HQ_E_CONFIG, "tile must hold 2^9..2^14 amplitudes");
+    }
+    // ---- trailing X / CNOT gates: a basis permutation P applied to the
+    // readout instead of the state (E = Σ_j w(P j)|ψ_j|², λ = w(P·) ψ) ----
+    const char* noperm = std::getenv("HQ_NO_PERM");
+    if (allow_fold && !(noperm && noperm[0] == '1')) {
+      size_t cut = gates.size();
+      while (cut > 1 && (gates[cut - 1].kind == HQ_GATE_X || gates[cut - 1].kind == HQ_GATE_CNOT)) --cut;
+      if (cut < gates.size()) {
+        pl->perm_mask.assign(n, 0);
+        pl->perm_const.assign(n, 0);
+        for (int qb = 0; qb < n; ++qb) pl->perm_mask[qb] = 1ull << qb;
+        for (size_t k = cut; k < gates.size(); ++k) {
+          const hq_op& g = gates[k];
+          if (g.kind == HQ_GATE_X) {
+            pl->perm_const[g.q0] ^= 1;
+          } else {
+            pl->perm_mask[g.q1] ^= pl->perm_mask[g.q0];
+            pl->perm_const[g.q1] ^= pl->perm_const[g.q0];
+          }
+        }
+        pl->perm = true;
+        pl->perm_ops = (int32_t)(gates.size() - cut);
+        gates.resize(cut);
+      }
     }
     pl->passes = schedule_passes(gates, n, pl->tile_bits, f);
 
@@ -967,7 +994,7 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
       delete pl;
       return fail(HQ_E_CONFIG, "HQ_REG_BITS needs the specialised kernels: " + why);
     }
-    if (js != HQ_OK && !(opts & kPreferOnchip) && (pl->fold || n <= onchip_max_qubits(d->precision))) {
+    if (js != HQ_OK && !(opts & kPreferOnchip) && (pl->fold || pl->perm || n <= onchip_max_qubits(d->precision))) {
       // folding needs the specialised kernels; small circuits fall back to the interpreter
       delete pl;
       if (std::getenv("HQ_JIT_COMPILE_ONLY")) return fail(HQ_E_CONFIG, why);
@@ -991,6 +1018,7 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
   } else {
     os << " path=stream kernels=" << (pl->jit.ok ? "jit" : "generic") << " tile_bits=" << pl->tile_bits
        << " reg_bits=" << pl->reg_bits << " folded=" << pl->fold_ops << (pl->fold_grad ? "(grad)" : "")
+       << " readout_perm=" << pl->perm_ops
        << " passes=" << pl->passes.size() << " [";
     for (size_t i = 0; i < pl->passes.size(); ++i)
       os << (i ? "," : "") << pl->passes[i].n_dops << "/" << pl->passes[i].wins.size() << "w";
@@ -1075,6 +1103,10 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
   put(blob, off, fold_nl.data(), fold_nl.size(), r_fnl);
   const int32_t* r_floc;
   put(blob, off, pl->fold_local.data(), pl->fold_local.size(), r_floc);
+  const uint64_t* r_pmask;
+  const int32_t* r_pconst;
+  put(blob, off, pl->perm_mask.data(), pl->perm_mask.size(), r_pmask);
+  put(blob, off, pl->perm_const.data(), pl->perm_const.size(), r_pconst);
   blob.resize(align_up(std::max<size_t>(blob.size(), 16)));
   cudaError_t ce = cudaMalloc(&pl->dmem, blob.size());
   if (ce != cudaSuccess) {
@@ -1133,9 +1165,11 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
   dv.n_fold_nonlocal = (int32_t)fold_nl.size();
   dv.fold_local = rebase(r_floc, base);
   dv.n_fold_local = (int32_t)pl->fold_local.size();
+  dv.perm = pl->perm ? 1 : 0;
+  dv.perm_mask = rebase(r_pmask, base);
+  dv.perm_const = rebase(r_pconst, base);
   pl->dev = dv;
   pl->d_tape = rebase(r_tape, base);
-  pl->host_measured = meas;
   pl->n_tape = d->n_ops;
   if (pl->fold) pl->desc_copy = std::make_shared<DescCopy>(d);
   pl->d_wops = rebase(r_wops, base);

@@ -126,6 +126,12 @@ struct hq_plan_s {
   bool fold = false, fold_grad = false;
   std::vector<int32_t> fold_ptr, fold_kind, fold_slot, fold_dslot;
   std::vector<int32_t> fold_local;        // first-tile qubits with differentiated folded gates
+  // trailing X/CNOT gates folded into the readout: output bit q of the final
+  // basis permutation = parity(index & perm_mask[q]) ^ perm_const[q]
+  bool perm = false;
+  std::vector<uint64_t> perm_mask;
+  std::vector<int32_t> perm_const;
+  int32_t perm_ops = 0;
   int64_t fold_ops = 0;
   // hq_state with a caller-provided initial state runs on an unfolded twin
   std::shared_ptr<void> desc_copy;

@@ -1059,7 +1059,25 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     }
     // fused: the last window's block is still open here
     const WinDev& WL = P.wins[nwin - 1];
-    if (fused) {
+    if (fused && pl->perm) {
+      // readout through the folded trailing permutation: w(P g), P's output bit
+      // for measured qubit m = parity(g & mask_m) ^ c_m, g = global index
+      o << "{\n";
+      emit_tw(WL);
+      for (int i = 0; i < g.N; ++i) {
+        o << "{ const uint64_t gi = base | tw | " << hex64(reg_goff(WL, i)) << "; const double w = 0.0";
+        for (size_t m = 0; m < pl->host_measured.size(); ++m) {
+          const int q = pl->host_measured[m];
+          o << " + (double)((__popcll(gi & " << hex64(pl->perm_mask[q]) << ") + " << pl->perm_const[q] << ") & 1) * "
+            << (double)(1ull << m);
+        }
+        const std::string P_ = g.P(i), L_ = g.L(i);
+        o << "; e += w * (double)(" << P_ << ".x * " << P_ << ".x + " << P_ << ".y * " << P_ << ".y); " << L_
+          << ".x = (R)w * " << P_ << ".x; " << L_ << ".y = (R)w * " << P_ << ".y; }\n";
+      }
+      o << "}\n";
+      regs_live = true;
+    } else if (fused) {
       // readout + λ = wψ on the registers (tile index of logical register i =
       // deposit(i, R) | deposit(tid, S))
       const std::vector<int> S = Sbits(WL), R = Rbits(WL);
@@ -1085,11 +1103,25 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         for (int b2 = 0; b2 < g.RB; ++b2)
           if (i >> b2 & 1) o << " + wt[" << (g.Q - g.RB + b2) << "]";
         o << "; const C z = tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u]; const uint64_t g2 = base | ot | "
-          << hex64(hi_off(i)) << "; e += w * (double)(z.x * z.x + z.y * z.y); gout[g2] = z;"
+          << hex64(hi_off(i)) << ";";
+        if (pl->perm) {
+          // folded trailing permutation: weight of P(g2), amplitude lands at P(g2)
+          o << " w = 0.0";
+          for (size_t m = 0; m < pl->host_measured.size(); ++m) {
+            const int q = pl->host_measured[m];
+            o << " + (double)((__popcll(g2 & " << hex64(pl->perm_mask[q]) << ") + " << pl->perm_const[q]
+              << ") & 1) * " << (double)(1ull << m);
+          }
+          o << ";";
+        }
+        o << " e += w * (double)(z.x * z.x + z.y * z.y); gout[g2] = z;"
           << " if (glam) { C y; y.x = (R)w * z.x; y.y = (R)w * z.y; glam[g2] = y; }"
-          << " if (a.state) { double* dst = a.state + v * ((int64_t)1 << p.n_qubits) * 2; "
-             "dst[2 * g2] = (double)z.x * gph[0] - (double)z.y * gph[1]; "
-             "dst[2 * g2 + 1] = (double)z.x * gph[1] + (double)z.y * gph[0]; } }\n";
+          << " if (a.state) { double* dst = a.state + v * ((int64_t)1 << p.n_qubits) * 2; uint64_t gs = g2;";
+        if (pl->perm)
+          o << " gs = 0; for (int q_ = 0; q_ < p.n_qubits; ++q_) gs |= (uint64_t)((__popcll(g2 & p.perm_mask[q_]) + "
+               "p.perm_const[q_]) & 1) << q_;";
+        o << " dst[2 * gs] = (double)z.x * gph[0] - (double)z.y * gph[1]; "
+             "dst[2 * gs + 1] = (double)z.x * gph[1] + (double)z.y * gph[0]; } }\n";
       }
       o << "}\n";
     } else if (!direct_ok(WL)) {

@@ -44,6 +44,9 @@ struct DevPlan {
   int32_t n_fold_nonlocal;
   const int32_t* fold_local;    // first-tile qubits with differentiated folded gates
   int32_t n_fold_local;
+  int32_t perm;                 // trailing X/CNOT gates folded into the readout
+  const uint64_t* perm_mask;    // [n_qubits]
+  const int32_t* perm_const;    // [n_qubits]
 };
 
 struct KArgs {

@@ -511,3 +511,33 @@ def test_light_cone_cfg4_matches_full(monkeypatch):
     assert i1["plan"].description.startswith("n=10 ")
     np.testing.assert_allclose(r1, r0, atol=1e-12)
     np.testing.assert_allclose(j1.cpu().numpy(), j0.cpu().numpy(), atol=1e-11)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_trailing_permutation_state_and_readout(prec, monkeypatch):
+    # trailing X / CNOT gates fold into the readout (and the amplitude output)
+    monkeypatch.setenv("HQ_FORCE_STREAM", "1")
+    monkeypatch.setenv("HQ_TILE_BITS", "9")
+    n = 13
+    rng = np.random.default_rng(31)
+    c, oc = Circuit(n), O.Circuit(n)
+    for q in range(n):
+        a = float(rng.uniform(-3, 3))
+        c.ry(q, a); oc.add(O.Op("RY", (q,), a))
+    for q in range(n - 1):
+        c.cnot(q, q + 1); oc.add(O.Op("CNOT", (q, q + 1)))
+        b = float(rng.uniform(-3, 3))
+        c.rx(q + 1, b); oc.add(O.Op("RX", (q + 1,), b))
+    for k in range(12):                       # the trailing permutation
+        if k % 3 == 0:
+            q = int(rng.integers(n)); c.x(q); oc.add(O.Op("X", (q,)))
+        else:
+            a, t = (int(v) for v in rng.choice(n, 2, replace=False))
+            c.cnot(a, t); oc.add(O.Op("CNOT", (a, t)))
+    c.measure(0, 5, 12); oc.measure(0, 5, 12)
+    st = engine.final_states([c], prec)[0]
+    want = O.simulate(oc)
+    tol = 1e-12 if prec == "c128" else 2e-6
+    np.testing.assert_allclose(st, want, atol=tol)
+    e = engine.evaluate_circuits([c], prec)[0]
+    assert e == pytest.approx(O.expectation(oc), abs=1e-10 if prec == "c128" else 1e-4)
