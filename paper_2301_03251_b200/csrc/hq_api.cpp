@@ -264,14 +264,15 @@ namespace {
 // Greedy pass scheduler (see file comment).
 // excl0: qubits that must stay out of the first pass's tile (their folded
 // gates' gradients are read from λ contracted over that tile)
-std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int q, int f, uint64_t excl0 = 0) {
+std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int q, int f, uint64_t excl0 = 0,
+                                      size_t op_cap = kMaxPassOps) {
   std::vector<hq::Pass> passes;
   std::vector<char> done(ops.size(), 0);
   size_t left = ops.size();
   const uint64_t fixed = (f >= 64) ? ~0ull : ((1ull << f) - 1);
   // Tile choice by lookahead (HQ_PASS_LOOKAHEAD=0: first-come greedy + lowest-
   // qubit top-up): cfg4 17 -> 8 passes, 4,676 -> 5,646 samples/s
-  size_t max_ops = kMaxPassOps;   // HQ_MAX_PASS_OPS: test hook (code size per pass kernel)
+  size_t max_ops = op_cap;   // HQ_MAX_PASS_OPS: test hook (code size per pass kernel)
   if (const char* e = std::getenv("HQ_MAX_PASS_OPS")) max_ops = std::max<size_t>(8, std::min<size_t>(kMaxPassOps, std::atoll(e)));
   const char* pla = std::getenv("HQ_PASS_LOOKAHEAD");
   const bool lookahead = !(pla && pla[0] == '0');
@@ -632,7 +633,7 @@ const T* rebase(const T* rel, char* base) {
 
 // opts: kNoFold (no folded prefixes), kOnchipOk (small circuits may use the
 // shared-memory interpreter when the specialised kernels are unavailable)
-enum { kNoFold = 1, kPreferOnchip = 2 };
+enum { kNoFold = 1, kPreferOnchip = 2, kSmallPasses = 4 };
 static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts);
 
 extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
@@ -797,6 +798,9 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
     pl->tile_bits = tile_bits_for(d->precision);
     if (tb_env) pl->tile_bits = std::max(3, std::min(14, std::atoi(tb_env)));
     if (n < pl->tile_bits) pl->tile_bits = n;   // whole state in one tile
+    // the generic window kernels run at most 256 threads per tile
+    if ((opts & kSmallPasses) && pl->tile_bits - reg_bits_for(d->precision) > 8)
+      pl->tile_bits = reg_bits_for(d->precision) + 8;
     if (pl->tile_bits < 2) {
       delete pl;
       return fail(HQ_E_CONFIG, "circuit too small for the streaming path");
@@ -846,7 +850,8 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
         gates.resize(cut);
       }
     }
-    pl->passes = schedule_passes(gates, n, pl->tile_bits, f);
+    const size_t op_cap = (opts & kSmallPasses) ? 48 : kMaxPassOps;   // generic kernels: shared-memory tables per pass
+    pl->passes = schedule_passes(gates, n, pl->tile_bits, f, 0, op_cap);
 
     // ---- fold leading single-qubit gates into the initial product state ----
     // Qubits outside the first pass's tile: their whole single-qubit prefix
@@ -905,7 +910,7 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
         gates.swap(kept);
         // folded qubits with gradients: outside the first tile through λ contracted
         // over the tile (lamN), inside it through the tile-level contraction (locpart)
-        pl->passes = schedule_passes(gates, n, pl->tile_bits, f, fold_local_grad ? 0 : excl);
+        pl->passes = schedule_passes(gates, n, pl->tile_bits, f, fold_local_grad ? 0 : excl, op_cap);
         for (int b : pl->passes[0].local)
           if (excl >> b & 1ull) {
             if (!fold_local_grad) {
@@ -999,6 +1004,16 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
       delete pl;
       if (std::getenv("HQ_JIT_COMPILE_ONLY")) return fail(HQ_E_CONFIG, why);
       return plan_create_impl(d, out, opts | kNoFold | kPreferOnchip);
+    }
+    if (js != HQ_OK && !(opts & kSmallPasses)) {
+      // the generic window kernels keep per-pass tables in shared memory
+      size_t need = 0;
+      for (int i = 0; i < (int)pl->passes.size(); ++i)
+        need = std::max(need, std::max(hq::stream_smem_bytes(pl, i, false), hq::stream_smem_bytes(pl, i, true)));
+      if (need > 220 * 1024 || pl->tile_bits - pl->reg_bits > 8) {
+        delete pl;
+        return plan_create_impl(d, out, opts | kSmallPasses | kNoFold);
+      }
     }
     if (js != HQ_OK) {
       pl->jit.ok = false;

@@ -145,6 +145,15 @@ struct Gen {
   bool packed = false;  // complex64: FFMA2/FMUL2 on (re, im) pairs
   std::vector<int> map;  // logical register index -> variable number
   bool pending = false;  // a per-thread phase is pending in this window
+  bool ph_decl = false;  // phx/phy already declared in the current C++ scope
+  void declare_ph() {
+    if (ph_decl) {
+      o << "phx = (R)1; phy = (R)0;\n";
+    } else {
+      o << "R phx = (R)1, phy = (R)0;\n";
+      ph_decl = true;
+    }
+  }
 
   std::string R() const { return c64 ? "float" : "double"; }
   std::string P(int i) const { return "p" + std::to_string(map[i]); }
@@ -160,7 +169,7 @@ struct Gen {
   std::string trig(int s, int k) const { return "trig[" + std::to_string(8 * s + k) + "]"; }
 
   void ensure_pending() {
-    if (!pending) { o << "R phx = (R)1, phy = (R)0;\n"; pending = true; }
+    if (!pending) { declare_ph(); pending = true; }
   }
   // in-place rotation of the real pair (x, y) by the slot's half angle (sign
   // folded into the pending phase by the caller): 3 FMA
@@ -179,7 +188,7 @@ struct Gen {
   }
   void pend(const std::string& c, const std::string& x, const std::string& y) {
     // php *= (c ? (x, y) : (1, 0))
-    if (!pending) { o << "R phx = (R)1, phy = (R)0;\n"; pending = true; }
+    if (!pending) { declare_ph(); pending = true; }
     o << "{ const bool c_ = " << c << "; const R ex = c_ ? (R)(" << x << ") : (R)1, ey = c_ ? (R)(" << y
       << ") : (R)0; const R t_ = phx * ex - phy * ey; phy = phx * ey + phy * ex; phx = t_; }\n";
   }
@@ -288,7 +297,7 @@ struct Gen {
             });
             o << "}\n";
           } else {
-            if (!pending) { o << "R phx = (R)1, phy = (R)0;\n"; pending = true; }
+            if (!pending) { declare_ph(); pending = true; }
             o << "{ const R c_ = " << trig(op.slot, 0) << ", s_ = " << cond(a) << " ? " << s1 << trig(op.slot, 1)
               << " : " << s0 << trig(op.slot, 1) << "; const R t_ = phx * c_ - phy * s_; phy = phx * s_ + phy * c_; phx = t_; }\n";
           }
@@ -905,7 +914,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       const bool uni = op.kind == HQ_GATE_CNOT && !Gen::is_reg(op.a) && (op.a >= 64 || op.a - 16 >= 5);
       if (budget > 0 && uni) {
         const std::vector<int> map0 = g.map, bq0 = g.bq;
-        const bool pend0 = g.pending, na0 = na;
+        const bool pend0 = g.pending, na0 = na, decl0 = g.ph_decl;
         if (op.a < 64) na = true;
         WOp x{};
         x.kind = HQ_GATE_X;
@@ -920,11 +929,13 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         g.map = map0;
         g.bq = bq0;
         g.pending = pend0;
+        g.ph_decl = decl0;
         emit_steps(ks, i + 1, adj, tail, budget - 1);
         o << "}\n";
         g.map = map0;
         g.bq.clear();
         g.pending = pend0;
+        g.ph_decl = decl0;
         na = na0;
         return;
       }
@@ -1031,6 +1042,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     for (int w = 0; w < nwin; ++w) {
       const WinDev& W = P.wins[w];
       o << "{ // window " << w << "\n";
+      g.ph_decl = false;
       g.win_tb(W, tbits);
       if (!(w == 0 && regs_live)) {
         identity_map();
@@ -1138,6 +1150,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         regs_live = false;
       } else if (direct_ok(WL)) {
         o << "{ // window " << nwin - 1 << " (adjoint): direct load\n";
+        g.ph_decl = false;
         g.win_tb(WL, tbits);
         direct_load(WL, true);
         regs_live = true;
@@ -1158,6 +1171,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       const bool cont = wi == 0 && regs_live;  // block already open, registers hold window w
       if (!cont) {
         o << "{ // window " << w << " (adjoint)\n";
+        g.ph_decl = false;
         g.win_tb(W, tbits);
         identity_map();
         if (!(ablate & 1)) {

@@ -541,3 +541,30 @@ def test_trailing_permutation_state_and_readout(prec, monkeypatch):
     np.testing.assert_allclose(st, want, atol=tol)
     e = engine.evaluate_circuits([c], prec)[0]
     assert e == pytest.approx(O.expectation(oc), abs=1e-10 if prec == "c128" else 1e-4)
+
+
+def test_randomised_streaming_sweep(monkeypatch):
+    # tools/fuzz_parity.py's generator at a fixed seed: random gates, tiles
+    # 9-12, half the circuits ending in a CNOT layer (trailing permutation);
+    # caught a phase-variable redeclaration in fused kernels
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "fuzz_parity", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools",
+                                    "fuzz_parity.py"))
+    fz = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(fz)
+    rng = np.random.default_rng(77)
+    for t in range(8):
+        n = int(rng.integers(9, 14))
+        monkeypatch.setenv("HQ_FORCE_STREAM", "1")
+        monkeypatch.setenv("HQ_TILE_BITS", str(int(rng.integers(9, min(n, 12) + 1))))
+        b = fz.builder_for(n, int(rng.integers(20, 70)), rng)
+        x = rng.uniform(-3, 3, (2, 2))
+        th = rng.uniform(0, 6, 4)
+        out, jx, jp, _, _ = O.layer(lambda i, p: b(i, p, Circ=O.Circuit), x, th)
+        for prec in PRECS:
+            res, jac, info = engine.run_batch(b, x, th, True, True, prec, cache=engine.PlanCache(2))
+            check_vals(res, out, prec)
+            j = jac.cpu().numpy()
+            check_vals(j[:, :2], jx, prec, grad=True)
+            check_vals(j[:, 2:], jp, prec, grad=True)
