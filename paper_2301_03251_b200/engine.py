@@ -266,7 +266,7 @@ def _check_preps(tape: tr.Tape, x: np.ndarray, theta: np.ndarray):
 
 def run_batch(builder, xd: np.ndarray, pd: np.ndarray, want_x: bool, want_p: bool,
               precision: str = "c128", shift: float = math.pi / 2, grad_scale: float = 0.5,
-              cache: PlanCache | None = None):
+              cache: PlanCache | None = None, light_cone: bool = False):
     """Host-boundary entry: numpy in, numpy out.
 
     Returns ``(out [B], jac [B, d+P] | None, info)``.
@@ -279,7 +279,7 @@ def run_batch(builder, xd: np.ndarray, pd: np.ndarray, want_x: bool, want_p: boo
         return run_per_sample(builder, xd, pd, want_x, want_p, precision, shift, grad_scale)
     if tape.preps:
         _check_preps(tape, xd, pd)
-    if os.environ.get("HQ_LIGHTCONE") == "1":
+    if light_cone or os.environ.get("HQ_LIGHTCONE") == "1":
         # opt-in: drop gates outside the readout's backward light cone (identical E and gradients)
         tape = tr.light_cone(tape) or tape
     wanted = [want_x] * d + [want_p] * P

@@ -568,3 +568,20 @@ def test_randomised_streaming_sweep(monkeypatch):
             j = jac.cpu().numpy()
             check_vals(j[:, :2], jx, prec, grad=True)
             check_vals(j[:, 2:], jp, prec, grad=True)
+
+
+def test_light_cone_layer_keyword():
+    from paper_2301_03251_b200 import workloads as wl
+    b = wl.make_builder("cfg4", qsim, T)
+    x = wl.inputs_for("cfg4", 3)
+    th = wl.params_for("cfg4")
+    outs = []
+    for lc in (False, True):
+        layer = QuantumLayer(b, n_params=th.size, param_init=th, light_cone=lc)
+        xt = Tensor(x, requires_grad=False, dtype=np.float64)
+        out = layer(xt)
+        backward(tsum(out))
+        outs.append((out.numpy()[:, 0], layer.params.grad.copy(), layer.last_info["plan"].description))
+    assert outs[1][2].startswith("n=10 ") and outs[0][2].startswith("n=20 ")
+    np.testing.assert_allclose(outs[1][0], outs[0][0], atol=1e-12)
+    np.testing.assert_allclose(outs[1][1], outs[0][1], atol=1e-11)
