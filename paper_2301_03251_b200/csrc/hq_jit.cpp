@@ -579,11 +579,6 @@ typedef unsigned long size_t;
 
 const char* kHelpers = R"(
 __device__ __forceinline__ void bar_na() { asm volatile("barrier.sync 0;" ::: "memory"); }
-__device__ __forceinline__ void cp8(void* s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"((unsigned)__cvta_generic_to_shared(s)), "l"(g) : "memory"); }
-__device__ __forceinline__ void cp16(void* s, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"((unsigned)__cvta_generic_to_shared(s)), "l"(g) : "memory"); }
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 namespace hq {
 __device__ __forceinline__ uint32_t jpad(uint32_t j) { return j + (j >> 4) + (j >> 8); }
 // packed FP32x2 (sm_100 FFMA2/FMUL2/FADD2): a complex64 amplitude is one
@@ -609,18 +604,6 @@ __device__ __forceinline__ float2 swp2(float2 a) { return make_float2(a.y, a.x);
 // z * (c + i s) = z*c + swap(z)*(-s, s)
 __device__ __forceinline__ float2 cmul2f(float2 z, float c, float s) {
   return fma2(swp2(z), make_float2(-s, s), mul2(z, bc2(c))); }
-template <int BYTES>
-__device__ __forceinline__ void cp_async(void* dst, const void* src) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-  if (BYTES == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
-  else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
-}
-__device__ __forceinline__ void prefetch_l2_64(const void* p) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], 64;\n" ::"l"(p));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 __device__ __forceinline__ float fmaf_r(float a, float b, float c) { return fmaf(a, b, c); }
 __device__ __forceinline__ double fmaf_r(double a, double b, double c) { return fma(a, b, c); }
 __device__ __forceinline__ float warp_sum_r(float v) {
@@ -944,61 +927,12 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     tail();
   };
 
-  // Tile prefetch (cp.async) into the transposition buffers: once the last
-  // window of a tile has read its registers from shared memory, the next
-  // tile's first window is copied into tp/tl asynchronously, overlapping that
-  // window's math and HBM store; the next tile then starts from shared memory.
-  // Needs direct (HBM-contiguous) first and last windows.
-  const WinDev& Wfirst = bwd ? P.wins[nwin - 1] : P.wins[0];
-  bool pf = !fused && !(fwd && first) && !(fwd && last) && direct_ok(Wfirst) &&
-            (bwd ? (first || direct_ok(P.wins[0])) : direct_ok(P.wins[nwin - 1]));
-  {
-    const char* e = std::getenv("HQ_PF");
-    if (!(e && e[0] == '1')) pf = false;
-  }
-  auto emit_tile_prefetch = [&](const char* texpr) {
-    o << "{ const uint64_t t2 = " << texpr << "; const uint64_t base2 = 0ull";
-    for (size_t i = 0; i < nonlocal.size(); ++i) o << " | (((t2 >> " << i << ") & 1ull) << " << nonlocal[i] << ")";
-    o << ";\n";
-    g.win_tb(Wfirst, tbits);
-    emit_tw(Wfirst);
-    for (int i = 0; i < g.N; ++i) {
-      const char* cp = c64 ? "cp8" : "cp16";
-      o << cp << "(&tp[tb + " << g.phys(Wfirst, i) << "u], gpsi + (base2 | tw | " << hex64(reg_goff(Wfirst, i)) << "));\n";
-      if (bwd) o << cp << "(&tl[tb + " << g.phys(Wfirst, i) << "u], glam + (base2 | tw | " << hex64(reg_goff(Wfirst, i)) << "));\n";
-    }
-    o << "}\n";
-  };
-  if (pf) emit_tile_prefetch("(uint64_t)chunk * ps.tpc");
-
   // ---- tile loop
   o << "for (int tt = 0; tt < ps.tpc; ++tt) {\n"
     << "const uint64_t t = (uint64_t)chunk * ps.tpc + tt;\n"
     << "const uint64_t base = 0ull";
   for (size_t i = 0; i < nonlocal.size(); ++i) o << " | (((t >> " << i << ") & 1ull) << " << nonlocal[i] << ")";
   o << ";\n";
-
-  // L2 prefetch of the next tile: 2^(Q-f) contiguous runs of 2^f amplitudes
-  // (64 B) per vector, spread over the threads; issued once the current tile's
-  // loads are out, so the next tile's loads hit L2 instead of HBM.
-  // measured slower on cfg4 (3,276 vs 3,533 samples/s): opt-in via HQ_L2PF=1
-  const bool l2pf = std::getenv("HQ_L2PF") && !(fwd && first && !bwd);
-  auto emit_prefetch = [&](bool lam) {
-    if (!l2pf) return;
-    const int runs = 1 << (g.Q - f);
-    o << "if (tt + 1 < ps.tpc) { const uint64_t t2 = t + 1; const uint64_t base2 = 0ull";
-    for (size_t i = 0; i < nonlocal.size(); ++i) o << " | (((t2 >> " << i << ") & 1ull) << " << nonlocal[i] << ")";
-    o << ";\n";
-    for (int r0 = 0; r0 < runs; r0 += g.T) {
-      // run index = tid + r0; its tile index bits start at bit f
-      o << "{ const uint32_t run = (uint32_t)tid + " << r0 << "u; if (run < " << runs << "u) { uint64_t off = 0ull;";
-      for (int bb = 0; bb < g.Q - f; ++bb) o << " if ((run >> " << bb << ") & 1u) off |= " << hex64(gbit[f + bb]) << ";";
-      o << " prefetch_l2_64(gpsi + (base2 | off));";
-      if (lam) o << " prefetch_l2_64(glam + (base2 | off));";
-      o << " } }\n";
-    }
-    o << "}\n";
-  };
 
   bool regs_live = false;  // registers hold the current window's data
   if (fwd) {
@@ -1025,8 +959,6 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         o << "else { for (uint32_t j = tid; j < (1u << Q); j += T) { tp[jpad(j)].x = (R)((base | goff_j(j)) == 0); "
              "tp[jpad(j)].y = (R)0; } } }\n__syncthreads();\n";
       }
-    } else if (pf) {
-      o << "cp_wait();\n__syncthreads();\n";
     } else if (direct_ok(W0)) {
       o << "{ // window 0: direct load\n";
       direct_load(W0, false);
@@ -1037,7 +969,6 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       for (int i = 0; i < g.N; ++i) o << "tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u] = p" << i << ";\n";
       o << "__syncthreads();\n";
     }
-    if (!first) emit_prefetch(false);
     // -- forward windows
     for (int w = 0; w < nwin; ++w) {
       const WinDev& W = P.wins[w];
@@ -1047,10 +978,6 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       if (!(w == 0 && regs_live)) {
         identity_map();
         g.load_regs(W, "p", "tp");
-      }
-      if (pf && w == nwin - 1) {
-        o << "__syncthreads();\nif (tt + 1 < ps.tpc) ";
-        emit_tile_prefetch("t + 1");
       }
       g.pending = false;
       std::vector<int> ks;
@@ -1145,10 +1072,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     const WinDev& WL = P.wins[nwin - 1];
     if (!fused) {
       identity_map();
-      if (pf) {
-        o << "cp_wait();\n__syncthreads();\n";
-        regs_live = false;
-      } else if (direct_ok(WL)) {
+      if (direct_ok(WL)) {
         o << "{ // window " << nwin - 1 << " (adjoint): direct load\n";
         g.ph_decl = false;
         g.win_tb(WL, tbits);
@@ -1163,7 +1087,6 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         regs_live = false;
       }
     }
-    if (!fused) emit_prefetch(true);
     for (int wi = 0; wi < nwin; ++wi) {
       const int w = nwin - 1 - wi;
       if (first && w < stop_win) break;
@@ -1178,10 +1101,6 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
           g.load_regs(W, "p", "tp");
           g.load_regs(W, "l", "tl");
         }
-      }
-      if (pf && (first ? (wi == nwin - 1 || w == stop_win) : (w == 0))) {
-        o << "__syncthreads();\nif (tt + 1 < ps.tpc) ";
-        emit_tile_prefetch("t + 1");
       }
       g.pending = false;
       const int lo = std::max<int>(W.op0, first ? stop_op : 0);
