@@ -976,6 +976,12 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
     if (g.kind == HQ_GATE_RX || g.kind == HQ_GATE_RY) rot_slots.push_back(g.slot);
   }
 
+  if (pl->onchip && n <= 4 && !pl->has_preps) {
+    // one-thread-per-sample specialised kernel; the interpreter stays for
+    // initial states, amplitude output or without NVRTC
+    std::string why;
+    if (hq::jit_build(pl, why) != HQ_OK) pl->jit.small = nullptr;
+  }
   if (!pl->onchip && std::getenv("HQ_PLAN_WINDOWS")) {
     std::fprintf(stderr, "hq windows:");
     for (const auto& ps : pl->passes) std::fprintf(stderr, " %d/%zu", ps.n_dops, ps.wins.size());
@@ -1029,7 +1035,7 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
      << " slots=" << d->n_slots << " preps=" << d->n_preps << " adjoint_slots=" << pl->n_adj
      << " twopoint_vars=" << pl->n_tp;
   if (pl->onchip) {
-    os << " path=onchip smem=" << hq::onchip_smem_bytes(pl);
+    os << " path=onchip smem=" << hq::onchip_smem_bytes(pl) << (pl->jit.small ? " kernel=small-jit" : "");
   } else {
     os << " path=stream kernels=" << (pl->jit.ok ? "jit" : "generic") << " tile_bits=" << pl->tile_bits
        << " reg_bits=" << pl->reg_bits << " folded=" << pl->fold_ops << (pl->fold_grad ? "(grad)" : "")

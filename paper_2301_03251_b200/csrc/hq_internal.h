@@ -141,5 +141,6 @@ struct hq_plan_s {
     std::string why;                      // why the static kernels run instead
     std::vector<cudaKernel_t> fwd, bwd;   // per pass
     cudaKernel_t fused = nullptr;         // last forward pass + its backward
+    cudaKernel_t small = nullptr;         // on-chip plans up to 4 qubits: one thread per sample
   } jit;
 };

@@ -1242,6 +1242,100 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   return o.str();
 }
 
+// One thread per (virtual) sample for the smallest circuits (n ≤ 4): the
+// whole state and λ in registers (2^n each), every gate a compile-time
+// register operation (renamings, shears, phases), derivative dots into
+// register accumulators.  Readout / gradients only; initial states, state
+// loads and amplitude output stay with the interpreter.
+static std::string gen_small(const hq_plan_s* pl) {
+  const bool c64 = pl->precision == HQ_C64;
+  Gen g;
+  g.RB = pl->n_qubits;
+  g.N = 1 << g.RB;
+  g.Q = pl->n_qubits;
+  g.T = 1;
+  g.c64 = c64;
+  g.packed = c64 && !std::getenv("HQ_NO_F32X2");
+  g.exact = false;
+  g.map.assign(g.N, 0);
+  for (int i = 0; i < g.N; ++i) g.map[i] = i;
+  std::ostringstream& o = g.o;
+  const int A = std::max(1, pl->n_slots);
+  std::vector<WOp> wops;
+  std::vector<int> dslot_of_dl;
+  for (const DOp& d : pl->dops) {
+    WOp w{};
+    w.kind = (int8_t)d.kind;
+    w.a = (int8_t)d.a;
+    w.b = (int8_t)d.b;
+    w.slot = (int16_t)d.slot;
+    w.dl = -1;
+    if (d.dslot >= 0) {
+      w.dl = (int16_t)dslot_of_dl.size();
+      dslot_of_dl.push_back(d.dslot);
+    }
+    wops.push_back(w);
+  }
+  const int K = (int)dslot_of_dl.size();
+  o << "extern \"C\" __global__ void __launch_bounds__(128) hq_small(const hq::KArgs a) {\n"
+    << "using namespace hq;\n"
+    << "typedef " << g.R() << " R; typedef " << (c64 ? "float2" : "double2") << " C;\n"
+    << "const R HH = (R)0.70710678118654752440;\n(void)HH;\n"
+    << "const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;\nif (v >= a.V) return;\n"
+    << "const DevPlan& p = a.p;\nconst VSample vs = decode_vsample(p, v, a.B);\n"
+    << "const double* xr = a.x + vs.b * a.ldx;\n"
+    << "R trig[" << 8 * A << "];\n"
+    << "for (int i = 0; i < p.n_slots; ++i) { const double sv = eval_slot(p, i, xr, a.theta, vs.shvar, vs.shval); "
+       "double sn, cs; sincos(0.5 * sv, &sn, &cs); const double sg = cs < 0.0 ? -1.0 : 1.0; "
+       "const double c2 = sg * cs, s2 = sg * sn; trig[8 * i] = (R)cs; trig[8 * i + 1] = (R)sn; "
+       "trig[8 * i + 2] = (R)(cs * cs - sn * sn); trig[8 * i + 3] = (R)(2.0 * cs * sn); "
+       "trig[8 * i + 4] = (R)(-s2 / (1.0 + c2)); trig[8 * i + 5] = (R)s2; trig[8 * i + 6] = (R)sg; "
+       "trig[8 * i + 7] = (R)0; }\n";
+  o << "C";
+  for (int i = 0; i < g.N; ++i) o << (i ? ", " : " ") << "p" << i;
+  o << ";\n";
+  for (int i = 0; i < g.N; ++i) o << "p" << i << ".x = (R)" << (i == 0 ? 1 : 0) << "; p" << i << ".y = (R)0;\n";
+  for (const WOp& w : wops) g.apply(w, false, false);
+  g.flush_pending(false);
+  // readout weights: w(i) = Σ_k 2^k bit(i, measured[k])
+  auto weight = [&](int i) {
+    double wv = 0.0;
+    for (size_t k = 0; k < pl->host_measured.size(); ++k)
+      if ((i >> pl->host_measured[k]) & 1) wv += (double)(1ull << k);
+    return wv;
+  };
+  o << "double e = 0.0;\n";
+  for (int i = 0; i < g.N; ++i) {
+    const double wv = weight(i);
+    if (wv != 0.0)
+      o << "e += " << wv << " * (double)(" << g.P(i) << ".x * " << g.P(i) << ".x + " << g.P(i) << ".y * " << g.P(i)
+        << ".y);\n";
+  }
+  o << "if (vs.u < 0) a.out[v] = e; else a.tp[vs.u] = e;\n";
+  if (K > 0) {
+    o << "if (a.want_adj && vs.u < 0) {\nC";
+    for (int i = 0; i < g.N; ++i) o << (i ? ", " : " ") << "l" << i;
+    o << ";\n";
+    for (int i = 0; i < g.N; ++i)
+      o << g.L(i) << ".x = (R)" << weight(i) << " * " << g.P(i) << ".x; " << g.L(i) << ".y = (R)" << weight(i) << " * "
+        << g.P(i) << ".y;\n";
+    for (int k = 0; k < K; ++k) o << "R da" << k << " = (R)0;\n";
+    g.pending = false;
+    g.ph_decl = false;
+    for (int k = (int)wops.size() - 1; k >= 0; --k) {
+      g.dot(wops[k], true, 32, 1, K);
+      g.apply(wops[k], true, true);
+    }
+    g.flush_pending(true);
+    for (int k = 0; k < K; ++k)
+      o << "{ double* dst = a.dpart + (v * p.n_adj + " << dslot_of_dl[k] << ") * a.n_parts; dst[0] = (double)da" << k
+        << "; for (int q_ = 1; q_ < a.n_parts; ++q_) dst[q_] = 0.0; }\n";
+    o << "}\n";
+  }
+  o << "}\n";
+  return o.str();
+}
+
 namespace {
 
 struct Unit {
@@ -1283,12 +1377,14 @@ hq_status jit_build(hq_plan_s* pl, std::string& err) {
   const char* env = std::getenv("HQ_JIT");
   if (env && env[0] == '0') { err = "disabled by HQ_JIT=0"; return HQ_E_CONFIG; }
   Nvrtc& nv = nvrtc();
-  const int np = (int)pl->passes.size();
+  const bool small = pl->onchip;
+  const int np = small ? 1 : (int)pl->passes.size();
   const std::string head = std::string(kHeader) + kJitPod + kJitDev + kHelpers;
   std::vector<Unit> units(np);
   std::string dump;
   for (int i = 0; i < np; ++i) {
-    units[i].src = head + gen_pass(pl, i, 0) + gen_pass(pl, i, 1) + (i == np - 1 ? gen_pass(pl, i, 2) : "");
+    units[i].src = small ? head + gen_small(pl)
+                         : head + gen_pass(pl, i, 0) + gen_pass(pl, i, 1) + (i == np - 1 ? gen_pass(pl, i, 2) : "");
     units[i].hash = fnv1a(units[i].src);
     if (std::getenv("HQ_JIT_DUMP")) dump += units[i].src;
   }
@@ -1329,6 +1425,28 @@ hq_status jit_build(hq_plan_s* pl, std::string& err) {
     }
   }
   if (std::getenv("HQ_JIT_COMPILE_ONLY")) { err = "compile-only"; return HQ_E_CONFIG; }
+  if (small) {
+    cudaLibrary_t lib = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      auto it = g_libs.find(units[0].hash);
+      if (it != g_libs.end()) lib = it->second;
+    }
+    if (!lib) {
+      cudaError_t ce = cudaLibraryLoadData(&lib, units[0].cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+      if (ce != cudaSuccess) {
+        err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(ce);
+        return HQ_E_CUDA;
+      }
+      std::lock_guard<std::mutex> lk(g_mu);
+      g_libs[units[0].hash] = lib;
+    }
+    if (cudaLibraryGetKernel(&pl->jit.small, lib, "hq_small") != cudaSuccess) {
+      err = "generated kernel missing";
+      return HQ_E_CUDA;
+    }
+    return HQ_OK;
+  }
   pl->jit.fwd.assign(np, nullptr);
   pl->jit.bwd.assign(np, nullptr);
   for (int i = 0; i < np; ++i) {
@@ -1366,6 +1484,12 @@ hq_status jit_build(hq_plan_s* pl, std::string& err) {
   }
   pl->jit.ok = true;
   return HQ_OK;
+}
+
+cudaError_t jit_launch_small(const hq_plan_s* pl, const KArgs& a, cudaStream_t st) {
+  KArgs ac = a;
+  void* args[] = {&ac};
+  return cudaLaunchKernel((const void*)pl->jit.small, dim3((unsigned)((a.V + 127) / 128)), dim3(128), args, 0, st);
 }
 
 cudaError_t jit_launch_pass(const hq_plan_s* pl, int i, int mode, const KArgs& a, const JPass& ps,

@@ -20,6 +20,8 @@ JitLayout jit_layout(const hq_plan_s* pl, int pass, bool bwd, bool fused = false
 // compile (or fetch from the in-process / on-disk cache) the plan's pass kernels
 hq_status jit_build(hq_plan_s* pl, std::string& err);
 // mode 0 forward, 1 backward, 2 fused last-forward + first-backward
+// one-thread-per-sample kernel of a small on-chip plan (readout + gradients)
+cudaError_t jit_launch_small(const hq_plan_s* pl, const KArgs& a, cudaStream_t st);
 cudaError_t jit_launch_pass(const hq_plan_s* pl, int pass, int mode, const KArgs& a, const JPass& ps,
                             unsigned grid, cudaStream_t st);
 

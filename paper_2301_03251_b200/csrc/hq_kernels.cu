@@ -18,6 +18,7 @@
 #include <cstdio>
 
 #include "hq_common.cuh"
+#include "hq_jit.h"
 
 namespace hq {
 
@@ -191,6 +192,11 @@ int onchip_parts(const hq_plan_s* pl) { return onchip_threads(pl->n_qubits) / 32
 
 template <typename R>
 static cudaError_t run_onchip(const hq_plan_s* pl, const KArgs& a, cudaStream_t st) {
+  if (pl->jit.small && !a.init && !a.state) {
+    ProfScope ps(pl, st, HQ_K_ONCHIP, (double)a.B * (pl->n_inputs + 1) * 8.0);
+    cudaError_t e = jit_launch_small(pl, a, st);
+    return e != cudaSuccess ? e : cudaGetLastError();
+  }
   const size_t smem = onchip_smem(pl, sizeof(R) == 4);
   const int T = onchip_threads(pl->n_qubits);
   cudaError_t e = cudaFuncSetAttribute(k_onchip<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

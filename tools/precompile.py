@@ -38,7 +38,7 @@ def plan_for(cfg, prec, want_x=False, want_p=True):
 if __name__ == "__main__":
     engine._torch = lambda: _FakeTorch
     # cfg:prec[:x] (x: input gradients too, as cfg1/cfg2 train them)
-    jobs = sys.argv[1:] or ["cfg4:c64", "cfg4:c128", "cfg3:c128", "cfg2:c64:x"]
+    jobs = sys.argv[1:] or ["cfg4:c64", "cfg4:c128", "cfg3:c128", "cfg2:c64:x", "cfg1:c128:x", "cfg1:c64:x"]
     for job in jobs:
         parts = job.split(":")
         plan_for(parts[0], parts[1], want_x=len(parts) > 2 and parts[2] == "x")
