@@ -772,7 +772,8 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
 
   // ---- header / prologue
   // occupancy hint: ~128 registers per thread for ψ+λ kernels, ~80 for forward
-  const int minb = std::max(1, 65536 / (g.T * (bwd ? 128 : 80)));
+  int minb = std::max(1, 65536 / (g.T * (bwd ? 128 : 80)));
+  if (const char* e = std::getenv(bwd ? "HQ_BWD_MINB" : "HQ_FWD_MINB")) minb = std::max(1, std::atoi(e));
   o << "extern \"C\" __global__ void __launch_bounds__(" << g.T << ", " << minb << ") "
     << (fused ? "hq_fb" : (bwd ? "hq_b" : "hq_f")) << pi << "(const hq::KArgs a, const hq::JPass ps) {\n"
     << "using namespace hq;\n"
