@@ -1228,13 +1228,16 @@ static hq_status run(hq_plan pl, const double* x, int64_t ldx, const double* the
   if (init && pl->fold) {
     // a caller-provided initial state replaces the folded product state: run
     // the same tape unfolded (same workspace layout for hq_state)
-    if (!pl->twin) {
-      hq_plan tw = nullptr;
-      const hq_status st = plan_create_impl(&static_cast<DescCopy*>(pl->desc_copy.get())->d, &tw, kNoFold);
-      if (st != HQ_OK) return st;
-      pl->twin = tw;
+    hq_plan tw = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(pl->twin_mu);
+      if (!pl->twin) {
+        const hq_status st = plan_create_impl(&static_cast<DescCopy*>(pl->desc_copy.get())->d, &pl->twin, kNoFold);
+        if (st != HQ_OK) return st;
+      }
+      tw = pl->twin;
     }
-    return run(pl->twin, x, ldx, theta, batch, flags, out, jac, state, init, init_rows, ws, ws_bytes, stream);
+    return run(tw, x, ldx, theta, batch, flags, out, jac, state, init, init_rows, ws, ws_bytes, stream);
   }
   const Layout L = layout_for(pl, batch, flags);
   if (ws_bytes < L.total || (!ws && L.total > 256)) return fail(HQ_E_CONFIG, "workspace too small");

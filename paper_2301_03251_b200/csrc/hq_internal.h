@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -136,6 +137,7 @@ struct hq_plan_s {
   // hq_state with a caller-provided initial state runs on an unfolded twin
   std::shared_ptr<void> desc_copy;
   hq_plan_s* twin = nullptr;
+  std::mutex twin_mu;                     // plans are shared across threads; the twin is built once
   struct Jit {
     bool ok = false;
     std::string why;                      // why the static kernels run instead
