@@ -184,7 +184,8 @@ size_t hq_noisy_workspace_bytes(hq_plan plan, int64_t batch, int32_t flags, int3
  * out[b] = Σ outcome / shots (qnn.py:27-32); HQ_WANT_JAC: jac rows by the
  * two-point rule on the same streams (every differentiated variable must be
  * HQ_GRAD_TWOPOINT); counts (optional) [batch, 2^m] uint64.  Complex128
- * state; circuits up to 13 qubits without state loads.
+ * state; circuits up to 26 qubits without state loads (n > 13: the state lives
+ * in the workspace, see hq_noisy_workspace_bytes).
  * Replaces: qnn.py:109-111 (NOISY _execute) and its shift-rule closures. */
 hq_status hq_noisy(hq_plan plan, const double* x, int64_t ldx, const double* theta, int64_t batch,
                    int32_t flags, const hq_noise_site* sites, int32_t n_sites, int64_t shots, uint64_t seed,

@@ -60,10 +60,44 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 
 
+// Execution teams: one warp per trajectory with the state in shared memory
+// (n ≤ 13), or one 256-thread CTA per trajectory with the state in global
+// memory (larger circuits, up to the reference's 24 qubits and beyond).
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct WarpTeam {
+  int tid;
+  static constexpr int T = 32;
+  __device__ void sync() const { __syncwarp(); }
+  __device__ double sum(double v) const { return warp_sum_d(v); }
+};
+
+struct BlockTeam {
+  int tid;
+  double* red;  // [T / 32] shared
+  static constexpr int T = 256;
+  __device__ void sync() const { __syncthreads(); }
+  __device__ double sum(double v) const {  // fixed order, result on every thread
+    v = warp_sum_d(v);
+    if ((tid & 31) == 0) red[tid >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int w = 0; w < T / 32; ++w) s += red[w];
+    __syncthreads();
+    return s;
+  }
+};
+
 // 2x2 gate on qubit q (qsim.py:25-45 matrices)
-__device__ void w_gate1(double2* psi, int n, int q, double2 m00, double2 m01, double2 m10, double2 m11, int lane) {
+template <class Team>
+__device__ void t_gate1(double2* psi, int n, int q, double2 m00, double2 m01, double2 m10, double2 m11,
+                        const Team& tm) {
   const uint32_t half = 1u << (n - 1);
-  for (uint32_t i = lane; i < half; i += 32) {
+  for (uint32_t i = tm.tid; i < half; i += Team::T) {
     const uint32_t i0 = ins0(i, q), i1 = i0 | (1u << q);
     const double2 a0 = psi[i0], a1 = psi[i1];
     psi[i0] = cadd(cmul(m00, a0), cmul(m01, a1));
@@ -71,31 +105,32 @@ __device__ void w_gate1(double2* psi, int n, int q, double2 m00, double2 m01, do
   }
 }
 
-__device__ void w_apply(double2* psi, int n, int kind, int q0, int q1, double ang, int lane) {
+template <class Team>
+__device__ void t_apply(double2* psi, int n, int kind, int q0, int q1, double ang, const Team& tm) {
   const double2 z = make_double2(0.0, 0.0), one = make_double2(1.0, 0.0);
   switch (kind) {
     case HQ_GATE_H: {
       const double h = 0.70710678118654752440;
-      w_gate1(psi, n, q0, make_double2(h, 0), make_double2(h, 0), make_double2(h, 0), make_double2(-h, 0), lane);
+      t_gate1(psi, n, q0, make_double2(h, 0), make_double2(h, 0), make_double2(h, 0), make_double2(-h, 0), tm);
       break;
     }
-    case HQ_GATE_X: w_gate1(psi, n, q0, z, one, one, z, lane); break;
-    case HQ_GATE_Y: w_gate1(psi, n, q0, z, make_double2(0, -1), make_double2(0, 1), z, lane); break;
-    case HQ_GATE_Z: w_gate1(psi, n, q0, one, z, z, make_double2(-1, 0), lane); break;
+    case HQ_GATE_X: t_gate1(psi, n, q0, z, one, one, z, tm); break;
+    case HQ_GATE_Y: t_gate1(psi, n, q0, z, make_double2(0, -1), make_double2(0, 1), z, tm); break;
+    case HQ_GATE_Z: t_gate1(psi, n, q0, one, z, z, make_double2(-1, 0), tm); break;
     case HQ_GATE_RX: {
       const double c = cos(ang / 2.0), s = sin(ang / 2.0);
-      w_gate1(psi, n, q0, make_double2(c, 0), make_double2(0, -s), make_double2(0, -s), make_double2(c, 0), lane);
+      t_gate1(psi, n, q0, make_double2(c, 0), make_double2(0, -s), make_double2(0, -s), make_double2(c, 0), tm);
       break;
     }
     case HQ_GATE_RY: {
       const double c = cos(ang / 2.0), s = sin(ang / 2.0);
-      w_gate1(psi, n, q0, make_double2(c, 0), make_double2(-s, 0), make_double2(s, 0), make_double2(c, 0), lane);
+      t_gate1(psi, n, q0, make_double2(c, 0), make_double2(-s, 0), make_double2(s, 0), make_double2(c, 0), tm);
       break;
     }
     case HQ_GATE_RZ: {
       double s, c;
       sincos(0.5 * ang, &s, &c);
-      w_gate1(psi, n, q0, make_double2(c, -s), z, z, make_double2(c, s), lane);
+      t_gate1(psi, n, q0, make_double2(c, -s), z, z, make_double2(c, s), tm);
       break;
     }
     default: {  // two-qubit kinds: loop over the quarter space
@@ -104,7 +139,7 @@ __device__ void w_apply(double2* psi, int n, int kind, int q0, int q1, double an
       const uint32_t b0 = 1u << q0, b1 = 1u << q1;
       double2 ph = make_double2(-1.0, 0.0);
       if (kind == HQ_GATE_CR) { double s, c; sincos(ang, &s, &c); ph = make_double2(c, s); }
-      for (uint32_t i = lane; i < quarter; i += 32) {
+      for (uint32_t i = tm.tid; i < quarter; i += Team::T) {
         const uint32_t base = ins0(ins0(i, lo), hi);
         if (kind == HQ_GATE_CNOT) {
           const double2 t = psi[base | b0];
@@ -121,38 +156,28 @@ __device__ void w_apply(double2* psi, int n, int kind, int q0, int q1, double an
       break;
     }
   }
-  __syncwarp();
+  tm.sync();
 }
 
-__device__ __forceinline__ double warp_sum_d(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-__global__ void k_noisy(NoisyArgs na) {
-  extern __shared__ __align__(16) unsigned char smem[];
+// One trajectory (virtual sample v, shot) on `psi` (2^n amplitudes) with
+// marginal scratch `marg` (2^m doubles).
+template <class Team>
+__device__ void run_trajectory(const NoisyArgs& na, double2* psi, double* marg, int64_t v, uint64_t shot,
+                               const Team& tm) {
   const KArgs& a = na.a;
   const DevPlan& p = a.p;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t traj = (int64_t)blockIdx.x * na.warps + w;
-  if (traj >= a.V * na.shots) return;
-  const int64_t v = traj / na.shots;
-  const uint64_t shot = (uint64_t)(traj - v * na.shots);
   const VSample vs = decode_vsample(p, v, a.B);
   const double* xr = a.x + vs.b * a.ldx;
   const int n = na.n;
   const uint32_t N = 1u << n;
-  double2* psi = reinterpret_cast<double2*>(smem + (size_t)w * na.warp_bytes);
-  double* marg = reinterpret_cast<double*>(psi + N);
-  for (uint32_t i = lane; i < N; i += 32) psi[i] = make_double2(i == 0 ? 1.0 : 0.0, 0.0);
-  __syncwarp();
+  for (uint32_t i = tm.tid; i < N; i += Team::T) psi[i] = make_double2(i == 0 ? 1.0 : 0.0, 0.0);
+  tm.sync();
   uint64_t k = 0;  // draws consumed
   int sp = 0;
   for (int oi = 0; oi < na.n_ops; ++oi) {
     const hq_op op = na.ops[oi];
     const double ang = op.slot >= 0 ? eval_slot(p, op.slot, xr, a.theta, vs.shvar, vs.shval) : 0.0;
-    w_apply(psi, n, op.kind, op.q0, op.q1, ang, lane);
+    t_apply(psi, n, op.kind, op.q0, op.q1, ang, tm);
     for (; sp < na.n_sites && na.sites[sp].op == oi; ++sp) {
       const hq_noise_site st = na.sites[sp];
       const double pr = st.param;
@@ -160,9 +185,9 @@ __global__ void k_noisy(NoisyArgs na) {
       const double u = philox_draw(na.seed, shot, k++);
       const int q = st.qubit;
       if (st.channel == HQ_CH_BIT_FLIP) {
-        if (u < pr) w_apply(psi, n, HQ_GATE_X, q, -1, 0.0, lane);
+        if (u < pr) t_apply(psi, n, HQ_GATE_X, q, -1, 0.0, tm);
       } else if (st.channel == HQ_CH_PHASE_FLIP) {
-        if (u < pr) w_apply(psi, n, HQ_GATE_Z, q, -1, 0.0, lane);
+        if (u < pr) t_apply(psi, n, HQ_GATE_Z, q, -1, 0.0, tm);
       } else if (st.channel == HQ_CH_DEPOLARIZING) {
         if (u < 0.75 * pr) {
           // Python float floor division u // (0.25 p) (CPython float_floor_div)
@@ -172,19 +197,19 @@ __global__ void k_noisy(NoisyArgs na) {
           double fl = floor(div);
           if (div - fl > 0.5) fl += 1.0;
           const int which = (int)fl;
-          w_apply(psi, n, which == 0 ? HQ_GATE_X : which == 1 ? HQ_GATE_Y : HQ_GATE_Z, q, -1, 0.0, lane);
+          t_apply(psi, n, which == 0 ? HQ_GATE_X : which == 1 ? HQ_GATE_Y : HQ_GATE_Z, q, -1, 0.0, tm);
         }
       } else {  // amplitude damping (noise.py:112-127)
         double ex = 0.0;
-        for (uint32_t i = lane; i < (N >> 1); i += 32) {
+        for (uint32_t i = tm.tid; i < (N >> 1); i += Team::T) {
           const double2 a1 = psi[ins0(i, q) | (1u << q)];
           ex += a1.x * a1.x + a1.y * a1.y;
         }
-        const double p_jump = pr * warp_sum_d(ex);
+        const double p_jump = pr * tm.sum(ex);
         double norm;
         if (u < p_jump) {
           const double sq = sqrt(pr);
-          for (uint32_t i = lane; i < (N >> 1); i += 32) {
+          for (uint32_t i = tm.tid; i < (N >> 1); i += Team::T) {
             const uint32_t i0 = ins0(i, q), i1 = i0 | (1u << q);
             psi[i0] = make_double2(sq * psi[i1].x, sq * psi[i1].y);
             psi[i1] = make_double2(0.0, 0.0);
@@ -192,41 +217,63 @@ __global__ void k_noisy(NoisyArgs na) {
           norm = sqrt(p_jump);
         } else {
           const double sq = sqrt(1.0 - pr);
-          for (uint32_t i = lane; i < (N >> 1); i += 32) {
+          for (uint32_t i = tm.tid; i < (N >> 1); i += Team::T) {
             const uint32_t i1 = ins0(i, q) | (1u << q);
             psi[i1] = make_double2(sq * psi[i1].x, sq * psi[i1].y);
           }
           norm = sqrt(1.0 - p_jump);
         }
-        __syncwarp();
+        tm.sync();
         if (norm > 0.0) {
-          for (uint32_t i = lane; i < N; i += 32) psi[i] = make_double2(psi[i].x / norm, psi[i].y / norm);
+          for (uint32_t i = tm.tid; i < N; i += Team::T) psi[i] = make_double2(psi[i].x / norm, psi[i].y / norm);
         }
-        __syncwarp();
+        tm.sync();
       }
     }
   }
-  // marginal over the measured qubits: lane owns outcomes j ≡ lane (mod 32),
-  // each summed over the other qubits in increasing amplitude index
+  // marginal over the measured qubits (outcome bit t = measured[t])
   const int m = na.m;
-  const uint32_t nout = 1u << m, nrest = 1u << (n - m);
-  uint32_t mmask = 0;
-  for (int t = 0; t < m; ++t) mmask |= 1u << na.measured[t];
-  for (uint32_t j = lane; j < nout; j += 32) {
-    uint32_t ib = 0;
-    for (int t = 0; t < m; ++t) ib |= ((j >> t) & 1u) << na.measured[t];
-    double s = 0.0;
-    for (uint32_t r = 0; r < nrest; ++r) {
-      uint32_t ir = 0, rr = r;
-      for (int q = 0; q < n && rr; ++q)
-        if (!(mmask >> q & 1u)) { ir |= (rr & 1u) << q; rr >>= 1; }
-      const double2 z = psi[ib | ir];
-      s += z.x * z.x + z.y * z.y;
+  const uint32_t nout = 1u << m;
+  if (nout <= 16) {
+    // every thread: strided partials of all outcomes; then one fixed-order
+    // team reduction per outcome
+    double part[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) part[j] = 0.0;
+    for (uint32_t i = tm.tid; i < N; i += Team::T) {
+      uint32_t o = 0;
+      for (int t = 0; t < m; ++t) o |= ((i >> na.measured[t]) & 1u) << t;
+      const double2 z = psi[i];
+      const double pz = z.x * z.x + z.y * z.y;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j == (int)o) part[j] += pz;
     }
-    marg[j] = s;
+    for (uint32_t j = 0; j < nout; ++j) {
+      const double s = tm.sum(part[j]);
+      if (tm.tid == 0) marg[j] = s;
+    }
+  } else {
+    // thread owns outcomes j ≡ tid (mod T), each summed in increasing index order
+    const uint32_t nrest = 1u << (n - m);
+    uint32_t mmask = 0;
+    for (int t = 0; t < m; ++t) mmask |= 1u << na.measured[t];
+    for (uint32_t j = tm.tid; j < nout; j += Team::T) {
+      uint32_t ib = 0;
+      for (int t = 0; t < m; ++t) ib |= ((j >> t) & 1u) << na.measured[t];
+      double s = 0.0;
+      for (uint32_t r = 0; r < nrest; ++r) {
+        uint32_t ir = 0, rr = r;
+        for (int q = 0; q < n && rr; ++q)
+          if (!(mmask >> q & 1u)) { ir |= (rr & 1u) << q; rr >>= 1; }
+        const double2 z = psi[ib | ir];
+        s += z.x * z.x + z.y * z.y;
+      }
+      marg[j] = s;
+    }
   }
-  __syncwarp();
-  if (lane == 0) {
+  tm.sync();
+  if (tm.tid == 0) {
     const double u = philox_draw(na.seed, shot, k);
     double cum = 0.0;
     uint32_t idx = nout - 1;
@@ -237,6 +284,39 @@ __global__ void k_noisy(NoisyArgs na) {
     atomicAdd(na.sum + v, (unsigned long long)idx);
     if (na.counts && v < a.B) atomicAdd(na.counts + (size_t)v * nout + idx, 1ull);
   }
+}
+
+__global__ void k_noisy(NoisyArgs na) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t traj = (int64_t)blockIdx.x * na.warps + w;
+  if (traj >= na.a.V * na.shots) return;
+  const int64_t v = traj / na.shots;
+  const uint64_t shot = (uint64_t)(traj - v * na.shots);
+  double2* psi = reinterpret_cast<double2*>(smem + (size_t)w * na.warp_bytes);
+  double* marg = reinterpret_cast<double*>(psi + ((size_t)1 << na.n));
+  run_trajectory(na, psi, marg, v, shot, WarpTeam{lane});
+}
+
+// one CTA per trajectory of [traj0, traj0 + gridDim.x); state in global
+// memory (states != nullptr) or in dynamic shared memory
+__global__ void __launch_bounds__(256) k_noisy_block(NoisyArgs na, int64_t traj0, double2* states, double* margs) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double red[8];
+  const int64_t traj = traj0 + blockIdx.x;
+  if (traj >= na.a.V * na.shots) return;
+  const int64_t v = traj / na.shots;
+  const uint64_t shot = (uint64_t)(traj - v * na.shots);
+  double2* psi;
+  double* marg;
+  if (states) {
+    psi = states + (size_t)blockIdx.x * ((size_t)1 << na.n);
+    marg = margs + (size_t)blockIdx.x * ((size_t)1 << na.m);
+  } else {
+    psi = reinterpret_cast<double2*>(smem);
+    marg = reinterpret_cast<double*>(psi + ((size_t)1 << na.n));
+  }
+  run_trajectory(na, psi, marg, v, shot, BlockTeam{(int)threadIdx.x, red});
 }
 
 __global__ void k_noisy_finish(const unsigned long long* sum, int64_t V, int64_t B, int64_t shots, double* out,
@@ -254,11 +334,26 @@ namespace {
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 }
 
+constexpr int kNoisySmemQubits = 13;   // above: one CTA per trajectory, state in global memory
+
+// trajectories resident at once in the global-memory variant: ≤ 1024 CTAs
+// (≈7 per SM) and ≤ 4 GiB of states
+static int64_t noisy_chunk(const hq_plan_s* pl) {
+  const size_t per = ((size_t)16 << pl->n_qubits) + ((size_t)8 << pl->dev.n_measured);
+  const int64_t c = (int64_t)(((size_t)4 << 30) / per);
+  return std::max<int64_t>(1, std::min<int64_t>(c, 1024));
+}
+
 extern "C" size_t hq_noisy_workspace_bytes(hq_plan pl, int64_t batch, int32_t flags, int32_t n_sites) {
   if (!pl || batch < 0) return 0;
   const int64_t V = batch + ((flags & HQ_WANT_JAC) ? batch * 2 * pl->n_tp : 0);
-  return al((size_t)V * 8) + al((size_t)(V - batch) * 8 + 8) + al((size_t)std::max(n_sites, 1) * sizeof(hq_noise_site)) +
-         256;
+  size_t b = al((size_t)V * 8) + al((size_t)(V - batch) * 8 + 8) + al((size_t)std::max(n_sites, 1) * sizeof(hq_noise_site)) +
+             256;
+  if (pl->n_qubits > kNoisySmemQubits) {
+    const int64_t c = noisy_chunk(pl);
+    b += al((size_t)c << (pl->n_qubits + 4)) + al((size_t)c << (pl->dev.n_measured + 3));
+  }
+  return b;
 }
 
 extern "C" hq_status hq_noisy(hq_plan pl, const double* x, int64_t ldx, const double* theta, int64_t batch,
@@ -271,7 +366,7 @@ extern "C" hq_status hq_noisy(hq_plan pl, const double* x, int64_t ldx, const do
   if (shots < 1) return hq::fail_status(HQ_E_CONFIG, "shots must be >= 1");
   if (pl->has_preps) return hq::fail_status(HQ_E_CIRCUIT, "noisy trajectories need gate-level state preparation");
   const int n = pl->n_qubits;
-  if (n > 13) return hq::fail_status(HQ_E_CONFIG, "noisy trajectories support up to 13 qubits");
+  if (n > 26) return hq::fail_status(HQ_E_CONFIG, "noisy trajectories support up to 26 qubits");
   if (pl->n_inputs > 0 && (!x || ldx < pl->n_inputs)) return hq::fail_status(HQ_E_DIMENSION, "input rows too narrow");
   if (pl->n_params > 0 && !theta) return hq::fail_status(HQ_E_DIMENSION, "missing parameters");
   const bool want_jac = (flags & HQ_WANT_JAC) != 0;
@@ -313,18 +408,38 @@ extern "C" hq_status hq_noisy(hq_plan pl, const double* x, int64_t ldx, const do
   if (na.m > 16) return hq::fail_status(HQ_E_CONFIG, "too many measured qubits");
   for (int t = 0; t < na.m; ++t) na.measured[t] = pl->host_measured[t];
   cudaError_t e;
-  na.warp_bytes = ((size_t)16 << n) + ((size_t)8 << na.m);
-  na.warps = (int32_t)std::max<size_t>(1, std::min<size_t>(8, (size_t)(96 * 1024) / na.warp_bytes));
-  const size_t smem = (size_t)na.warps * na.warp_bytes;
   na.sum = sum;
   na.counts = reinterpret_cast<unsigned long long*>(counts);
   if (!keep.empty()) cudaMemcpyAsync(dsites, keep.data(), keep.size() * sizeof(hq_noise_site), cudaMemcpyHostToDevice, st);
   cudaMemsetAsync(sum, 0, (size_t)V * 8, st);
   if (counts) cudaMemsetAsync(counts, 0, ((size_t)batch << na.m) * 8, st);
-  e = cudaFuncSetAttribute(hq::k_noisy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return hq::fail_status(HQ_E_CUDA, cudaGetErrorString(e));
   const int64_t traj = V * shots;
-  hq::k_noisy<<<(unsigned)((traj + na.warps - 1) / na.warps), 32 * na.warps, smem, st>>>(na);
+  if (n > kNoisySmemQubits) {
+    const int64_t c = noisy_chunk(pl);
+    char* sbase = reinterpret_cast<char*>(dsites) + al((size_t)std::max(n_sites, 1) * sizeof(hq_noise_site));
+    auto* states = reinterpret_cast<double2*>(sbase);
+    auto* margs = reinterpret_cast<double*>(sbase + al((size_t)c << (n + 4)));
+    for (int64_t t0 = 0; t0 < traj; t0 += c)
+      hq::k_noisy_block<<<(unsigned)std::min<int64_t>(c, traj - t0), 256, 0, st>>>(na, t0, states, margs);
+  } else if (const size_t tb = ((size_t)16 << n) + ((size_t)8 << na.m);
+             traj <= 148 * (int64_t)std::min<size_t>(8, (size_t)(200 * 1024) / tb)) {
+    // one wave of CTAs holds every trajectory: a whole CTA per trajectory
+    // (8× the lanes on each state) beats a warp per trajectory
+    e = cudaFuncSetAttribute(hq::k_noisy_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb);
+    if (e != cudaSuccess) return hq::fail_status(HQ_E_CUDA, cudaGetErrorString(e));
+    hq::k_noisy_block<<<(unsigned)traj, 256, tb, st>>>(na, 0, nullptr, nullptr);
+  } else {
+    na.warp_bytes = ((size_t)16 << n) + ((size_t)8 << na.m);
+    // few trajectories: spread them over the SMs (fewer warps per CTA)
+    const int64_t spread = std::max<int64_t>(1, (traj + 147) / 148);
+    na.warps = (int32_t)std::max<int64_t>(
+        1, std::min<int64_t>(std::min<int64_t>(8, spread), (int64_t)((size_t)(96 * 1024) / na.warp_bytes)));
+    const size_t smem = (size_t)na.warps * na.warp_bytes;
+    e = cudaFuncSetAttribute(hq::k_noisy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return hq::fail_status(HQ_E_CUDA, cudaGetErrorString(e));
+    hq::k_noisy<<<(unsigned)((traj + na.warps - 1) / na.warps), 32 * na.warps, smem, st>>>(na);
+  }
+
   hq::k_noisy_finish<<<(unsigned)((V + 255) / 256), 256, 0, st>>>(sum, V, batch, shots, out, tp);
   if (want_jac && jac && pl->n_inputs + pl->n_params > 0) {
     const int64_t tot = batch * (pl->n_inputs + pl->n_params);

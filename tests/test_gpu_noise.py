@@ -72,7 +72,7 @@ def test_noise_layer_matches_reference_golden():
     np.testing.assert_allclose(layer.params.grad, g["layer_grad_p"], atol=1e-13)
 
 
-@pytest.mark.parametrize("n", [2, 5, 9])
+@pytest.mark.parametrize("n", [2, 5, 9, 13, 14, 16])
 def test_noisy_random_models_vs_oracle(n):
     rng = np.random.default_rng(n)
     kinds = ["H", "X", "Y", "Z", "RX", "RY", "RZ", "CNOT", "CZ", "CR", "SWAP"]
@@ -88,7 +88,8 @@ def test_noisy_random_models_vs_oracle(n):
             a = float(rng.uniform(-3, 3)) if k in ("RX", "RY", "RZ", "CR") else None
             getattr(c, k.lower())(*tg) if a is None else getattr(c, k.lower())(*tg, a)
             oc.add(O.Op(k, tg, a))
-        meas = [int(q) for q in rng.choice(n, min(n, 2), replace=False)]
+        # up to 6 measured qubits: both marginal paths (≤ 16 outcomes, > 16)
+        meas = [int(q) for q in rng.choice(n, min(n, 2 + 2 * trial), replace=False)]
         c.measure(*meas)
         oc.measure(*meas)
         m, om = N.NoiseModel(), O.NoiseModel()

@@ -14,27 +14,30 @@ def model(mod, ch):
         .add("RX", ch("bit_flip", 0.01)).add("RZ", ch("phase_flip", 0.01))
 
 
-def run(cfg, B, shots, steps=3):
+def run(cfg, B, shots, steps=3, grads=True, oracle_shots=None):
     n, d, P, _, _ = wl.CONFIGS[cfg]
     b = wl.make_builder(cfg, qsim, T)
     x = wl.inputs_for(cfg, B); th = wl.params_for(cfg)
     m = model(N, N.Channel)
-    engine.run_batch_noisy(b, x, th, True, True, m, shots, 0)
+    engine.run_batch_noisy(b, x, th, grads, grads, m, shots, 0)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(steps):
-        e, jac = engine.run_batch_noisy(b, x, th, True, True, m, shots, 0)
+        e, jac = engine.run_batch_noisy(b, x, th, grads, grads, m, shots, 0)
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / steps
-    traj = B * (1 + 2 * (d + P)) * shots
+    rows = (1 + 2 * (d + P)) if grads else 1
+    traj = B * rows * shots
     # oracle: one forward evaluation of one sample on one core
     ob = wl.make_builder(cfg, O, O)
     om = model(O, O.Channel)
+    osh = oracle_shots or shots
     t1 = time.perf_counter()
-    O.noisy_expectation(ob([float(v) for v in x[0]], [float(v) for v in th]), om, shots, 0)
-    one = time.perf_counter() - t1
-    cpu_samples_per_s = 1.0 / (one * (1 + 2 * (d + P)))
-    return {"config": cfg, "n_qubits": n, "batch": B, "shots": shots, "ms_per_step": dt * 1e3,
+    O.noisy_expectation(ob([float(v) for v in x[0]], [float(v) for v in th]), om, osh, 0)
+    one = (time.perf_counter() - t1) * shots / osh
+    cpu_samples_per_s = 1.0 / (one * rows)
+    return {"config": cfg, "n_qubits": n, "batch": B, "shots": shots, "gradients": grads,
+            "ms_per_step": dt * 1e3,
             "samples_per_s": B / dt, "trajectories_per_s": traj / dt,
             "oracle_1core_samples_per_s": cpu_samples_per_s, "speedup_vs_1core_port": B / dt / cpu_samples_per_s}
 
@@ -42,3 +45,6 @@ def run(cfg, B, shots, steps=3):
 if __name__ == "__main__":
     for cfg, B, shots in (("cfg1", 64, 100), ("cfg2", 64, 100)):
         print(json.dumps(run(cfg, B, shots)), flush=True)
+    # global-memory trajectory kernel (n > 13): forward values only
+    print(json.dumps(run("cfg3", 16, 20, grads=False)), flush=True)
+    print(json.dumps(run("cfg4", 4, 10, steps=1, grads=False, oracle_shots=1)), flush=True)
