@@ -14,7 +14,8 @@ One JSON line on rank 0.  `value` is device-timed (CUDA events, inputs resident
 in HBM, max over ranks); `e2e` goes through the public QuantumLayer API with
 host tensors (H2D of inputs, D2H of outputs and gradients inside the timed
 region); `roofline` uses the amplitude-update kernel's live CUDA-event time;
-`cpu_baseline` times the NumPy oracle port of the reference on a bounded sample.
+`cpu_baseline` times the NumPy oracle port of the reference on a bounded sample;
+`complex128` repeats the device-timed step at the reference's own precision.
 """
 
 from __future__ import annotations
@@ -49,6 +50,7 @@ def parse():
     ap.add_argument("--precision", default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c128", action="store_true", help="skip the complex128 companion measurement")
     ap.add_argument("--backend", default="nccl", help="process-group backend (gloo: dry runs of the "
                     "multi-rank path with several ranks on one device)")
     return ap.parse_args()
@@ -371,6 +373,47 @@ def run_ours(a):
                        "steps": k, "h2d_bytes_per_step": int(x.nbytes + theta.nbytes + B * 8),
                        "d2h_bytes_per_step": int(B * 8 + theta.nbytes + (x.nbytes if want_x else 0)),
                        "api": "QuantumLayer.forward + hyqnet-style backward (host numpy tensors)"}
+
+    # the same workload at the reference's own precision (complex128),
+    # device-timed like `value` (companion number; `value` stays the plan's)
+    if prec == "c64" and not a.no_c128:
+        del plan
+        torch.cuda.empty_cache()
+        p128 = engine.Plan(tape, d, P, "c128", grad)
+
+        def step128():
+            out, jac = p128.forward(xd, td, True)
+            gx, gt = p128.vjp(jac, up, want_x, True)
+            if world > 1:
+                dist.all_reduce(gt)
+            return gt
+
+        step128()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        k = max(2, min(a.steps, 4))
+        ev0.record()
+        for _ in range(k):
+            step128()
+        ev1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([ev0.elapsed_time(ev1) / k], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        v128 = world * B / (float(t.item()) / 1e3)
+        R, D, _ = wl.gate_counts(cfg)
+        f_unit = (1 << n) * (18 * R + 8 * D + 6)
+        f64peak, f64kind = fp_peak("c128")
+        line["complex128"] = {"value": v128, "unit": UNIT,
+                              "ms_per_step": float(t.item()), "steps": k, "dtype": "f64",
+                              "fp64": {"flops_per_unit": f_unit, "achieved_TFLOPs": f_unit * v128 / world / 1e12,
+                                       "peak_TFLOPs": f64peak, "peak_source": f64kind,
+                                       "frac": f_unit * v128 / world / 1e12 / f64peak},
+                              "note": "same workload, complex128 amplitudes (the reference's precision)",
+                              "plan": p128.description}
+        del p128
+        torch.cuda.empty_cache()
 
     if rank == 0 and world == 1 and not a.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, x[0], theta)
