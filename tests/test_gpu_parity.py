@@ -301,7 +301,7 @@ def test_no_grad_skips_jacobian():
     assert "adjoint_slots=0" in layer.last_info["plan"].description
 
 
-def test_cfg4_full_size_norm_and_round_trip():
+def test_cfg4_full_size_norm():
     """Size-independent properties at the bench's full circuit (n = 20)."""
     b = wl.make_builder("cfg4", qsim, T)
     x = wl.inputs_for("cfg4", 2)
@@ -313,6 +313,47 @@ def test_cfg4_full_size_norm_and_round_trip():
         st = plan.state(torch.tensor(x, device="cuda"), torch.tensor(th, device="cuda"))
         z = st[..., 0].double() ** 2 + st[..., 1].double() ** 2
         np.testing.assert_allclose(z.sum(dim=1).cpu().numpy(), 1.0, atol=tol)
+
+
+def test_cfg5_size_32_qubit_invariants():
+    """cfg5 (n = 32, a 64 GiB complex128 state) is beyond the
+    reference's reach, so it is pinned by invariants at full size: the cfg5
+    layer structure U followed by U† returns |0…0⟩ exactly enough that X on
+    three qubits reads back E = 7, and a product state matches its closed form."""
+    import torch
+    rng = np.random.default_rng(32)
+    n = 32
+    u = Circuit(n)
+    for _ in range(4):                      # cfg5's layer: RY RZ per qubit, CNOT chain
+        for q in range(n):
+            u.ry(q, float(rng.uniform(0, 2 * np.pi)))
+            u.rz(q, float(rng.uniform(0, 2 * np.pi)))
+        for q in range(n - 1):
+            u.cnot(q, q + 1)
+    rt = Circuit(n)
+    for op in u.ops:
+        rt.add(op)
+    for op in reversed(u.ops):
+        if op.kind == "CNOT":
+            rt.cnot(*op.targets)
+        else:
+            getattr(rt, op.kind.lower())(op.targets[0], -op.angle)
+    for q in (3, 17, 31):
+        rt.x(q)
+    rt.measure(3, 17, 31)
+    th = rng.uniform(0, 2 * np.pi, n)
+    prod = Circuit(n)
+    for q in range(n):
+        prod.ry(q, float(th[q]))
+    prod.measure(0, 5, 31)
+    try:
+        e = engine.evaluate_circuits([rt], "c128")[0]
+        assert abs(e - 7.0) < 1e-9
+        e = engine.evaluate_circuits([prod], "c128")[0]
+        want = sum(w * math.sin(th[q] / 2) ** 2 for w, q in ((1, 0), (2, 5), (4, 31)))
+        assert abs(e - want) < 1e-12
+    finally:
+        torch.cuda.empty_cache()
 
 
 def test_layer_builds_output_in_the_inputs_graph_module():
