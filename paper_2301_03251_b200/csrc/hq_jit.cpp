@@ -155,6 +155,98 @@ struct Gen {
     }
   }
 
+  // Deferred register RZ phases: an RZ on a register bit only records its
+  // angle on the variables holding the |1> half (vph[var]: slot ->
+  // multiplicity); renamings carry the records along.  A non-diagonal gate on
+  // bit k first needs equal records on each of its pairs (then the common
+  // phase commutes with it; derivative dots see the same phase on ψ and λ and
+  // are unchanged), otherwise every record is flushed at once: one complex
+  // multiply per variable by a precomputed product e^{iΣ kθ} (ptab, per CTA in
+  // shared memory) instead of one per RZ.
+  bool defer = false;
+  std::vector<std::map<int, int>> vph;
+  std::vector<std::map<int, int>> ptab;
+  std::map<std::map<int, int>, int> ptab_ix;
+  int ptab_find(const std::map<int, int>& m) {
+    auto it = ptab_ix.find(m);
+    if (it != ptab_ix.end()) return it->second;
+    const int k = (int)ptab.size();
+    ptab.push_back(m);
+    ptab_ix[m] = k;
+    return k;
+  }
+  void vph_reset() { vph.assign(N, {}); }
+  bool vph_pairs_equal(int k) const {
+    for (int i = 0; i < N; ++i)
+      if (!(i >> k & 1) && vph[map[i]] != vph[map[i | 1 << k]]) return false;
+    return true;
+  }
+  void flush_vph(bool both) {
+    if (!defer) return;
+    for (int v = 0; v < N; ++v) {
+      flush_one(v, vph[v], both);
+      vph[v].clear();
+    }
+  }
+  void flush_one(int v, const std::map<int, int>& m, bool both) {
+    if (m.empty()) return;
+    const int k = ptab_find(m);
+    o << "{ const C ph_ = ptab_[" << k << "];\n";
+    cmul_amp("p" + std::to_string(v), "ph_.x", "ph_.y");
+    if (both) cmul_amp("l" + std::to_string(v), "ph_.x", "ph_.y");
+    o << "}\n";
+  }
+  // equalise the records on the pairs of bit k: each member flushes only the
+  // terms it does not share with its partner (at most one RZ's worth of work
+  // when a single RZ on bit k is pending); the shared rest stays deferred
+  void flush_pairs(int k, bool both) {
+    for (int i = 0; i < N; ++i) {
+      if (i >> k & 1) continue;
+      const int A = map[i], B = map[i | 1 << k];
+      if (vph[A] == vph[B]) continue;
+      std::map<int, int> com, ea, eb;
+      for (const auto& kv : vph[A]) {
+        auto it = vph[B].find(kv.first);
+        if (it != vph[B].end() && it->second == kv.second) com.insert(kv);
+        else ea.insert(kv);
+      }
+      for (const auto& kv : vph[B])
+        if (!com.count(kv.first)) eb.insert(kv);
+      flush_one(A, ea, both);
+      flush_one(B, eb, both);
+      vph[A] = com;
+      vph[B] = com;
+    }
+  }
+  // before op's derivative dot and its application: equalise the pending
+  // records on the pairs it mixes (runtime-controlled CNOT targets included)
+  void prepare(const WOp& op, bool both) {
+    if (!defer) return;
+    int k = -1;
+    switch (op.kind) {
+      case HQ_GATE_H: case HQ_GATE_Y: case HQ_GATE_RX: case HQ_GATE_RY: k = op.a; break;
+      case HQ_GATE_CNOT: if (!is_reg(op.a)) k = op.b; break;
+      default: break;
+    }
+    if (k < 0 || !is_reg(k) || vph_pairs_equal(k)) return;
+    // partial flush (only the unshared terms of bit k's pairs) when it is
+    // clearly cheaper than flushing every record now
+    int part = 0, full = 0;
+    for (int v = 0; v < N; ++v) full += !vph[v].empty();
+    for (int i = 0; i < N; ++i) {
+      if (i >> k & 1) continue;
+      const auto &A = vph[map[i]], &B = vph[map[i | 1 << k]];
+      if (A == B) continue;
+      bool ea = false, eb = false;
+      for (const auto& kv : A) { auto it = B.find(kv.first); if (it == B.end() || it->second != kv.second) ea = true; }
+      for (const auto& kv : B) { auto it = A.find(kv.first); if (it == A.end() || it->second != kv.second) eb = true; }
+      part += ea + eb;
+    }
+    static const int pf = std::getenv("HQ_DEFER_PARTIAL") ? std::atoi(std::getenv("HQ_DEFER_PARTIAL")) : 2;
+    if (pf > 0 && part * pf <= full) flush_pairs(k, both);
+    else flush_vph(both);
+  }
+
   std::string R() const { return c64 ? "float" : "double"; }
   std::string P(int i) const { return "p" + std::to_string(map[i]); }
   std::string L(int i) const { return "l" + std::to_string(map[i]); }
@@ -203,6 +295,7 @@ struct Gen {
 
   // one gate on the named register set(s); inv = apply the inverse
   void apply(const WOp& op, bool inv, bool both) {
+    prepare(op, both);
     const int a = op.a, b = op.b;
     const char* sg = inv ? "-" : "";
     auto sets = [&](auto fn) { fn(false); if (both) fn(true); };
@@ -303,7 +396,13 @@ struct Gen {
           }
         } else {
           // global phase dropped: |1> half times e^{iφ}
-          if (is_reg(a)) {
+          if (is_reg(a) && defer) {
+            for (int i = 0; i < N; ++i)
+              if (i >> a & 1) {
+                auto& m = vph[map[i]];
+                if ((m[op.slot] += inv ? -1 : 1) == 0) m.erase(op.slot);
+              }
+          } else if (is_reg(a)) {
             o << "{ const R c_ = " << trig(op.slot, 2) << ", s_ = " << sg << trig(op.slot, 3) << ";\n";
             sets([&](bool lam) {
               for (int i = 0; i < N; ++i)
@@ -683,6 +782,12 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   g.c64 = c64;
   g.packed = c64 && !std::getenv("HQ_NO_F32X2");
   g.exact = false;  // hq_state corrects the dropped RZ phases / rotation signs in the last pass
+  {
+    const char* e = std::getenv("HQ_DEFER_RZ");
+    g.defer = !(e && e[0] == '0');
+  }
+  g.map.assign(g.N, 0);
+  g.vph_reset();
   const int tbits = g.Q - g.RB;
   const int n = pl->n_qubits;
   const int np = (int)pl->passes.size();
@@ -767,6 +872,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   auto identity_map = [&]() {
     g.map.assign(g.N, 0);
     for (int i = 0; i < g.N; ++i) g.map[i] = i;
+    g.vph_reset();
   };
   auto hi_off = [&](int i) { return goff((uint32_t)(i * g.T)); };
 
@@ -817,7 +923,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   if (fwd && last)
     o << "if (tid < Q) { double w = 0.0; for (int i = 0; i < p.n_measured; ++i) if (p.measured[i] == ps.local[tid]) "
          "w = (double)(1ull << i); wt[tid] = w; }\n";
-  o << "__syncthreads();\n";
+  o << "__syncthreads();\n/*HQ_PTAB_BUILD*/\n";
   if (fwd && first) o << "if (p.n_preps > 0) prep_norms(a, sval, inv, tid);\n__syncthreads();\n";
   if (fwd && first && pl->fold) {
     // tile index j = tid + k·T: thread-bit factor per thread, high-bit factors in a table
@@ -891,6 +997,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     for (; i < ks.size(); ++i) {
       const int k = ks[i];
       const WOp& op = P.wops[k];
+      g.prepare(op, adj);
       if (adj) {
         if (!(ablate & 4)) g.dot(op, L.per_thread, L.group, nw, reg_acc);
         if (first && !fold_end && k == stop_op && op.dl >= 0) continue;
@@ -898,6 +1005,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       const bool uni = op.kind == HQ_GATE_CNOT && !Gen::is_reg(op.a) && (op.a >= 64 || op.a - 16 >= 5);
       if (budget > 0 && uni) {
         const std::vector<int> map0 = g.map, bq0 = g.bq;
+        const auto vph0 = g.vph;
         const bool pend0 = g.pending, na0 = na, decl0 = g.ph_decl;
         if (op.a < 64) na = true;
         WOp x{};
@@ -911,12 +1019,14 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         emit_steps(ks, i + 1, adj, tail, budget - 1);
         o << "} else {\n";
         g.map = map0;
+        g.vph = vph0;
         g.bq = bq0;
         g.pending = pend0;
         g.ph_decl = decl0;
         emit_steps(ks, i + 1, adj, tail, budget - 1);
         o << "}\n";
         g.map = map0;
+        g.vph = vph0;
         g.bq.clear();
         g.pending = pend0;
         g.ph_decl = decl0;
@@ -926,6 +1036,34 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       if (!(adj && (ablate & 2))) g.apply(op, adj, adj);
     }
     tail();
+  };
+
+  // Deferred RZs gather before the next non-diagonal gate on their qubit when
+  // hoisted over the gates they commute with (in the backward's reversed
+  // order RZ⁻¹(q) directly precedes RY⁻¹(q); hoisting lines up a layer's RZs
+  // so one flush serves them all).  Reordering commuting gates changes neither
+  // the state nor any derivative dot.
+  auto commutes_rz = [](const WOp& z, const WOp& o2) {
+    switch (o2.kind) {
+      case HQ_GATE_Z: case HQ_GATE_RZ: case HQ_GATE_CZ: case HQ_GATE_CR: return true;
+      case HQ_GATE_H: case HQ_GATE_X: case HQ_GATE_Y: case HQ_GATE_RX: case HQ_GATE_RY: return o2.a != z.a;
+      case HQ_GATE_CNOT: return o2.b != z.a;
+      case HQ_GATE_SWAP: return o2.a != z.a && o2.b != z.a;
+      default: return false;
+    }
+  };
+  auto hoist = [&](std::vector<int>& ks) {
+    if (!g.defer) return;
+    if (first && !fold_end && std::find(ks.begin(), ks.end(), stop_op) != ks.end()) return;
+    for (size_t i = 1; i < ks.size(); ++i) {
+      const WOp& z = P.wops[ks[i]];
+      if (z.kind != HQ_GATE_RZ || !Gen::is_reg(z.a)) continue;
+      for (size_t j = i; j > 0; --j) {
+        const WOp& prev = P.wops[ks[j - 1]];
+        if (prev.kind == HQ_GATE_RZ || !commutes_rz(z, prev)) break;
+        std::swap(ks[j], ks[j - 1]);
+      }
+    }
   };
 
   // ---- tile loop
@@ -983,17 +1121,19 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       g.pending = false;
       std::vector<int> ks;
       for (int k = W.op0; k < W.op1; ++k) ks.push_back(k);
+      hoist(ks);
       if (w < nwin - 1) {
-        emit_steps(ks, 0, false, [&] { g.flush_pending(false); sync(); g.store_regs(W, "p", "tp"); sync(); }, ubudget);
+        emit_steps(ks, 0, false, [&] { g.flush_vph(false); g.flush_pending(false); sync(); g.store_regs(W, "p", "tp"); sync(); }, ubudget);
         o << "}\n";
       } else if (fused) {
         for (int k : ks) g.apply(P.wops[k], false, false);
+        g.flush_vph(false);
         g.flush_pending(false);
       } else if (last || !direct_ok(W)) {
-        emit_steps(ks, 0, false, [&] { g.flush_pending(false); sync(); g.store_regs(W, "p", "tp"); sync(); }, ubudget);
+        emit_steps(ks, 0, false, [&] { g.flush_vph(false); g.flush_pending(false); sync(); g.store_regs(W, "p", "tp"); sync(); }, ubudget);
         o << "}\n";
       } else {
-        emit_steps(ks, 0, false, [&] { g.flush_pending(false); direct_store(W, false); }, ubudget);
+        emit_steps(ks, 0, false, [&] { g.flush_vph(false); g.flush_pending(false); direct_store(W, false); }, ubudget);
         o << "}\n";
       }
     }
@@ -1107,10 +1247,12 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       const int lo = std::max<int>(W.op0, first ? stop_op : 0);
       std::vector<int> ks;
       for (int k = W.op1 - 1; k >= lo; --k) ks.push_back(k);
+      hoist(ks);
       const bool end = first ? (wi == nwin - 1 || w == stop_win) : (w == 0);
       if (end) {
         emit_steps(ks, 0, true, [&] {
           g.flush_batch();
+          g.flush_vph(true);
           g.flush_pending(true);
           if (fold_end) {
             // λ at the circuit start (all first-pass gates un-applied), contracted
@@ -1214,6 +1356,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       }
       emit_steps(ks, 0, true, [&] {
         g.flush_batch();
+        g.flush_vph(true);
         g.flush_pending(true);
         if (ablate & 1) return;
         sync();
@@ -1240,7 +1383,38 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       << "if (lane_ == 0) a.dpart[((int64_t)v * p.n_adj + ps.dlist[i]) * a.n_parts + chunk] = s; } }\n";
   }
   o << "}\n";
-  return o.str();
+  std::string body = o.str();
+  std::string decl, build;
+  if (!g.ptab.empty()) {
+    const std::string nm = std::string(fused ? "hq_fb" : (bwd ? "hq_b" : "hq_f")) + std::to_string(pi);
+    std::ostringstream d, b;
+    std::vector<int> off{0}, sl, mu;
+    for (const auto& m : g.ptab) {
+      for (const auto& kv : m) { sl.push_back(kv.first); mu.push_back(kv.second); }
+      off.push_back((int)sl.size());
+    }
+    auto arr = [&](const char* ty, const char* tag, const std::vector<int>& v) {
+      d << "__device__ const " << ty << " " << nm << tag << "[" << v.size() << "] = {";
+      for (size_t i = 0; i < v.size(); ++i) d << (i ? "," : "") << v[i];
+      d << "};\n";
+    };
+    arr("short", "_pto", off);
+    arr("short", "_pts", sl);
+    arr("signed char", "_ptk", mu);
+    decl = d.str();
+    const int K = (int)g.ptab.size();
+    b << "__shared__ C ptab_[" << K << "];\n"
+      << "for (int j_ = tid; j_ < " << K << "; j_ += T) { R x_ = (R)1, y_ = (R)0;\n"
+      << "  for (int m_ = " << nm << "_pto[j_]; m_ < " << nm << "_pto[j_ + 1]; ++m_) { const int s_ = " << nm
+      << "_pts[m_], k_ = " << nm << "_ptk[m_]; const R c_ = trig[8 * s_ + 2], sn_ = k_ < 0 ? -trig[8 * s_ + 3] : "
+         "trig[8 * s_ + 3];\n"
+      << "    for (int r_ = 0; r_ < (k_ < 0 ? -k_ : k_); ++r_) { const R t_ = x_ * c_ - y_ * sn_; y_ = x_ * sn_ + y_ * c_; "
+         "x_ = t_; } }\n"
+      << "  ptab_[j_].x = x_; ptab_[j_].y = y_; }\n__syncthreads();\n";
+    build = b.str();
+  }
+  body.replace(body.find("/*HQ_PTAB_BUILD*/"), std::strlen("/*HQ_PTAB_BUILD*/"), build);
+  return decl + body;
 }
 
 // One thread per (virtual) sample for the smallest circuits (n ≤ 4): the

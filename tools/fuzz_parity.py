@@ -31,8 +31,8 @@ def builder_for(n, depth, rng):
     return b
 
 
-def main(count=40):
-    rng = np.random.default_rng(2024)
+def main(count=40, seed=2024):
+    rng = np.random.default_rng(seed)
     worst = {"c64": 0.0, "c128": 0.0}
     for t in range(count):
         n = int(rng.integers(9, 16))
@@ -63,8 +63,8 @@ def main(count=40):
             lim = 1e-10 if prec == "c128" else 1e-4
             if err > lim:
                 print("MISMATCH", t, n, tile, prec, err, info["plan"].description[:200], flush=True)
-    print("worst", worst, flush=True)
+    print("worst", worst, "circuits", count, "seed", seed, flush=True)
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]) if len(sys.argv) > 1 else 40)
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 40, int(sys.argv[2]) if len(sys.argv) > 2 else 2024)
