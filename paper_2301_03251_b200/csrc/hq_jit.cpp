@@ -242,7 +242,7 @@ struct Gen {
       for (const auto& kv : B) { auto it = A.find(kv.first); if (it == A.end() || it->second != kv.second) eb = true; }
       part += ea + eb;
     }
-    static const int pf = std::getenv("HQ_DEFER_PARTIAL") ? std::atoi(std::getenv("HQ_DEFER_PARTIAL")) : 2;
+    const int pf = std::getenv("HQ_DEFER_PARTIAL") ? std::atoi(std::getenv("HQ_DEFER_PARTIAL")) : 2;
     if (pf > 0 && part * pf <= full) flush_pairs(k, both);
     else flush_vph(both);
   }

@@ -626,3 +626,60 @@ def test_light_cone_layer_keyword():
     assert outs[1][2].startswith("n=10 ") and outs[0][2].startswith("n=20 ")
     np.testing.assert_allclose(outs[1][0], outs[0][0], atol=1e-12)
     np.testing.assert_allclose(outs[1][1], outs[0][1], atol=1e-11)
+
+
+def _hea_rz_builder(n, layers, seed):
+    """Layers of per-gate-parameter RY/RZ, CNOT chains, a few CZ/CR/X/SWAP
+    (commutation barriers for the RZ hoisting), inputs on the first layer."""
+    rng = np.random.default_rng(seed)
+    extra = [(int(rng.integers(4)), tuple(int(q) for q in rng.choice(n, 2, replace=False))) for _ in range(layers)]
+    P = 2 * n * layers + layers
+
+    def b(inputs, params, Circ=Circuit):
+        c = Circ(n)
+        k = 0
+        for L in range(layers):
+            for q in range(n):
+                c.ry(q, params[k] + (inputs[q % 2] if L == 0 else 0.0))
+                c.rz(q, params[k + 1])
+                k += 2
+            for q in range(n - 1):
+                c.cnot(q, q + 1)
+            kind, (a, b2) = extra[L]
+            if kind == 0:
+                c.cz(a, b2)
+            elif kind == 1:
+                c.cr(a, b2, params[k])
+            elif kind == 2:
+                c.x(a)
+            else:
+                c.swap(a, b2)
+            k += 1
+        c.measure(0, n - 1)
+        return c
+    return b, P
+
+
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("mode", ["defer", "partial", "off"])
+def test_deferred_rz_phases_vs_oracle(prec, mode, monkeypatch):
+    """Deferred register RZ phases (hoisted, combined flushes; the partial
+    flush variant; and switched off) against the oracle, values and every
+    parameter's gradient."""
+    monkeypatch.setenv("HQ_FORCE_STREAM", "1")
+    monkeypatch.setenv("HQ_TILE_BITS", "10")
+    if mode == "off":
+        monkeypatch.setenv("HQ_DEFER_RZ", "0")
+    if mode == "partial":
+        monkeypatch.setenv("HQ_DEFER_PARTIAL", "1")
+    b, P = _hea_rz_builder(13, 4, seed=5)
+    rng = np.random.default_rng(55)
+    x = rng.uniform(-3, 3, (3, 2))
+    th = rng.uniform(0, 6, P)
+    res, jac, info = engine.run_batch(b, x, th, True, True, prec, cache=engine.PlanCache(2))
+    assert "path=stream" in info["plan"].description
+    out, jx, jp, _, _ = O.layer(lambda i, p: b(i, p, Circ=O.Circuit), x, th)
+    check_vals(res, out, prec)
+    j = jac.cpu().numpy()
+    check_vals(j[:, :2], jx, prec, grad=True)
+    check_vals(j[:, 2:], jp, prec, grad=True)
