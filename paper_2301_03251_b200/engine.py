@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _native as nat
 from . import tracer as tr
-from .errors import CircuitError, ConfigError, EncodingError, NativeError
+from .errors import CircuitError, ConfigError, DimensionError, EncodingError, NativeError
 
 _PREC = {"c64": nat.HQ_C64, "c128": nat.HQ_C128, "complex64": nat.HQ_C64,
          "complex128": nat.HQ_C128}
@@ -360,6 +360,26 @@ def final_states(circuits, precision: str = "c128", init=None) -> list:
         for k, (idx, _) in enumerate(rows):
             res[idx] = s[k, :, 0] + 1j * s[k, :, 1]
     return res
+
+
+def final_state_device(circuit, init=None, precision: str = "c128"):
+    """Device-resident final amplitudes of one concrete circuit: ``init`` a
+    complex128 CUDA vector [2^n] (or None for |0…0⟩) -> complex128 CUDA [2^n].
+    No host round trip (the amplitude-sharded executor's local segments)."""
+    torch = _torch()
+    (tape, rows), = _circuit_rows([circuit]).values()
+    A = len(tape.slot_const)
+    plan = _global_cache.get(tape, A, 0, precision, None, math.pi / 2, 0.5)
+    dev = init.device if init is not None else torch.device(f"cuda:{plan.device}")
+    x = (torch.tensor([rows[0][1]], dtype=torch.float64, device=dev) if A
+         else torch.zeros((1, 1), dtype=torch.float64, device=dev))
+    pt = torch.zeros(1, dtype=torch.float64, device=dev)
+    it = None
+    if init is not None:
+        if init.dtype != torch.complex128 or init.numel() != (1 << tape.n_qubits):
+            raise DimensionError("init must be a complex128 vector of 2^n amplitudes")
+        it = torch.view_as_real(init.contiguous()).reshape(1, -1, 2)
+    return torch.view_as_complex(plan.state(x, pt, it)[0])
 
 
 def simulate_circuit(circuit, init=None, precision: str = "c128") -> np.ndarray:

@@ -231,6 +231,21 @@ def gpu_apply_local(L, precision="c128"):
     return apply_local
 
 
+def gpu_apply_local_dev(L, precision="c128"):
+    """Device-resident local executor for ``run_nccl``: the rank's complex128
+    CUDA shard goes through the plan as its initial state and the result stays
+    on the device (plans are cached per local-segment structure)."""
+    from . import engine
+
+    def apply_local_dev(shard, ops):
+        from .qsim import Circuit, GateOp
+        c = Circuit(L)
+        for kind, t, a in ops:
+            c.add(GateOp(kind, t, a))
+        return engine.final_state_device(c, shard, precision)
+    return apply_local_dev
+
+
 def _pack_half(shard, l, bit):
     """Elements of a device shard whose local bit l == bit, in index order."""
     import torch
