@@ -164,6 +164,9 @@ struct Gen {
   // multiply per variable by a precomputed product e^{iΣ kθ} (ptab, per CTA in
   // shared memory) instead of one per RZ.
   bool defer = false;
+  // phase-table cap (shared memory: ≤ ~16 KB complex128); past it new RZs
+  // apply immediately (they commute with the pending records)
+  static constexpr size_t kMaxPtab = 1024;
   std::vector<std::map<int, int>> vph;
   std::vector<std::map<int, int>> ptab;
   std::map<std::map<int, int>, int> ptab_ix;
@@ -396,7 +399,7 @@ struct Gen {
           }
         } else {
           // global phase dropped: |1> half times e^{iφ}
-          if (is_reg(a) && defer) {
+          if (is_reg(a) && defer && ptab.size() < kMaxPtab) {
             for (int i = 0; i < N; ++i)
               if (i >> a & 1) {
                 auto& m = vph[map[i]];
