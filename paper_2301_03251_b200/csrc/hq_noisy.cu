@@ -9,9 +9,11 @@
 // counter k/4 + 1); the final outcome consumes one more draw:
 // searchsorted(cumsum(marginal), u, side="right") clamped (qsim.py:227-229).
 // E = Σ outcome / shots with an exact integer sum (qnn.py:27-32).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -88,6 +90,31 @@ struct BlockTeam {
     double s = 0.0;
     for (int w = 0; w < T / 32; ++w) s += red[w];
     __syncthreads();
+    return s;
+  }
+};
+
+// A cluster of kClusterCtas CTAs on one trajectory (large n, few
+// trajectories): the state in global memory, barrier.cluster between gates
+// (release/acquire at cluster scope covers the global-memory state), sums
+// through distributed shared memory in a fixed order.
+constexpr int kClusterCtas = 8;
+struct ClusterTeam {
+  int tid;      // cluster rank * 256 + threadIdx.x
+  double* red;  // [8] shared, per CTA
+  static constexpr int T = 256 * kClusterCtas;
+  __device__ void sync() const { cooperative_groups::this_cluster().sync(); }
+  __device__ double sum(double v) const {
+    auto cl = cooperative_groups::this_cluster();
+    v = warp_sum_d(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    cl.sync();
+    double s = 0.0;
+    for (int r = 0; r < kClusterCtas; ++r) {
+      const double* rr = cl.map_shared_rank(red, r);
+      for (int w = 0; w < 8; ++w) s += rr[w];
+    }
+    cl.sync();
     return s;
   }
 };
@@ -298,6 +325,21 @@ __global__ void k_noisy(NoisyArgs na) {
   run_trajectory(na, psi, marg, v, shot, WarpTeam{lane});
 }
 
+// one cluster per trajectory of [traj0, traj0 + gridDim.x / kClusterCtas)
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(256)
+    k_noisy_cluster(NoisyArgs na, int64_t traj0, double2* states, double* margs) {
+  __shared__ double red[8];
+  const int64_t c = blockIdx.x / kClusterCtas;
+  const int64_t traj = traj0 + c;
+  if (traj >= na.a.V * na.shots) return;   // whole cluster: c is uniform in it
+  const int64_t v = traj / na.shots;
+  const uint64_t shot = (uint64_t)(traj - v * na.shots);
+  double2* psi = states + (size_t)c * ((size_t)1 << na.n);
+  double* marg = margs + (size_t)c * ((size_t)1 << na.m);
+  const int rank = (int)cooperative_groups::this_cluster().block_rank();
+  run_trajectory(na, psi, marg, v, shot, ClusterTeam{rank * 256 + (int)threadIdx.x, red});
+}
+
 // one CTA per trajectory of [traj0, traj0 + gridDim.x); state in global
 // memory (states != nullptr) or in dynamic shared memory
 __global__ void __launch_bounds__(256) k_noisy_block(NoisyArgs na, int64_t traj0, double2* states, double* margs) {
@@ -419,8 +461,15 @@ extern "C" hq_status hq_noisy(hq_plan pl, const double* x, int64_t ldx, const do
     char* sbase = reinterpret_cast<char*>(dsites) + al((size_t)std::max(n_sites, 1) * sizeof(hq_noise_site));
     auto* states = reinterpret_cast<double2*>(sbase);
     auto* margs = reinterpret_cast<double*>(sbase + al((size_t)c << (n + 4)));
-    for (int64_t t0 = 0; t0 < traj; t0 += c)
-      hq::k_noisy_block<<<(unsigned)std::min<int64_t>(c, traj - t0), 256, 0, st>>>(na, t0, states, margs);
+    if (traj * hq::kClusterCtas <= 2 * 148 * 8 && !std::getenv("HQ_NOISY_NO_CLUSTER")) {
+      // few trajectories: a cluster of CTAs per trajectory spreads them over the SMs
+      for (int64_t t0 = 0; t0 < traj; t0 += c)
+        hq::k_noisy_cluster<<<(unsigned)(std::min<int64_t>(c, traj - t0) * hq::kClusterCtas), 256, 0, st>>>(
+            na, t0, states, margs);
+    } else {
+      for (int64_t t0 = 0; t0 < traj; t0 += c)
+        hq::k_noisy_block<<<(unsigned)std::min<int64_t>(c, traj - t0), 256, 0, st>>>(na, t0, states, margs);
+    }
   } else if (const size_t tb = ((size_t)16 << n) + ((size_t)8 << na.m);
              traj <= 148 * (int64_t)std::min<size_t>(8, (size_t)(200 * 1024) / tb)) {
     // one wave of CTAs holds every trajectory: a whole CTA per trajectory

@@ -74,6 +74,18 @@ def test_noise_layer_matches_reference_golden():
 
 @pytest.mark.parametrize("n", [2, 5, 9, 13, 14, 16])
 def test_noisy_random_models_vs_oracle(n):
+    _random_models_vs_oracle(n)
+
+
+@pytest.mark.parametrize("n", [14, 15])
+def test_noisy_global_state_kernels_vs_oracle(n, monkeypatch):
+    """n > 13 with few trajectories runs a CTA cluster per trajectory; the
+    CTA-per-trajectory kernel (many trajectories) is forced here."""
+    monkeypatch.setenv("HQ_NOISY_NO_CLUSTER", "1")
+    _random_models_vs_oracle(n)
+
+
+def _random_models_vs_oracle(n):
     rng = np.random.default_rng(n)
     kinds = ["H", "X", "Y", "Z", "RX", "RY", "RZ", "CNOT", "CZ", "CR", "SWAP"]
     chans = ["bit_flip", "phase_flip", "depolarizing", "amplitude_damping"]
