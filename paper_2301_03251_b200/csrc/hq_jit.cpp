@@ -446,7 +446,19 @@ struct Gen {
         }
         const std::string px = op.kind == HQ_GATE_CZ ? "(R)-1" : trig(op.slot, 2);
         const std::string py = op.kind == HQ_GATE_CZ ? "(R)0" : std::string(sg) + trig(op.slot, 3);
-        if (cnd.empty()) {
+        if (cnd.empty() && defer && ptab.size() < kMaxPtab) {
+          // deferred like RZ; CZ's -1 is the pseudo-slot -1 (multiplicity mod 2)
+          for (int i = 0; i < N; ++i)
+            if ((i & M) == M) {
+              auto& m = vph[map[i]];
+              if (op.kind == HQ_GATE_CZ) {
+                if (m.count(-1)) m.erase(-1);
+                else m[-1] = 1;
+              } else if ((m[op.slot] += inv ? -1 : 1) == 0) {
+                m.erase(op.slot);
+              }
+            }
+        } else if (cnd.empty()) {
           o << "{ const R x_ = " << px << ", y_ = " << py << ";\n";
           sets([&](bool lam) {
             for (int i = 0; i < N; ++i)
@@ -1409,8 +1421,9 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     b << "__shared__ C ptab_[" << K << "];\n"
       << "for (int j_ = tid; j_ < " << K << "; j_ += T) { R x_ = (R)1, y_ = (R)0;\n"
       << "  for (int m_ = " << nm << "_pto[j_]; m_ < " << nm << "_pto[j_ + 1]; ++m_) { const int s_ = " << nm
-      << "_pts[m_], k_ = " << nm << "_ptk[m_]; const R c_ = trig[8 * s_ + 2], sn_ = k_ < 0 ? -trig[8 * s_ + 3] : "
-         "trig[8 * s_ + 3];\n"
+      << "_pts[m_], k_ = " << nm << "_ptk[m_];\n"
+      << "    if (s_ < 0) { x_ = -x_; y_ = -y_; continue; }\n"
+      << "    const R c_ = trig[8 * s_ + 2], sn_ = k_ < 0 ? -trig[8 * s_ + 3] : trig[8 * s_ + 3];\n"
       << "    for (int r_ = 0; r_ < (k_ < 0 ? -k_ : k_); ++r_) { const R t_ = x_ * c_ - y_ * sn_; y_ = x_ * sn_ + y_ * c_; "
          "x_ = t_; } }\n"
       << "  ptab_[j_].x = x_; ptab_[j_].y = y_; }\n__syncthreads();\n";
