@@ -997,8 +997,12 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   // HQ_ABLATE (timing experiments only, results are wrong): backward kernels
   // without window transitions (1), gate math (2), derivative dots (4)
   const int ablate = std::getenv("HQ_ABLATE") ? std::atoi(std::getenv("HQ_ABLATE")) : 0;
-  int ubudget = 2;
+  // complex128 backward passes: the branch copies cost more than the FSEL swaps
+  // they save (2 CTAs/SM, latency bound; profiles/r01_ncu_c128_summary.md)
+  int ubudget = (bwd && !c64) ? 0 : 2;
   if (const char* e = std::getenv("HQ_UBRANCH")) ubudget = std::atoi(e);
+  if (bwd)
+    if (const char* e = std::getenv("HQ_UBRANCH_BWD")) ubudget = std::atoi(e);
   if (fused) ubudget = 0;
   if (first) {
     // the first pass is one long kernel: code size (instruction-cache misses) matters more
