@@ -44,6 +44,7 @@ hq_status fail(hq_status s, const std::string& msg) {
 constexpr int kMaxQubits = 34;
 constexpr int kMaxPreps = 32;
 constexpr size_t kMaxPassOps = 2048;   // bounds the per-pass trig cache in shared memory
+constexpr size_t kC128PassOps = 140;   // complex128 default cap (see make_plan)
 
 bool takes_angle(int k) {
   return k == HQ_GATE_RX || k == HQ_GATE_RY || k == HQ_GATE_RZ || k == HQ_GATE_CR;
@@ -850,7 +851,13 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
         gates.resize(cut);
       }
     }
-    const size_t op_cap = (opts & kSmallPasses) ? 48 : kMaxPassOps;   // generic kernels: shared-memory tables per pass
+    // generic kernels: shared-memory tables per pass.  complex128 pass kernels
+    // run at 2 CTAs/SM with 128 registers; a long first pass (cfg4: 184 ops,
+    // 15 windows) costs more than the extra pass a cap can add (cfg4 c128
+    // forward+backward 426.8 -> 381.1 ms at B=1024 with cap 140, 9 -> 8 passes;
+    // complex64 gets slower with any cap: profiles/r01_c128_pass_cap.log)
+    const size_t op_cap = (opts & kSmallPasses) ? 48
+                        : (d->precision == HQ_C128 ? kC128PassOps : kMaxPassOps);
     pl->passes = schedule_passes(gates, n, pl->tile_bits, f, 0, op_cap);
 
     // ---- fold leading single-qubit gates into the initial product state ----
