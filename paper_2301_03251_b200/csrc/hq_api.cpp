@@ -44,7 +44,7 @@ hq_status fail(hq_status s, const std::string& msg) {
 constexpr int kMaxQubits = 34;
 constexpr int kMaxPreps = 32;
 constexpr size_t kMaxPassOps = 2048;   // bounds the per-pass trig cache in shared memory
-constexpr size_t kC128PassOps = 140;   // complex128 default cap (see make_plan)
+constexpr size_t kC128PassOps = 140;   // complex128 candidate cap (see the plan builder)
 
 bool takes_angle(int k) {
   return k == HQ_GATE_RX || k == HQ_GATE_RY || k == HQ_GATE_RZ || k == HQ_GATE_CR;
@@ -852,13 +852,23 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
       }
     }
     // generic kernels: shared-memory tables per pass.  complex128 pass kernels
-    // run at 2 CTAs/SM with 128 registers; a long first pass (cfg4: 184 ops,
-    // 15 windows) costs more than the extra pass a cap can add (cfg4 c128
-    // forward+backward 426.8 -> 381.1 ms at B=1024 with cap 140, 9 -> 8 passes;
-    // complex64 gets slower with any cap: profiles/r01_c128_pass_cap.log)
-    const size_t op_cap = (opts & kSmallPasses) ? 48
-                        : (d->precision == HQ_C128 ? kC128PassOps : kMaxPassOps);
-    pl->passes = schedule_passes(gates, n, pl->tile_bits, f, 0, op_cap);
+    // run at 2 CTAs/SM with 128 registers: a schedule capped at 140 ops per
+    // pass is kept when it needs strictly fewer passes than the uncapped one
+    // (cfg4 c128: 9 -> 8 passes, first pass 184 -> 140 ops, forward+backward
+    // 426.8 -> 381.1 ms at B=1024).  With equal counts the capped schedule lost
+    // (cfg5 adjoint 8.09 -> 9.00 s), and complex64 gets slower with any cap
+    // (profiles/r01_c128_pass_cap.log).
+    const size_t op_cap = (opts & kSmallPasses) ? 48 : kMaxPassOps;
+    const bool try_cap = !(opts & kSmallPasses) && d->precision == HQ_C128;
+    auto schedule = [&](uint64_t excl0) {
+      auto best = schedule_passes(gates, n, pl->tile_bits, f, excl0, op_cap);
+      if (try_cap) {
+        auto capped = schedule_passes(gates, n, pl->tile_bits, f, excl0, kC128PassOps);
+        if (capped.size() < best.size()) best.swap(capped);
+      }
+      return best;
+    };
+    pl->passes = schedule(0);
 
     // ---- fold leading single-qubit gates into the initial product state ----
     // Qubits outside the first pass's tile: their whole single-qubit prefix
@@ -917,7 +927,7 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
         gates.swap(kept);
         // folded qubits with gradients: outside the first tile through λ contracted
         // over the tile (lamN), inside it through the tile-level contraction (locpart)
-        pl->passes = schedule_passes(gates, n, pl->tile_bits, f, fold_local_grad ? 0 : excl, op_cap);
+        pl->passes = schedule(fold_local_grad ? 0 : excl);
         for (int b : pl->passes[0].local)
           if (excl >> b & 1ull) {
             if (!fold_local_grad) {
