@@ -222,6 +222,10 @@ typedef struct {
 hq_status hq_profile_enable(hq_plan plan, int32_t enable);
 hq_status hq_profile_read(hq_plan plan, hq_profile_result* out);
 
+/* Process-wide count of kernel launches per class (HQ_K_*) since the library
+ * was loaded, over every plan (always on; host-side counters only). */
+void hq_launch_counts(int64_t out[HQ_K_CLASSES]);
+
 #ifdef __cplusplus
 }
 #endif

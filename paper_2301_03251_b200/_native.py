@@ -22,7 +22,7 @@ KIND_CODE = {"H": 0, "X": 1, "Y": 2, "Z": 3, "RX": 4, "RY": 5, "RZ": 6, "CNOT": 
 EXPORTS = ("hq_abi_version", "hq_last_error", "hq_plan_create", "hq_plan_destroy",
            "hq_plan_describe", "hq_workspace_bytes", "hq_forward", "hq_vjp", "hq_state",
            "hq_stats", "hq_profile_enable", "hq_profile_read", "hq_sample_workspace_bytes", "hq_sample",
-           "hq_shot_uniforms", "hq_noisy_workspace_bytes", "hq_noisy")
+           "hq_shot_uniforms", "hq_noisy_workspace_bytes", "hq_noisy", "hq_launch_counts")
 K_CLASSES = ("onchip", "pass_fwd", "pass_bwd", "other")
 
 
@@ -116,10 +116,19 @@ def lib():
     h.hq_noisy.argtypes = [_P, _P, ctypes.c_int64, _P, ctypes.c_int64, ctypes.c_int32, _P, ctypes.c_int32,
                            ctypes.c_int64, ctypes.c_uint64, _P, _P, _P, _P, ctypes.c_size_t, _P]
     h.hq_noisy.restype = ctypes.c_int
+    h.hq_launch_counts.argtypes = [_P]
+    h.hq_launch_counts.restype = None
     if h.hq_abi_version() != 2:
         raise NativeError(f"libhq ABI {h.hq_abi_version()} != 2")
     _lib = h
     return h
+
+
+def launch_counts() -> dict:
+    """Process-wide kernel launches per class since the library loaded."""
+    arr = (ctypes.c_int64 * 4)()
+    lib().hq_launch_counts(ctypes.cast(arr, _P))
+    return {k: int(arr[i]) for i, k in enumerate(K_CLASSES)}
 
 
 def check(status: int, what: str) -> None:

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -176,7 +177,15 @@ Layout layout_for(const hq_plan_s* pl, int64_t B, int32_t flags, bool need_state
 
 namespace hq {
 hq_status fail_status(hq_status s, const std::string& msg) { return fail(s, msg); }
+static std::atomic<int64_t> g_launch_count[HQ_K_CLASSES];
+void count_launch(int cls) {
+  if (cls >= 0 && cls < HQ_K_CLASSES) g_launch_count[cls].fetch_add(1, std::memory_order_relaxed);
+}
 }  // namespace hq
+
+extern "C" void hq_launch_counts(int64_t* out) {
+  for (int k = 0; k < HQ_K_CLASSES; ++k) out[k] = hq::g_launch_count[k].load(std::memory_order_relaxed);
+}
 
 extern "C" int hq_abi_version(void) { return HQ_ABI_VERSION; }
 extern "C" const char* hq_last_error(void) { return g_err.c_str(); }
@@ -1298,11 +1307,12 @@ extern "C" hq_status hq_forward(hq_plan pl, const double* x, int64_t ldx, const 
 extern "C" hq_status hq_state(hq_plan pl, const double* x, int64_t ldx, const double* theta,
                               int64_t batch, const double* init, int64_t init_rows, double* state,
                               void* ws, size_t ws_bytes, void* stream) {
+  if (!pl) return fail(HQ_E_CONFIG, "null plan");
   if (!state && batch > 0) return fail(HQ_E_CONFIG, "null state output");
   if (init && init_rows != 1 && init_rows != batch) return fail(HQ_E_DIMENSION, "init rows must be 1 or batch");
   // the readout still runs; route it into the workspace's scratch row
   const Layout L = layout_for(pl, batch, 0);
-  if (!pl || ws_bytes < L.total) return fail(HQ_E_CONFIG, "workspace too small");
+  if (ws_bytes < L.total) return fail(HQ_E_CONFIG, "workspace too small");
   char* w = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
   double* out = reinterpret_cast<double*>(w + L.scratch);
   return run(pl, x, ldx, theta, batch, 0, out, nullptr, state, init, init_rows, ws, ws_bytes, stream);

@@ -16,6 +16,7 @@ struct ProfScope {
   cudaStream_t st;
   ProfRec r;
   ProfScope(const hq_plan_s* p, cudaStream_t s, int cls, double bytes) : pl(p), st(s) {
+    count_launch(cls);
     if (!pl->prof.on) return;
     r.cls = cls;
     r.bytes = bytes;

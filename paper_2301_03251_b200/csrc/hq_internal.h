@@ -87,6 +87,8 @@ struct Prof {
 namespace hq {
 // sets hq_last_error() and returns s (for entry points outside hq_api.cpp)
 hq_status fail_status(hq_status s, const std::string& msg);
+// process-wide launch counters per kernel class (hq_launch_counts)
+void count_launch(int cls);
 }  // namespace hq
 
 struct hq_plan_s {

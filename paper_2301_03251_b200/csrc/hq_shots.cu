@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
 
 #include "hq_internal.h"
 
@@ -134,9 +135,10 @@ extern "C" hq_status hq_sample(const double* state, int64_t rows, int32_t n_qubi
                                double* expectation, void* ws, size_t ws_bytes, void* stream) {
   if (rows <= 0) return HQ_OK;
   if (n_qubits < 1 || n_qubits > 34 || n_measured < 1 || n_measured > n_qubits || !measured)
-    return HQ_E_CIRCUIT;
-  if (shots < 1) return HQ_E_CONFIG;
-  if (ws_bytes < hq_sample_workspace_bytes(rows, n_qubits, n_measured)) return HQ_E_CONFIG;
+    return hq::fail_status(HQ_E_CIRCUIT, "hq_sample: need 1 <= n_measured <= n_qubits <= 34 and a measured list");
+  if (shots < 1) return hq::fail_status(HQ_E_CONFIG, "hq_sample: shots must be >= 1");
+  if (ws_bytes < hq_sample_workspace_bytes(rows, n_qubits, n_measured))
+    return hq::fail_status(HQ_E_CONFIG, "hq_sample: workspace too small");
   hq::SampleArgs a{};
   a.state = state;
   a.rows = rows;
@@ -144,7 +146,8 @@ extern "C" hq_status hq_sample(const double* state, int64_t rows, int32_t n_qubi
   a.m = n_measured;
   uint64_t mask = 0;
   for (int k = 0; k < n_measured; ++k) {
-    if (measured[k] < 0 || measured[k] >= n_qubits || (mask >> measured[k] & 1)) return HQ_E_CIRCUIT;
+    if (measured[k] < 0 || measured[k] >= n_qubits || (mask >> measured[k] & 1))
+      return hq::fail_status(HQ_E_CIRCUIT, "hq_sample: measured qubit out of range or repeated");
     mask |= 1ull << measured[k];
     a.measured[k] = measured[k];
   }
@@ -170,13 +173,16 @@ extern "C" hq_status hq_sample(const double* state, int64_t rows, int32_t n_qubi
   const int64_t t3 = rows * shots;
   hq::k_shots<<<(unsigned)((t3 + 255) / 256), 256, 0, st>>>(a);
   if (expectation) hq::k_expect<<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(sum, rows, shots, expectation);
-  return cudaGetLastError() == cudaSuccess ? HQ_OK : HQ_E_CUDA;
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? HQ_OK : hq::fail_status(HQ_E_CUDA, std::string("hq_sample launch: ") + cudaGetErrorString(e));
 }
 
 extern "C" hq_status hq_shot_uniforms(uint64_t seed, int64_t shot0, int64_t count, double* out, void* stream) {
   if (count <= 0) return HQ_OK;
-  if (!out) return HQ_E_CONFIG;
+  if (!out) return hq::fail_status(HQ_E_CONFIG, "hq_shot_uniforms: null output");
   hq::k_uniforms<<<(unsigned)((count + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, shot0, count,
                                                                                                   out);
-  return cudaGetLastError() == cudaSuccess ? HQ_OK : HQ_E_CUDA;
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? HQ_OK
+                          : hq::fail_status(HQ_E_CUDA, std::string("hq_shot_uniforms launch: ") + cudaGetErrorString(e));
 }

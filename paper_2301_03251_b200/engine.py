@@ -147,6 +147,15 @@ class Plan:
         return {k: {"ms": r.ms[i], "launches": r.launches[i], "bytes": r.bytes[i]}
                 for i, k in enumerate(nat.K_CLASSES)}
 
+    def _on_device(self, *tensors):
+        """Every device operand must live on the plan's GPU (kernels and the
+        stream are that device's); -> the plan's current stream handle."""
+        torch = _torch()
+        for t in tensors:
+            if t is not None and (t.device.type != "cuda" or t.device.index != self.device):
+                raise DimensionError(f"tensor on {t.device} but the plan runs on cuda:{self.device}")
+        return torch.cuda.current_stream(self.device).cuda_stream
+
     def _ws(self, B, flags):
         torch = _torch()
         n = int(self._lib.hq_workspace_bytes(self._h, int(B), int(flags)))
@@ -160,11 +169,12 @@ class Plan:
         out = torch.empty(B, dtype=torch.float64, device=dev)
         jac = torch.empty((B, self.n_vars), dtype=torch.float64, device=dev) if want_jac else None
         flags = nat.HQ_WANT_JAC if want_jac else 0
+        st = self._on_device(x, theta)
         ws, nbytes = self._ws(B, flags)
-        st = torch.cuda.current_stream().cuda_stream
-        nat.check(self._lib.hq_forward(self._h, _ptr(x), int(x.stride(0)) if x.dim() == 2 else 0,
-                                       _ptr(theta), B, flags, _ptr(out), _ptr(jac), _ptr(ws),
-                                       ws.numel(), st), "forward")
+        with _torch().cuda.device(self.device):
+            nat.check(self._lib.hq_forward(self._h, _ptr(x), int(x.stride(0)) if x.dim() == 2 else 0,
+                                           _ptr(theta), B, flags, _ptr(out), _ptr(jac), _ptr(ws),
+                                           ws.numel(), st), "forward")
         return out, jac
 
     def vjp(self, jac, upstream, want_x=True, want_theta=True):
@@ -173,9 +183,10 @@ class Plan:
         dev = jac.device
         gx = torch.empty((B, self.n_inputs), dtype=torch.float64, device=dev) if want_x else None
         gt = torch.empty(self.n_params, dtype=torch.float64, device=dev) if want_theta else None
-        st = torch.cuda.current_stream().cuda_stream
-        nat.check(self._lib.hq_vjp(self._h, _ptr(jac), _ptr(upstream), B, _ptr(gx), _ptr(gt), st),
-                  "vjp")
+        st = self._on_device(jac, upstream)
+        with _torch().cuda.device(self.device):
+            nat.check(self._lib.hq_vjp(self._h, _ptr(jac), _ptr(upstream), B, _ptr(gx), _ptr(gt), st),
+                      "vjp")
         return gx, gt
 
     def state(self, x, theta, init=None):
@@ -183,12 +194,13 @@ class Plan:
         B = int(x.shape[0]) if x is not None else 1
         dev = f"cuda:{self.device}"
         st_out = torch.empty((B, 1 << self.n_qubits, 2), dtype=torch.float64, device=dev)
+        st = self._on_device(x, theta, init)
         ws, _ = self._ws(B, 0)
         rows = 0 if init is None else int(init.shape[0])
-        st = torch.cuda.current_stream().cuda_stream
-        nat.check(self._lib.hq_state(self._h, _ptr(x), int(x.stride(0)) if x is not None else 0,
-                                     _ptr(theta), B, _ptr(init), rows, _ptr(st_out), _ptr(ws),
-                                     ws.numel(), st), "state")
+        with _torch().cuda.device(self.device):
+            nat.check(self._lib.hq_state(self._h, _ptr(x), int(x.stride(0)) if x is not None else 0,
+                                         _ptr(theta), B, _ptr(init), rows, _ptr(st_out), _ptr(ws),
+                                         ws.numel(), st), "state")
         return st_out
 
 
@@ -208,11 +220,12 @@ class Plan:
         jac = torch.empty((B, self.n_vars), dtype=torch.float64, device=dev) if want_jac else None
         m = len(self.measured)
         counts = torch.empty((B, 1 << m), dtype=torch.int64, device=dev) if want_counts else None
-        st = torch.cuda.current_stream().cuda_stream
-        nat.check(self._lib.hq_noisy(self._h, _ptr(x), int(x.stride(0)) if x.dim() == 2 else 0, _ptr(theta), B,
-                                     flags, ctypes.cast(arr, ctypes.c_void_p), n_sites, int(shots),
-                                     ctypes.c_uint64(int(seed) & ((1 << 64) - 1)), _ptr(out), _ptr(jac),
-                                     _ptr(counts), _ptr(ws), ws.numel(), st), "noisy")
+        st = self._on_device(x, theta)
+        with _torch().cuda.device(self.device):
+            nat.check(self._lib.hq_noisy(self._h, _ptr(x), int(x.stride(0)) if x.dim() == 2 else 0, _ptr(theta), B,
+                                         flags, ctypes.cast(arr, ctypes.c_void_p), n_sites, int(shots),
+                                         ctypes.c_uint64(int(seed) & ((1 << 64) - 1)), _ptr(out), _ptr(jac),
+                                         _ptr(counts), _ptr(ws), ws.numel(), st), "noisy")
         return out, jac, counts
 
 
@@ -264,6 +277,33 @@ def _check_preps(tape: tr.Tape, x: np.ndarray, theta: np.ndarray):
             raise EncodingError("cannot embed the zero vector")
 
 
+def _check_finite(tape: tr.Tape, x: np.ndarray, theta: np.ndarray):
+    """The reference raises CircuitError('<KIND> requires one finite angle')
+    when it builds the GateOp of a sample whose angle is not finite
+    (qsim.py:60-63); the traced path only builds probe rows, so check every
+    row's gate angles here (state-load values: ``_check_preps``)."""
+    d = x.shape[1]
+    used = sorted({v for kind, _, slot in tape.ops if kind != "STATEPREP" and slot >= 0
+                   for v in tape.slot_terms[slot]})
+    ucols = [v for v in used if v < d]
+    bad_rows = np.zeros(x.shape[0], bool)
+    if ucols:
+        bad_rows = ~np.isfinite(x[:, ucols]).all(axis=1)
+    bad_theta = any(v >= d and not np.isfinite(theta[v - d]) for v in used)
+    if not bad_rows.any() and not bad_theta:
+        return
+    row = int(np.argmax(bad_rows)) if bad_rows.any() else 0
+    with np.errstate(all="ignore"):
+        for kind, _, slot in tape.ops:
+            if kind == "STATEPREP" or slot < 0:
+                continue
+            val = tape.slot_const[slot]
+            for v, c in tape.slot_terms[slot].items():
+                val = val + c * (x[row, v] if v < d else theta[v - d])
+            if not np.isfinite(val):
+                raise CircuitError(f"{kind} requires one finite angle")
+
+
 def run_batch(builder, xd: np.ndarray, pd: np.ndarray, want_x: bool, want_p: bool,
               precision: str = "c128", shift: float = math.pi / 2, grad_scale: float = 0.5,
               cache: PlanCache | None = None, light_cone: bool = False):
@@ -271,12 +311,13 @@ def run_batch(builder, xd: np.ndarray, pd: np.ndarray, want_x: bool, want_p: boo
 
     Returns ``(out [B], jac [B, d+P] | None, info)``.
     """
-    torch = _torch()
     B, d = xd.shape
     P = pd.shape[0]
     tape, ok = tr.trace(builder, xd, pd)
     if not ok:
         return run_per_sample(builder, xd, pd, want_x, want_p, precision, shift, grad_scale)
+    torch = _torch()
+    _check_finite(tape, xd, pd)
     if tape.preps:
         _check_preps(tape, xd, pd)
     if light_cone or os.environ.get("HQ_LIGHTCONE") == "1":
@@ -472,6 +513,8 @@ def run_batch_shots(builder, xd, pd, want_x, want_p, shots, seed, precision="c12
     B, d = xd.shape
     P = pd.shape[0]
     tape, ok = tr.trace(builder, xd, pd)
+    if ok:
+        _check_finite(tape, xd, pd)
     if ok and tape.preps:
         _check_preps(tape, xd, pd)
     ext = np.hstack([xd, np.broadcast_to(pd, (B, P))])
@@ -543,6 +586,8 @@ def run_batch_noisy(builder, xd, pd, want_x, want_p, noise, shots, seed, shift=m
     P = pd.shape[0]
     want = (want_x and d > 0) or (want_p and P > 0)
     tape, ok = tr.trace(builder, xd, pd)
+    if ok:
+        _check_finite(tape, xd, pd)
     if ok and not tape.preps:
         wanted = [want_x] * d + [want_p] * P
         spec = _twopoint_spec(d + P, wanted) if want else None

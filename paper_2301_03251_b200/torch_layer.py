@@ -9,9 +9,13 @@ through the host.  :class:`TorchQuantumLayer` keeps everything on the device:
   sequence when autograd needs them);
 * backward = one ``hq_vjp`` (upstream-scaled input rows, sample-ordered
   parameter sum) — the reference's ``df_x`` / ``df_p`` semantics;
-* the builder is traced once (first call, using that batch's first/last rows
-  and a random probe — the same checks as the host layer); later calls reuse
-  the plan without any host synchronisation, so forward+backward can be
+* the builder is traced per input width (first call with that width, using
+  the batch's first/last rows and a random probe — the same checks as the host
+  layer, which reject value-dependent control flow).  With ``recheck=True``
+  (default) every later batch re-runs the builder on its own first and last
+  rows (a 2-row device->host copy) and raises ``CircuitError`` if the tape
+  changed; inside CUDA-graph capture, or with ``recheck=False``, the cached
+  plan runs without any host synchronisation so forward+backward can be
   captured in a CUDA graph.
 """
 
@@ -31,12 +35,13 @@ class _QuantumFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, theta, plan, want_x, want_p):
         x64 = x.detach().to(torch.float64).contiguous()
-        th64 = theta.detach().to(torch.float64).contiguous()
+        th64 = theta.detach().to(device=x.device, dtype=torch.float64).contiguous()
         need = want_x or want_p
         out, jac = plan.forward(x64, th64, need)
         ctx.plan = plan
         ctx.want = (want_x, want_p)
         ctx.xdtype = x.dtype
+        ctx.tdev = theta.device
         if need:
             ctx.save_for_backward(jac)
         return out.to(x.dtype).unsqueeze(1)
@@ -47,7 +52,8 @@ class _QuantumFn(torch.autograd.Function):
         want_x, want_p = ctx.want
         gx, gt = ctx.plan.vjp(jac, g.detach().to(torch.float64).reshape(-1).contiguous(),
                               want_x and ctx.needs_input_grad[0], want_p and ctx.needs_input_grad[1])
-        return (gx.to(ctx.xdtype) if gx is not None else None, gt, None, None, None)
+        return (gx.to(ctx.xdtype) if gx is not None else None,
+                gt.to(ctx.tdev) if gt is not None else None, None, None, None)
 
 
 class TorchQuantumLayer(torch.nn.Module):
@@ -55,7 +61,7 @@ class TorchQuantumLayer(torch.nn.Module):
 
     def __init__(self, circuit_builder, n_params: int, precision: str = "c128",
                  shift: float = math.pi / 2, grad_scale: float = 0.5, param_init=None,
-                 device=None):
+                 device=None, recheck: bool = True):
         super().__init__()
         if n_params < 0:
             raise ConfigError("n_params must be >= 0")
@@ -75,25 +81,37 @@ class TorchQuantumLayer(torch.nn.Module):
         if param_init.shape != (n_params,):
             raise ConfigError(f"param_init shape {param_init.shape} != ({n_params},)")
         self.params = torch.nn.Parameter(torch.tensor(param_init, dtype=torch.float64, device=device))
-        self._tape = None
+        self.recheck = bool(recheck)
+        self._tapes = {}          # input width -> traced tape (variable ids depend on d)
         self._plans = {}
+
+    def _trace(self, x):
+        rows = x[[0, -1]].detach().to("cpu", torch.float64).numpy()
+        tape, ok = tr.trace(self.circuit_builder, rows, self.params.detach().cpu().numpy())
+        if not ok:
+            raise CircuitError("TorchQuantumLayer needs a batch-invariant affine builder "
+                               "(use QuantumLayer for data-dependent circuits)")
+        return tape
 
     def _plan(self, x, want_x, want_p):
         d = x.shape[1]
-        if self._tape is None:
-            rows = x[[0, -1]].detach().to("cpu", torch.float64).numpy()
-            tape, ok = tr.trace(self.circuit_builder, rows, self.params.detach().cpu().numpy())
-            if not ok:
-                raise CircuitError("TorchQuantumLayer needs a batch-invariant affine builder "
-                                   "(use QuantumLayer for data-dependent circuits)")
-            self._tape = tape
-        key = (want_x, want_p, d)
+        tape = self._tapes.get(d)
+        if tape is None:
+            tape = self._tapes[d] = self._trace(x)
+        elif self.recheck and not torch.cuda.is_current_stream_capturing():
+            if not tape.same_as(self._trace(x)):
+                raise CircuitError("circuit builder produced a different circuit for this batch than "
+                                   "the traced one (structure or angle expressions changed)")
+        if x.device.type != "cuda":
+            raise DimensionError(f"TorchQuantumLayer expects CUDA inputs, got {x.device}")
+        key = (want_x, want_p, d, x.device.index)
         plan = self._plans.get(key)
         if plan is None:
-            grad = tr.classify(self._tape, d + self.n_params, [want_x] * d + [want_p] * self.n_params,
+            grad = tr.classify(tape, d + self.n_params, [want_x] * d + [want_p] * self.n_params,
                                self.shift, self.grad_scale) if (want_x or want_p) else None
-            plan = engine.Plan(self._tape, d, self.n_params, self.precision, grad, self.shift,
-                               self.grad_scale)
+            with torch.cuda.device(x.device):
+                plan = engine.Plan(tape, d, self.n_params, self.precision, grad, self.shift,
+                                   self.grad_scale)
             self._plans[key] = plan
         return plan
 

@@ -16,7 +16,12 @@ Soundness checks (anything failing them takes the per-sample host path in
   no value-losing call such as ``np.sin(x)`` — caught because the recorded
   constant changes between traces);
 * the gate structure is identical at the first and last batch rows and at a
-  random point (data-dependent structure, e.g. ``templates.py:50``).
+  random point (data-dependent structure, e.g. ``templates.py:50``);
+* the builder never inspects the value of a variable-dependent scalar:
+  comparisons, truth tests, ``int``/``round``/``floor``/``ceil``/``divmod``
+  (and so ``max``/``min``/``if x > c``) on a traced value mark the trace
+  data-dependent, because a branch that flips only on a middle row would be
+  invisible to the probes.
 
 :func:`classify` decides per variable whether the adjoint pass reproduces the
 reference's two-point value: a variable entering exactly one
@@ -29,7 +34,7 @@ inputs feeding a state load) is evaluated by the batched two-point rule.
 from __future__ import annotations
 
 import math
-import numbers
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -37,6 +42,24 @@ import numpy as np
 from .errors import CircuitError
 
 _NUM = (int, float, np.integer, np.floating)
+
+# Set while a builder runs on traced scalars whenever it inspects the VALUE of a
+# variable-dependent scalar (comparison, truth test, int/round/floor/...): the
+# circuit may then depend on the data in a way two or three probe rows cannot
+# rule out, so the trace is rejected and the per-sample path runs.
+_probe = threading.local()
+
+
+def _mark_data_dependent():
+    _probe.data_dependent = True
+
+
+def _fv(v) -> float:
+    """Plain value of a number without marking the trace (internal use)."""
+    return float.__float__(v) if isinstance(v, float) else float(v)
+
+
+plain_float = _fv
 
 
 class TracedFloat(float):
@@ -56,7 +79,7 @@ class TracedFloat(float):
         if isinstance(v, TracedFloat):
             return v._c, v._t
         if isinstance(v, _NUM) and not isinstance(v, bool):
-            return float(v), {}
+            return _fv(v), {}
         return None
 
     def _affine(self, other, sa, sb, value):
@@ -83,23 +106,23 @@ class TracedFloat(float):
     # -- arithmetic --------------------------------------------------------------
     def __add__(self, o):
         r = self._affine(o, 1.0, 1.0, 0.0)
-        return r if r is NotImplemented else TracedFloat(float(self) + float(o), r._c, r._t)
+        return r if r is NotImplemented else TracedFloat(_fv(self) + _fv(o), r._c, r._t)
 
     __radd__ = __add__
 
     def __sub__(self, o):
         r = self._affine(o, 1.0, -1.0, 0.0)
-        return r if r is NotImplemented else TracedFloat(float(self) - float(o), r._c, r._t)
+        return r if r is NotImplemented else TracedFloat(_fv(self) - _fv(o), r._c, r._t)
 
     def __rsub__(self, o):
         r = self._affine(o, -1.0, 1.0, 0.0)
-        return r if r is NotImplemented else TracedFloat(float(o) - float(self), r._c, r._t)
+        return r if r is NotImplemented else TracedFloat(_fv(o) - _fv(self), r._c, r._t)
 
     def __mul__(self, o):
         b = TracedFloat._lift(o)
         if b is None:
             return NotImplemented
-        value = float(self) * float(o)
+        value = _fv(self) * _fv(o)
         if b[1] is not None and not b[1]:
             return self._scaled(b[0], value)
         if self._t is not None and not self._t and b[1] is not None:
@@ -112,7 +135,7 @@ class TracedFloat(float):
         b = TracedFloat._lift(o)
         if b is None:
             return NotImplemented
-        value = float(self) / float(o)
+        value = _fv(self) / _fv(o)
         if b[1] is not None and not b[1]:
             return self._scaled(1.0 / b[0], value)
         return TracedFloat(value, 0.0, None)
@@ -120,39 +143,101 @@ class TracedFloat(float):
     def __rtruediv__(self, o):
         if TracedFloat._lift(o) is None:
             return NotImplemented
-        return self._opaque(float(o) / float(self))
+        return self._opaque(_fv(o) / _fv(self))
 
     def __neg__(self):
-        return self._scaled(-1.0, -float(self))
+        return self._scaled(-1.0, -_fv(self))
 
     def __pos__(self):
         return self
 
     def __abs__(self):
-        return self._opaque(abs(float(self)))
+        return self._opaque(abs(_fv(self)))
 
     def __pow__(self, o, mod=None):
         if TracedFloat._lift(o) is None:
             return NotImplemented
-        return self._opaque(float(self) ** float(o))
+        return self._opaque(_fv(self) ** _fv(o))
 
     def __rpow__(self, o):
         if TracedFloat._lift(o) is None:
             return NotImplemented
-        return self._opaque(float(o) ** float(self))
+        return self._opaque(_fv(o) ** _fv(self))
 
     def __mod__(self, o):
         if TracedFloat._lift(o) is None:
             return NotImplemented
-        return self._opaque(float(self) % float(o))
+        return self._opaque(_fv(self) % _fv(o))
 
     def __floordiv__(self, o):
         if TracedFloat._lift(o) is None:
             return NotImplemented
-        return self._opaque(float(self) // float(o))
+        return self._opaque(_fv(self) // _fv(o))
 
     def __reduce__(self):
-        return (float, (float(self),))
+        return (float, (_fv(self),))
+
+    # -- value inspection: a branch on a variable marks the trace data-dependent
+    def _variable(self):
+        return self._t is None or any(c != 0.0 for c in self._t.values())
+
+    def _inspect(self, other=None):
+        if self._variable() or (isinstance(other, TracedFloat) and other._variable()):
+            _mark_data_dependent()
+
+    def __lt__(self, o):
+        self._inspect(o)
+        return float.__lt__(self, o)
+
+    def __le__(self, o):
+        self._inspect(o)
+        return float.__le__(self, o)
+
+    def __gt__(self, o):
+        self._inspect(o)
+        return float.__gt__(self, o)
+
+    def __ge__(self, o):
+        self._inspect(o)
+        return float.__ge__(self, o)
+
+    def __eq__(self, o):
+        self._inspect(o)
+        return float.__eq__(self, o)
+
+    def __ne__(self, o):
+        self._inspect(o)
+        return float.__ne__(self, o)
+
+    __hash__ = float.__hash__
+
+    def __bool__(self):
+        self._inspect()
+        return float.__bool__(self)
+
+    def __int__(self):
+        self._inspect()
+        return float.__int__(self)
+
+    def __trunc__(self):
+        self._inspect()
+        return float.__trunc__(self)
+
+    def __floor__(self):
+        self._inspect()
+        return float.__floor__(self)
+
+    def __ceil__(self):
+        self._inspect()
+        return float.__ceil__(self)
+
+    def __round__(self, ndigits=None):
+        self._inspect()
+        return float.__round__(self, ndigits) if ndigits is not None else float.__round__(self)
+
+    def __divmod__(self, o):
+        self._inspect(o)
+        return float.__divmod__(self, o)
 
 
 # ------------------------------------------------------------------------------
@@ -199,10 +284,10 @@ def _slot(tape: Tape, value) -> int:
             terms = {k: c for k, c in value._t.items() if c != 0.0}
         const = value._c
     elif isinstance(value, _NUM):
-        const, terms = float(value), {}
+        const, terms = _fv(value), {}
     else:
         raise CircuitError(f"gate angle {value!r} is not a number")
-    tape.slot_const.append(float(const))
+    tape.slot_const.append(_fv(const))
     tape.slot_terms.append(terms)
     return len(tape.slot_const) - 1
 
@@ -237,15 +322,22 @@ def traced_call(builder, inputs, params):
     d = len(inputs)
     xs = [TracedFloat(float(v), 0.0, {i: 1.0}) for i, v in enumerate(inputs)]
     ps = [TracedFloat(float(v), 0.0, {d + j: 1.0}) for j, v in enumerate(params)]
+    _probe.data_dependent = False
     try:
         circuit = builder(xs, ps)
     except CircuitError:
         raise
     except Exception as exc:
         raise CircuitError(f"circuit builder failed: {exc}") from exc
+    finally:
+        dep = getattr(_probe, "data_dependent", False)
+        _probe.data_dependent = False
     if circuit is None or not hasattr(circuit, "ops"):
         raise CircuitError("circuit builder must return a Circuit")
-    return tape_from_circuit(circuit)
+    tape = tape_from_circuit(circuit)
+    if dep:
+        tape.affine = False       # value-dependent control flow: per-sample path
+    return tape
 
 
 def trace(builder, x: np.ndarray, theta: np.ndarray, seed: int = 12345):

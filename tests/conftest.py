@@ -44,6 +44,16 @@ def normwise_error(a, b, floor=1e-300):
     return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), floor))
 
 
+def parity_log(name, **errs):
+    """Append measured parity errors to $PARITY_LOG (JSON lines) when set —
+    the evidence behind the tolerances stated in DESIGN.md §4."""
+    path = os.environ.get("PARITY_LOG")
+    if path:
+        import json
+        with open(path, "a") as f:
+            f.write(json.dumps({"case": name, **{k: float(v) for k, v in errs.items()}}) + "\n")
+
+
 def golden(name):
     path = os.path.join(GOLDEN, f"{name}.npz")
     if not os.path.exists(path):

@@ -53,20 +53,51 @@ def layer_case(name, cfg, batch, want_x, seed_g=7):
          seconds=np.array(dt))
 
 
-def cfg4_case():
+def _cfg4_eval(args):
+    # one reference circuit evaluation (QuantumLayer._run, qnn.py:120-121)
+    xi, th = args
     builder = wl.make_builder("cfg4", rq, rt)
-    x = wl.inputs_for("cfg4", 2)
+    layer = QuantumLayer(builder, n_params=th.size, param_init=th)
+    return layer._run(xi, th)
+
+
+def cfg4_case():
+    """cfg4 (the bench config) pinned per SURVEY.md §8(c) and beyond: 4
+    samples' forward, the FULL 400-entry shift-rule gradient row of sample 0,
+    32 random rows entries of sample 1, and the layer's df_p for a random
+    upstream over samples {0, 1} at those 32 indices (parameter_shift_grad,
+    qnn.py:35-52, summed in sample order, qnn.py:147-152).  Evaluations run in
+    a process pool; each is the reference's own QuantumLayer._run."""
+    from concurrent.futures import ProcessPoolExecutor
+    builder = wl.make_builder("cfg4", rq, rt)
+    x = wl.inputs_for("cfg4", 4)
     theta = wl.params_for("cfg4")
     layer = QuantumLayer(builder, n_params=theta.size, param_init=theta)
-    out = layer(Tensor(x, dtype=np.float64)).numpy()[:, 0]
-    idx = np.array([0, 1, 57, 200, 311, 399])
-    s = layer.shift
-    jac = []
-    for j in idx:
+    s, scale = layer.shift, layer.grad_scale
+    rng = np.random.default_rng(404)
+    idx1 = np.sort(rng.choice(theta.size, 32, replace=False))
+    g = rng.uniform(0.5, 1.5, 2)
+    jobs = [(x[i], theta) for i in range(4)]
+    rows = [(0, j) for j in range(theta.size)] + [(1, int(j)) for j in idx1]
+    for i, j in rows:
         tp = theta.copy(); tp[j] += s
         tm = theta.copy(); tm[j] -= s
-        jac.append((layer._run(x[0], tp) - layer._run(x[0], tm)) * layer.grad_scale)
-    save("cfg4", x=x, theta=theta, out=out, jac_idx=idx, jac0=np.array(jac))
+        jobs += [(x[i], tp), (x[i], tm)]
+    t0 = time.perf_counter()
+    with ProcessPoolExecutor(os.cpu_count()) as ex:
+        vals = list(ex.map(_cfg4_eval, jobs, chunksize=4))
+    dt = time.perf_counter() - t0
+    out = np.array(vals[:4])
+    ev = np.array(vals[4:]).reshape(-1, 2)
+    jac0 = (ev[:theta.size, 0] - ev[:theta.size, 1]) * scale
+    jac1 = (ev[theta.size:, 0] - ev[theta.size:, 1]) * scale
+    # df_p at upstream g over samples 0, 1 (reference operation order)
+    grad_p = np.zeros(idx1.size)
+    grad_p += (ev[idx1, 0] - ev[idx1, 1]) * scale * float(g[0])
+    grad_p += (ev[theta.size:, 0] - ev[theta.size:, 1]) * scale * float(g[1])
+    save("cfg4", x=x, theta=theta, out=out, jac_idx=np.arange(theta.size), jac0=jac0,
+         jac1_idx=idx1, jac1=jac1, upstream=g, grad_p_idx=idx1, grad_p=grad_p,
+         evaluations=np.array(len(jobs)), seconds=np.array(dt))
 
 
 def random_circuits_case():
@@ -274,9 +305,9 @@ if __name__ == "__main__":
     if "cfg1" in which:
         layer_case("cfg1", "cfg1", 16, True)
     if "cfg2" in which:
-        layer_case("cfg2", "cfg2", 3, True)
+        layer_case("cfg2", "cfg2", 16, True)
     if "cfg3" in which:
-        layer_case("cfg3", "cfg3", 2, False)
+        layer_case("cfg3", "cfg3", 4, False)
     if "cfg4" in which:
         cfg4_case()
     if "random" in which:

@@ -1,11 +1,15 @@
 """GPU parity: the sm_100a path against golden vectors (produced by the
 reference itself) and against the CPU oracle on seeded inputs.
 
-Tolerances (north_star): complex128 1e-10 relative (absolute floor 1e-4 for
-near-zero entries); complex64 1e-5 relative on expectations/amplitudes and
-1e-5 normwise on gradient vectors: ‖Δ‖∞ / max(‖ref‖∞, 0.1) — float32 state
-error makes elementwise relative error meaningless for gradients that are
-exactly or nearly zero.
+Tolerances (north_star):
+* complex128: 1e-10 normwise relative, ‖Δ‖∞ / ‖ref‖∞, no floor, on
+  expectation vectors and gradient vectors;
+* complex64: 1e-5 normwise relative on expectation vectors; gradient vectors
+  1e-5 of max(‖ref‖∞, 0.1) — gradient entries are differences of
+  expectations whose float32 rounding error scales with the expectation
+  (O(1)), not with the (small) gradient, so relative-to-gradient error is not a
+  property float32 amplitudes can have; the unfloored value is logged
+  (``parity_log``) and reported in DESIGN.md.
 """
 
 import math
@@ -14,7 +18,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import golden, normwise_error, relative_error
+from conftest import golden, normwise_error, parity_log, relative_error
 from oracle import hq_oracle as O
 from paper_2301_03251_b200 import (Circuit, QAELayer, QuantumLayer, Tensor, backward, no_grad,
                                    qsim, tsum, workloads as wl)
@@ -26,13 +30,16 @@ pytestmark = pytest.mark.gpu
 PRECS = ["c128", "c64"]
 
 
-def check_vals(got, want, prec, grad=False):
+def check_vals(got, want, prec, grad=False, name=None):
+    err = normwise_error(got, want)
+    if name:
+        parity_log(f"{name}:{prec}", normwise=err, floored=normwise_error(got, want, floor=0.1))
     if prec == "c128":
-        assert relative_error(got, want, floor=1e-3 if grad else 1e-4) < 1e-10
+        assert err < 1e-10, err
     elif grad:
         assert normwise_error(got, want, floor=0.1) < 1e-5
     else:
-        assert relative_error(got, want, floor=1e-3) < 1e-5
+        assert err < 1e-5, err
 
 
 def layer_run(builder, x, theta, prec, upstream=None, want_x=True):
@@ -75,9 +82,9 @@ def test_cfg1_golden(prec):
     b = wl.make_builder("cfg1", qsim, T)
     out, gx, gp, layer = layer_run(b, g["x"], g["theta"], prec, g["upstream"])
     assert "onchip" in layer.last_info["plan"].description
-    check_vals(out, g["out"], prec)
-    check_vals(gx, g["grad_x"], prec, grad=True)
-    check_vals(gp, g["grad_p"], prec, grad=True)
+    check_vals(out, g["out"], prec, name="cfg1.out")
+    check_vals(gx, g["grad_x"], prec, grad=True, name="cfg1.grad_x")
+    check_vals(gp, g["grad_p"], prec, grad=True, name="cfg1.grad_p")
 
 
 @pytest.mark.parametrize("prec", PRECS)
@@ -85,9 +92,10 @@ def test_cfg2_golden(prec):
     g = golden("cfg2")
     b = wl.make_builder("cfg2", qsim, T)
     out, gx, gp, _ = layer_run(b, g["x"], g["theta"], prec, g["upstream"])
-    check_vals(out, g["out"], prec)
-    check_vals(gx, g["grad_x"], prec, grad=True)
-    check_vals(gp, g["grad_p"], prec, grad=True)
+    assert len(out) == 16
+    check_vals(out, g["out"], prec, name="cfg2.out")
+    check_vals(gx, g["grad_x"], prec, grad=True, name="cfg2.grad_x")
+    check_vals(gp, g["grad_p"], prec, grad=True, name="cfg2.grad_p")
 
 
 def test_cfg3_golden_state_load_and_adjoint():
@@ -95,23 +103,36 @@ def test_cfg3_golden_state_load_and_adjoint():
     b = wl.make_builder("cfg3", qsim, T)
     out, _, gp, layer = layer_run(b, g["x"], g["theta"], "c128", g["upstream"], want_x=False)
     assert "preps=1" in layer.last_info["plan"].description
-    check_vals(out, g["out"], "c128")
-    check_vals(gp, g["grad_p"], "c128", grad=True)
+    assert len(out) == 4
+    check_vals(out, g["out"], "c128", name="cfg3.out")
+    check_vals(gp, g["grad_p"], "c128", grad=True, name="cfg3.grad_p")
 
 
 @pytest.mark.parametrize("prec", PRECS)
 def test_cfg4_golden_streaming(prec):
+    """The bench circuit on the bench's own plan (folded prefixes, folded
+    trailing permutation, deferred RZ phases) against the reference: 4
+    forwards, sample 0's full 400-entry gradient row, 32 entries of sample 1."""
     g = golden("cfg4")
     b = wl.make_builder("cfg4", qsim, T)
     layer = QuantumLayer(b, n_params=400, param_init=g["theta"], precision=prec)
     res, jac, info = engine.run_batch(b, g["x"], g["theta"], False, True, prec, cache=layer._plans)
     assert "stream" in info["plan"].description
-    check_vals(res, g["out"], prec)
-    j = jac.cpu().numpy()[0, 20:][g["jac_idx"]]
-    if prec == "c128":
-        assert relative_error(j, g["jac0"], floor=1e-4) < 1e-10
-    else:
-        assert np.max(np.abs(j - g["jac0"])) < 1e-5 * max(np.max(np.abs(g["jac0"])), 1e-2)
+    check_vals(res, g["out"], prec, name="cfg4.out")
+    j = jac.cpu().numpy()[:, 20:]
+    check_vals(j[0][g["jac_idx"]], g["jac0"], prec, grad=True, name="cfg4.jac0_full")
+    check_vals(j[1][g["jac1_idx"]], g["jac1"], prec, grad=True, name="cfg4.jac1")
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_cfg4_golden_layer_upstream(prec):
+    """df_p through the public layer for a random upstream over samples 0, 1
+    (reference: parameter_shift_grad summed in sample order, qnn.py:147-152)."""
+    g = golden("cfg4")
+    b = wl.make_builder("cfg4", qsim, T)
+    out, _, gp, _ = layer_run(b, g["x"][:2], g["theta"], prec, g["upstream"], want_x=False)
+    check_vals(out, g["out"][:2], prec, name="cfg4.layer_out")
+    check_vals(gp[g["grad_p_idx"]], g["grad_p"], prec, grad=True, name="cfg4.layer_grad_p")
 
 
 @pytest.mark.parametrize("prec", PRECS)
@@ -127,9 +148,9 @@ def test_reupload_two_point_path(prec):
         return c
     out, gx, gp, layer = layer_run(b, g["x"], g["theta"], prec, g["upstream"])
     assert "twopoint_vars=3" in layer.last_info["plan"].description  # x0, x1, θ0 enter twice
-    check_vals(out, g["out"], prec)
-    check_vals(gx, g["grad_x"], prec, grad=True)
-    check_vals(gp, g["grad_p"], prec, grad=True)
+    check_vals(out, g["out"], prec, name="reupload.out")
+    check_vals(gx, g["grad_x"], prec, grad=True, name="reupload.grad_x")
+    check_vals(gp, g["grad_p"], prec, grad=True, name="reupload.grad_p")
 
 
 @pytest.mark.parametrize("name,trash,total", [("qae_1_4", 1, 4), ("qae_2_7", 2, 7)])
@@ -139,8 +160,8 @@ def test_qae_layer_golden(name, trash, total):
     out = layer(Tensor(g["x"], dtype=np.float64))
     up = g.get("upstream", np.ones(len(g["x"])))
     backward(tsum(out * Tensor(up.reshape(-1, 1), dtype=np.float64)))
-    assert relative_error(out.numpy()[:, 0], g["out"], floor=1e-4) < 1e-10
-    assert relative_error(layer.params.grad, g["grad_p"], floor=1e-4) < 1e-10
+    check_vals(out.numpy()[:, 0], g["out"], "c128", name=f"{name}.out")
+    check_vals(layer.params.grad, g["grad_p"], "c128", grad=True, name=f"{name}.grad_p")
 
 
 def test_embedding_states_golden():
@@ -299,6 +320,76 @@ def test_no_grad_skips_jacobian():
         out = layer(Tensor(wl.inputs_for("cfg1", 8), dtype=np.float64))
     assert not out.requires_grad
     assert "adjoint_slots=0" in layer.last_info["plan"].description
+
+
+def _bwd_launches():
+    from paper_2301_03251_b200 import _native
+    return _native.launch_counts()["pass_bwd"]
+
+
+def test_lazy_jacobian_forward_only_launches_no_backward():
+    """The reference defers gradient work to the df closures (qnn.py:136-153):
+    a forward whose graph is never differentiated runs no backward pass."""
+    b = wl.make_builder("cfg2", qsim, T)
+    th = wl.params_for("cfg2")
+    x = wl.inputs_for("cfg2", 32)
+    layer = QuantumLayer(b, n_params=60, param_init=th)
+    n0 = _bwd_launches()
+    out = layer(Tensor(x, requires_grad=True, dtype=np.float64))
+    assert "stream" in layer.last_info["plan"].description
+    assert _bwd_launches() == n0                      # forward only
+    out2 = layer(Tensor(x, dtype=np.float64))          # evaluation loop without no_grad
+    assert _bwd_launches() == n0
+    # the first backward runs forward + adjoint at the forward-time snapshot
+    layer.params.data[:] = 0.0                          # later edits must not leak in
+    backward(tsum(out2))
+    assert _bwd_launches() > n0
+    o, _, _, _, gp = O.layer(wl.make_builder("cfg2", O, O), x, th)
+    assert normwise_error(out2.numpy()[:, 0], o) < 1e-10
+    assert normwise_error(layer.params.grad, gp) < 1e-10
+    # auto mode: once a gradient was used, the next forward produces it eagerly
+    layer.params.data[:] = th
+    layer.params.zero_grad()
+    n1 = _bwd_launches()
+    out3 = layer(Tensor(x, dtype=np.float64))
+    n2 = _bwd_launches()
+    assert n2 > n1
+    backward(tsum(out3))
+    assert _bwd_launches() == n2                        # nothing recomputed
+    assert normwise_error(layer.params.grad, gp) < 1e-10
+
+
+def test_eager_and_lazy_modes_agree():
+    b = wl.make_builder("cfg1", qsim, T)
+    th = wl.params_for("cfg1")
+    x = wl.inputs_for("cfg1", 16)
+    grads = []
+    for mode in ("eager", "lazy"):
+        layer = QuantumLayer(b, n_params=24, param_init=th, jacobian=mode)
+        xt = Tensor(x, requires_grad=True, dtype=np.float64)
+        backward(tsum(layer(xt)))
+        grads.append((xt.grad, layer.params.grad))
+    np.testing.assert_array_equal(grads[0][0], grads[1][0])
+    np.testing.assert_array_equal(grads[0][1], grads[1][1])
+
+
+def test_run_single_circuit_hook():
+    """QuantumLayer._run (used by the reference's runner.py:203) on the GPU."""
+    b = wl.make_builder("cfg1", qsim, T)
+    th = wl.params_for("cfg1")
+    x = wl.inputs_for("cfg1", 3)
+    layer = QuantumLayer(b, n_params=24, param_init=th)
+    for i in range(3):
+        e = layer._run(x[i], th)
+        assert isinstance(e, float)
+        assert e == pytest.approx(O.run(wl.make_builder("cfg1", O, O), x[i], th), abs=1e-12)
+    # shifted parameters, as parameter_shift_grad calls it (qnn.py:35-52)
+    tp = th.copy(); tp[3] += np.pi / 2
+    assert layer._run(x[0], tp) == pytest.approx(O.run(wl.make_builder("cfg1", O, O), x[0], tp), abs=1e-12)
+    for mt in ("shot_sampling",):
+        lay = QuantumLayer(b, n_params=24, param_init=th, machine_type=mt, shots=200, seed=3)
+        v = lay._run(x[0], th)
+        assert 0.0 <= v <= 1.0
 
 
 def test_cfg4_full_size_norm():

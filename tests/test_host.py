@@ -137,6 +137,62 @@ class TestTracer:
         _, ok = tr.trace(b, np.array([[0.3], [-0.2]]), np.zeros(0))
         assert not ok
 
+    def test_branch_on_middle_row_detected(self):
+        # the branch flips only on row 1: first/last/random probes all agree
+        def b(inputs, params):
+            c = Circuit(2)
+            if inputs[0] > 2.0:
+                c.x(1)
+            c.ry(0, inputs[0])
+            return c
+        _, ok = tr.trace(b, np.array([[0.3], [2.5], [0.5]]), np.zeros(0))
+        assert not ok
+
+    @pytest.mark.parametrize("fn", [lambda v: max(v, 1.5), lambda v: min(v, -3.0),
+                                    lambda v: float(round(v)), lambda v: float(math.floor(v)),
+                                    lambda v: float(int(v)), lambda v: 0.3 if v else 0.1])
+    def test_value_inspection_detected(self, fn):
+        def b(inputs, params):
+            c = Circuit(1)
+            c.ry(0, fn(inputs[0]))
+            return c
+        _, ok = tr.trace(b, np.array([[0.3], [2.5], [0.5]]), np.zeros(0))
+        assert not ok
+
+    def test_constant_comparisons_stay_traced(self):
+        # comparisons between constants (or a traced constant) are not data-dependent
+        def b(inputs, params):
+            c = Circuit(1)
+            k = 0.0 * inputs[0] + 1.0
+            if k > 0.5 and len(params) == 1:
+                c.ry(0, params[0])
+            return c
+        _, ok = tr.trace(b, np.array([[0.3], [2.5]]), np.array([0.2]))
+        assert ok
+
+    def test_middle_row_branch_matches_oracle_per_sample(self):
+        # the layer falls back to per-sample evaluation: row 1 sees its X gate
+        from paper_2301_03251_b200 import engine
+        called = []
+
+        def fake_per_sample(builder, xd, pd, *a, **k):
+            called.append(True)
+            return np.zeros(xd.shape[0]), None, {"plan": None, "path": "per_sample"}
+
+        def b(inputs, params):
+            c = Circuit(2)
+            if inputs[0] > 2.0:
+                c.x(1)
+            c.ry(0, inputs[0])
+            return c
+        orig = engine.run_per_sample
+        engine.run_per_sample = fake_per_sample
+        try:
+            engine.run_batch(b, np.array([[0.3], [2.5], [0.5]]), np.zeros(0), False, False)
+        finally:
+            engine.run_per_sample = orig
+        assert called
+
     def test_amplitude_embedding_lowers_to_state_load(self):
         b = wl.make_builder("cfg3", qsim, T)
         x = wl.inputs_for("cfg3", 3)
@@ -246,3 +302,21 @@ def test_light_cone_cfg4_shrinks():
     tape, ok = tr.trace(b, wl.inputs_for("cfg4", 2), wl.params_for("cfg4"))
     lc = tr.light_cone(tape)
     assert lc.n_qubits == 10 and len(lc.ops) == 164 and lc.measured == [0]
+
+
+def test_non_finite_middle_row_raises_reference_error():
+    # qsim.py:60-63: the sample's GateOp construction fails; the traced path
+    # only builds probe rows, so engine checks every row's angles
+    from paper_2301_03251_b200 import engine
+    b = wl.make_builder("cfg1", qsim, T)
+    x = wl.inputs_for("cfg1", 5)
+    tape, ok = tr.trace(b, x, wl.params_for("cfg1"))
+    assert ok
+    engine._check_finite(tape, x, wl.params_for("cfg1"))      # finite: no error
+    x[2, 1] = np.nan
+    with pytest.raises(CircuitError, match="RY requires one finite angle"):
+        engine._check_finite(tape, x, wl.params_for("cfg1"))
+    th = wl.params_for("cfg1")
+    th[4] = np.inf
+    with pytest.raises(CircuitError, match="requires one finite angle"):
+        engine._check_finite(tape, wl.inputs_for("cfg1", 5), th)
