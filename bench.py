@@ -1,29 +1,40 @@
 #!/usr/bin/env python
 """Benchmark: circuit forward+grad evals/s on the cfg4 workload.
 
-Workload ("step"): one forward + full parameter gradient of a batch of the
-20-qubit hardware-efficient ansatz (depth 10, 610 gates, 400 parameters,
-complex64) — BASELINE.json configs[3], the configuration the metric's
-"% HBM roofline" and the 1/2/4/8-GPU scaling are quoted on.  Weak scaling:
-every rank owns 4096 samples; the 400-dim gradient is all-reduced over NCCL.
+Workload ("step"): one forward + full parameter gradient of the global batch
+(B = 4096 samples) of the 20-qubit hardware-efficient ansatz (depth 10, 610
+gates, 400 parameters) — BASELINE.json configs[3], the configuration the
+metric's "% HBM roofline" and the 1/2/4/8-GPU scaling are quoted on.  The
+headline runs at complex128, the reference's own arithmetic (qsim.py:81,
+qnn.py:126); complex64 is reported beside it (`complex64`).
+
+Multi-GPU: strong scaling — the global batch is split into
+contiguous blocks of B/N samples per rank, θ is replicated, and each step ends
+with ONE all-reduce(sum) of the [400] f64 parameter gradient (replaces the
+serial batch loop and sequential gradient sum of qnn.py:131,147-152).
 
   python bench.py [--gpus N --steps K --warmup W]          (our arm)
   python bench.py --impl reference [...]                     (reference CPU arm)
 
-One JSON line on rank 0.  `value` is device-timed (CUDA events, inputs resident
-in HBM, max over ranks); `e2e` goes through the public QuantumLayer API with
-host tensors (H2D of inputs, D2H of outputs and gradients inside the timed
-region); `roofline` uses the amplitude-update kernel's live CUDA-event time;
-`cpu_baseline` times the NumPy oracle port of the reference on a bounded sample;
-`complex128` repeats the device-timed step at the reference's own precision.
+`--gpus N` without a torchrun environment re-launches itself under
+`torch.distributed.run` with N ranks (127.0.0.1).  One JSON line on rank 0.
+`value` is device-timed (CUDA events, inputs resident in HBM, max over
+ranks); `e2e` goes through the public QuantumLayer API with host tensors (H2D
+of inputs, D2H of outputs and gradients inside the timed region); `roofline`
+uses the dominant kernel class's live CUDA-event time; `cpu_baseline` times the
+reference itself (hyqnet, vendored into oracle/_ref by oracle/Makefile) on one
+core over a bounded sample.  `--stub --backend gloo` runs the multi-rank
+harness on CPU with a NumPy stand-in evaluator (tests only; marked "stub").
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -46,16 +57,84 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="cfg4")
-    ap.add_argument("--batch", type=int, default=None, help="samples per GPU")
-    ap.add_argument("--precision", default=None)
+    ap.add_argument("--batch", type=int, default=None, help="GLOBAL batch (split B/N over ranks)")
+    ap.add_argument("--precision", default="c128", choices=["c64", "c128"],
+                    help="headline precision (default: the reference's complex128)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-c128", action="store_true", help="skip the complex128 companion measurement")
-    ap.add_argument("--backend", default="nccl", help="process-group backend (gloo: dry runs of the "
-                    "multi-rank path with several ranks on one device)")
+    ap.add_argument("--no-companion", action="store_true",
+                    help="skip the other-precision companion measurement")
+    ap.add_argument("--backend", default="nccl")
+    ap.add_argument("--stub", action="store_true",
+                    help="CPU harness test: NumPy stand-in evaluator instead of the CUDA plan")
     return ap.parse_args()
 
 
+# ------------------------------------------------------------------------------
+# launcher
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def maybe_spawn(a) -> None:
+    """--gpus N outside torchrun: re-exec under torch.distributed.run (N ranks)."""
+    if a.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    r = subprocess.run(cmd)
+    sys.exit(r.returncode)
+
+
+class Dist:
+    """Process group plumbing (one process per GPU)."""
+
+    def __init__(self, a, device_required=True):
+        import torch
+        import torch.distributed as dist
+        self.dist = dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.cuda = device_required
+        if device_required:
+            self.local = self.local % max(torch.cuda.device_count(), 1)
+            torch.cuda.set_device(self.local)
+            self.device = torch.device(f"cuda:{self.local}")
+        else:
+            self.device = torch.device("cpu")
+        if self.world > 1:
+            if a.backend == "nccl":
+                dist.init_process_group("nccl", device_id=self.device)
+            else:
+                dist.init_process_group(a.backend)
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def allreduce_(self, t, op="sum"):
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM if op == "sum" else self.dist.ReduceOp.MAX)
+        return t
+
+    def max_scalar(self, v):
+        import torch
+        t = torch.tensor([float(v)], dtype=torch.float64, device=self.device)
+        return float(self.allreduce_(t, "max").item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------
+# peaks / clocks
 def fp_peak(prec):
     """Measured FMA throughput (tools/fma_peak.cu -> profiles/r01_fma_peak.json)."""
     try:
@@ -66,13 +145,13 @@ def fp_peak(prec):
         return (75.0 if prec == "c64" else 37.0), "datasheet"
 
 
-def peaks():
+def hbm_peak():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class Clocks:
@@ -123,47 +202,87 @@ class Clocks:
 
 
 # ------------------------------------------------------------------------------
-def cpu_baseline(cfg, x0, theta, budget_pairs=1):
-    """Oracle port of the reference, one core, bounded sample."""
+# the reference CPU implementation (measurement infrastructure, never the product)
+def reference_modules():
+    """(qsim, templates, QuantumLayer, kind): the reference hyqnet itself,
+    vendored unmodified into oracle/_ref by oracle/Makefile ("reference"), or
+    the NumPy oracle restatement when that copy is absent ("port")."""
+    ref = os.path.join(REPO, "oracle", "_ref")
+    if os.path.isdir(os.path.join(ref, "hyqnet")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        import hyqnet.qsim as rq
+        import hyqnet.templates as rt
+        from hyqnet.qnn import QuantumLayer as RL
+        return rq, rt, RL, "reference"
     from oracle import hq_oracle as O
+    return O, O, None, "port"
+
+
+def _ref_eval(builder_mods, cfg, x_row, theta):
+    rq, rt, RL, kind = builder_mods
     from paper_2301_03251_b200 import workloads as wl
-    b = wl.make_builder(cfg, O, O)
-    t0 = time.perf_counter()
-    evals = O.sample_cost(b, x0, theta, budget_pairs)
-    dt = time.perf_counter() - t0
-    per_sample = 1 + 2 * theta.size          # cfg4: θ-only gradient (801 evaluations)
-    return {"value": evals / dt / per_sample, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"1 sample: forward + {budget_pairs} shifted parameter pairs = {evals} of the "
-                      f"{per_sample} circuit evaluations one forward+grad takes (reference "
-                      f"parameter_shift_grad, qnn.py:35-52), {dt:.1f} s, extrapolated linearly"}
+    b = wl.make_builder(cfg, rq, rt)
+    if RL is not None:
+        lay = RL(b, n_params=theta.size, param_init=theta)
+        return lay._run(x_row, theta)              # qnn.py:120-121, as parameter_shift_grad calls it
+    from oracle import hq_oracle as O
+    return O.run(b, x_row, theta)
 
 
 def _ref_worker(args):
     cfg, x_row, theta = args
     sys.path.insert(0, REPO)
-    from oracle import hq_oracle as O
-    from paper_2301_03251_b200 import workloads as wl
-    return O.run(wl.make_builder(cfg, O, O), x_row, theta)
+    return _ref_eval(reference_modules(), cfg, x_row, theta)
+
+
+def evals_per_sample(cfg, P, d):
+    return 1 + 2 * P + (2 * d if cfg in ("cfg1", "cfg2") else 0)
+
+
+def cpu_baseline(cfg, x0, theta, budget_pairs=2):
+    """The reference on one core, bounded sample: one forward
+    plus ``budget_pairs`` shifted parameter pairs of sample 0, extrapolated to
+    the 1 + 2P evaluations of a forward + full gradient."""
+    mods = reference_modules()
+    shift = math.pi / 2
+    t0 = time.perf_counter()
+    _ref_eval(mods, cfg, x0, theta)
+    n = 1
+    for j in range(budget_pairs):
+        for s in (shift, -shift):
+            t = theta.copy()
+            t[j] += s
+            _ref_eval(mods, cfg, x0, t)
+            n += 1
+    dt = time.perf_counter() - t0
+    per = evals_per_sample(cfg, theta.size, 0)
+    return {"value": n / dt / per, "unit": UNIT, "cores": 1, "kind": mods[3],
+            "sample": f"1 sample: forward + {budget_pairs} shifted parameter pairs = {n} of the {per} "
+                      f"circuit evaluations of one forward+grad (QuantumLayer._run, qnn.py:120-121, as "
+                      f"parameter_shift_grad calls it, qnn.py:35-52), {dt:.1f} s on 1 core, extrapolated "
+                      f"linearly"}
 
 
 def run_reference(a):
-    """--impl reference: the NumPy port of the reference on all host cores."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """--impl reference: the reference's own CPU path on all host cores."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
     from concurrent.futures import ProcessPoolExecutor
     from paper_2301_03251_b200 import workloads as wl
     cfg = a.config
-    n, d, P, B, prec = wl.CONFIGS[cfg]
+    n, d, P, B0, _ = wl.CONFIGS[cfg]
+    B = a.batch or B0
     x = wl.inputs_for(cfg, 64 if cfg == "cfg4" else B)
     theta = wl.params_for(cfg)
+    kind = reference_modules()[3]
     cores = os.cpu_count() or 1
-    per_sample = 1 + 2 * P + (2 * d if cfg in ("cfg1", "cfg2") else 0)
+    per = evals_per_sample(cfg, P, d)
     times = []
     with ProcessPoolExecutor(cores) as ex:
         for step in range(a.warmup + a.steps):
-            # each step: one circuit evaluation per core (a shard of the
-            # 1 + 2P evaluations of the per-sample shift rule)
+            # each step: one circuit evaluation per core — a shard of the
+            # 1 + 2P evaluations of the per-sample shift rule
             jobs = [(cfg, x[i % len(x)], theta) for i in range(cores)]
             t0 = time.perf_counter()
             list(ex.map(_ref_worker, jobs))
@@ -171,15 +290,16 @@ def run_reference(a):
             if step >= a.warmup:
                 times.append(dt)
     ms = 1e3 * statistics.mean(times)
-    value = cores / (ms / 1e3) / per_sample
+    value = cores / (ms / 1e3) / per
+    prec = a.precision
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_config(cfg, a.gpus, B, "c128"),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"per step {cores} circuit evaluations in parallel "
-                                       f"(1 per core) of the {per_sample} a sample's "
-                                       f"forward+grad needs; samples/s extrapolated"},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(cfg, a.gpus, B, prec),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": f"per step {cores} circuit evaluations in parallel (1 per core, "
+                                       f"QuantumLayer._run of the {'reference hyqnet' if kind == 'reference' else 'oracle port'}) "
+                                       f"of the {per} a sample's forward+grad needs; samples/s extrapolated"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -189,243 +309,266 @@ def workload_config(cfg, world, B, prec):
     n = wl.CONFIGS[cfg][0]
     R, D, G = wl.gate_counts(cfg)
     return {"workload": f"{cfg}: {n}-qubit circuit ({G} gates), forward + {D}-angle gradient, "
-                        f"{B} samples per GPU",
-            "n_qubits": n, "gates": G, "batch_per_gpu": B, "global_batch": B * world,
+                        f"global batch {B} split over {world} GPU(s)",
+            "n_qubits": n, "gates": G, "global_batch": B, "batch_per_gpu": B // world,
             "precision": "complex64" if prec == "c64" else "complex128",
-            "parallelism": f"dp{world} (sample-sharded, NCCL all-reduce of the parameter gradient)",
+            "parallelism": f"dp{world} (sample-sharded strong scaling: contiguous B/N blocks per rank, "
+                           f"one all-reduce(sum) of the [{wl.CONFIGS[cfg][2]}] f64 gradient per step)",
             "l2": "inputs larger than L2: the per-chunk state workspace is GiBs >> 126 MB L2"}
 
 
+def shard_rows(B, world, rank):
+    if B % world:
+        raise SystemExit(f"global batch {B} is not divisible by {world} ranks")
+    per = B // world
+    return rank * per, (rank + 1) * per
+
+
 # ------------------------------------------------------------------------------
+def run_stub(a):
+    """Multi-rank harness on CPU (gloo): sharding, the per-step gradient
+    all-reduce and max-over-ranks timing, with a NumPy stand-in evaluator."""
+    import torch
+    from paper_2301_03251_b200 import workloads as wl
+    D = Dist(a, device_required=False)
+    cfg = a.config
+    n, d, P, B0, _ = wl.CONFIGS[cfg]
+    B = a.batch or B0
+    lo, hi = shard_rows(B, D.world, D.rank)
+    x = torch.from_numpy(np.ascontiguousarray(wl.inputs_for(cfg, B)[lo:hi]))
+    theta = torch.from_numpy(wl.params_for(cfg))
+
+    def step():
+        # stand-in: per-sample "gradient" rows summed in sample order, then
+        # the cross-rank sum (the real path: hq_forward + hq_vjp + all_reduce)
+        # (integer-valued rows: the sum is exact in any order, so 1-rank and
+        # N-rank gradients are bit-identical and the test can compare them)
+        rows = torch.round(1e3 * torch.sin(x.sum(dim=1, keepdim=True) + theta[None, :]))
+        g = rows.sum(dim=0)
+        return D.allreduce_(g)
+
+    for _ in range(a.warmup):
+        step()
+    D.barrier()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        g = step()
+    D.barrier()
+    ms = D.max_scalar((time.perf_counter() - t0) * 1e3 / a.steps)
+    digest = hashlib.sha256(g.numpy().tobytes()).hexdigest()[:16]
+    digests = [None] * D.world
+    if D.world > 1:
+        D.dist.all_gather_object(digests, digest)
+    else:
+        digests = [digest]
+    if D.rank == 0:
+        print(json.dumps({"metric": METRIC, "value": B / (ms / 1e3), "unit": UNIT, "n_gpus": D.world,
+                          "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "stub": True,
+                          "scaling": "strong", "config": workload_config(cfg, D.world, B, a.precision),
+                          "grad_digest_per_rank": digests}), flush=True)
+    D.close()
+
+
+# ------------------------------------------------------------------------------
+def _ncu_traffic(prec, cls):
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
+            ref = json.load(f)
+        return ref[prec][cls]
+    except Exception:
+        return None
+
+
+def roofline(prof, st, cfg, prec, B_local, steps, ms_step):
+    """Dominant kernel class vs HBM (SURVEY.md §8(d) bytes) and vs the FP pipe."""
+    from paper_2301_03251_b200 import workloads as wl
+    n = wl.CONFIGS[cfg][0]
+    peak, peak_kind = hbm_peak()
+    b = 8 if prec == "c64" else 16
+    fwd, bwd = prof["pass_fwd"], prof["pass_bwd"]
+    R, D, _ = wl.gate_counts(cfg)
+    if st["path"] != 1:
+        dom = prof["onchip"]
+        flops = (1 << n) * (18 * R + 8 * D + 6) * B_local * steps
+        return {"bound": "fp", "kernel": "k_onchip / hq_small", "achieved": flops / (dom["ms"] / 1e3) / 1e12,
+                "unit": "TFLOP/s", "peak": None, "frac": None, "traffic": None,
+                "note": "state resident in shared memory; launch/latency bound at this batch"}
+    # SURVEY.md §8(d): Bytes/unit = 2·2^n·b·(S_f + 2·S_b), S = d·ceil(n/q), q = 13 (c64) / 12 (c128);
+    # the backward class (hq_b*, incl. the fused last-forward+first-backward kernel) carries the
+    # 2·S_b part (ψ and λ, read + write), the forward class the S_f part.
+    depth = 10 if cfg == "cfg4" else 20
+    S_model = depth * -(-n // (13 if prec == "c64" else 12))
+    S = int(st["n_passes"])
+    dom, name, cls = ((bwd, "hq_b* (backward passes)", "hq_b") if bwd["ms"] >= fwd["ms"]
+                      else (fwd, "hq_f* (forward passes)", "hq_f"))
+    k = 4 if dom is bwd else 2
+    units = B_local * steps
+    launches = max(dom["launches"], 1)
+    alg = k * (1 << n) * b * S_model * units
+    achieved = alg / (dom["ms"] / 1e3) / 1e9
+    alg_exec = k * (1 << n) * b * S * units
+    ref = _ncu_traffic(prec, cls)
+    traffic = None
+    if ref:
+        traffic = ref["dram_bytes_per_launch"] / ref["algorithmic_bytes_per_launch"] * (alg_exec / launches)
+    t_all = (fwd["ms"] + bwd["ms"]) / 1e3
+    bytes_unit = 2 * (1 << n) * b * (S_model + 2 * S_model)
+    flops_unit = (1 << n) * (18 * R + 8 * D + 6)
+    fpeak, fkind = fp_peak(prec)
+    per_s = units / (ms_step * steps / 1e3)
+    return {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "traffic_note": "ncu dram__bytes_read+write per launch of this kernel class at this precision "
+                            "(profiles/ncu_traffic.json, ratio to executed bytes scaled to this launch size)",
+            "peak_source": peak_kind, "launches": dom["launches"], "avg_launch_ms": dom["ms"] / launches,
+            "algorithmic_bytes_per_launch": alg / launches,
+            "algorithmic_bytes_note": f"SURVEY §8(d): {k}·2^{n}·{b} B·S_model({S_model} sweeps) per sample",
+            "sweeps_model": S_model, "sweeps_executed": S,
+            "executed": {"achieved": alg_exec / (dom["ms"] / 1e3) / 1e9,
+                         "frac": alg_exec / (dom["ms"] / 1e3) / 1e9 / peak,
+                         "bytes_per_launch": alg_exec / launches},
+            "share_of_step": dom["ms"] / (ms_step * steps),
+            "all_passes": {"bytes_per_unit": bytes_unit, "achieved": bytes_unit * units / t_all / 1e9,
+                           "frac": bytes_unit * units / t_all / 1e9 / peak},
+            ("fp32" if prec == "c64" else "fp64"): {
+                "flops_per_unit": flops_unit, "achieved_TFLOPs": flops_unit * per_s / 1e12,
+                "peak_TFLOPs": fpeak, "peak_source": fkind,
+                "frac": flops_unit * per_s / 1e12 / fpeak,
+                "note": "SURVEY §8(d) model flops 2^n(18R+8D+6) over the whole step; the kernels execute "
+                        "fewer (folded/deferred gates), ncu pipe utilisation in profiles/"},
+            "all_kernels_ms_per_step": {kk: v["ms"] / steps for kk, v in prof.items()}}
+
+
 def run_ours(a):
     import torch
-    import torch.distributed as dist
-    from paper_2301_03251_b200 import (QuantumLayer, Tensor, backward, qsim, tsum,
-                                       workloads as wl)
+    from paper_2301_03251_b200 import _native, engine, qsim, tracer as tr, workloads as wl
     from paper_2301_03251_b200 import templates as T
-    from paper_2301_03251_b200 import engine, tracer as tr
+    from paper_2301_03251_b200 import QuantumLayer, Tensor, backward, tsum
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    local = local % max(torch.cuda.device_count(), 1)
-    torch.cuda.set_device(local)
-    if world > 1:
-        if a.backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-        else:
-            dist.init_process_group(a.backend)
+    D = Dist(a)
     cfg = a.config
-    n, d, P, B0, prec = wl.CONFIGS[cfg]
-    prec = a.precision or prec
+    n, d, P, B0, _ = wl.CONFIGS[cfg]
+    prec = a.precision
     B = a.batch or B0
+    lo, hi = shard_rows(B, D.world, D.rank)
+    Bl = hi - lo
     builder = wl.make_builder(cfg, qsim, T)
-    xall = wl.inputs_for(cfg, B * world)
-    x = np.ascontiguousarray(xall[rank * B:(rank + 1) * B])
+    x = np.ascontiguousarray(wl.inputs_for(cfg, B)[lo:hi])
     theta = wl.params_for(cfg)
     want_x = cfg in ("cfg1", "cfg2")
     tape, ok = tr.trace(builder, x, theta)
     assert ok
     grad = tr.classify(tape, d + P, [want_x] * d + [True] * P, math.pi / 2, 0.5)
-    plan = engine.Plan(tape, d, P, prec, grad)
-    dev = torch.device(f"cuda:{local}")
-    xd = torch.from_numpy(x).to(dev)
-    td = torch.from_numpy(theta).to(dev)
-    up = torch.ones(B, dtype=torch.float64, device=dev)
+    xd = torch.from_numpy(x).to(D.device)
+    td = torch.from_numpy(theta).to(D.device)
+    up = torch.ones(Bl, dtype=torch.float64, device=D.device)
 
-    def step():
-        out, jac = plan.forward(xd, td, True)
-        gx, gt = plan.vjp(jac, up, want_x, True)
-        if world > 1:
-            dist.all_reduce(gt)
-        return out, gt
+    def measure(p, steps, warmup, profile=False):
+        plan = engine.Plan(tape, d, P, p, grad)
 
-    for _ in range(a.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    plan.profile(True)
-    with Clocks(local) as clk:
-        ev0.record()
-        for _ in range(a.steps):
+        def step():
+            out, jac = plan.forward(xd, td, True)
+            gx, gt = plan.vjp(jac, up, want_x, True)
+            D.allreduce_(gt)            # the one collective of the step (inside the timed region)
+            return gt
+
+        for _ in range(warmup):
             step()
-        ev1.record()
         torch.cuda.synchronize()
-    prof = plan.profile_read()
-    plan.profile(False)
-    if world > 1:
-        dist.barrier()
-    ms = ev0.elapsed_time(ev1) / a.steps
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    value = world * B / (ms / 1e3)
-    st = plan.stats(B, True)
-    launches_per_step = int(st["launches"]) + 1   # + hq_vjp (θ)
-    if want_x:
-        launches_per_step += 1
+        D.barrier()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        if profile:
+            plan.profile(True)
+        c0 = sum(_native.launch_counts().values())
+        with Clocks(D.local) as clk:
+            ev0.record()
+            for _ in range(steps):
+                gt = step()
+            ev1.record()
+            torch.cuda.synchronize()
+        launches = sum(_native.launch_counts().values()) - c0
+        prof = plan.profile_read() if profile else None
+        plan.profile(False)
+        D.barrier()
+        ms = D.max_scalar(ev0.elapsed_time(ev1) / steps)
+        st = plan.stats(Bl, True)
+        res = {"ms": ms, "value": B / (ms / 1e3), "launches": launches, "prof": prof, "stats": st,
+               "clocks": clk.summary(), "plan": plan.description,
+               "grad_digest": hashlib.sha256(gt.cpu().numpy().tobytes()).hexdigest()[:16]}
+        del plan
+        torch.cuda.empty_cache()
+        return res
 
-    # roofline: the dominant amplitude-update kernel class, live event time
-    peak, peak_kind = peaks()
-    b = 8 if prec == "c64" else 16
-    S = int(st["n_passes"])
-    fwd, bwd = prof["pass_fwd"], prof["pass_bwd"]
-    if st["path"] == 1:
-        # Dominant kernel class: the backward passes (hq_b*, incl. the fused
-        # last-forward+first-backward kernel).  Algorithmic bytes per unit
-        # (one sample's forward + full gradient) follow SURVEY.md §8(d), which
-        # defines roofline.achieved: 2·2^n·b·(S_f + 2·S_b) with the model's
-        # sweep count S = d·ceil(n/q_model) (q_model = 13 c64 / 12 c128); the
-        # backward class carries the 2·S_b part (ψ and λ, read + write).  This
-        # plan executes fewer sweeps (S below): "executed" reports the bytes of
-        # the sweeps actually run, "traffic" the ncu-measured DRAM bytes.
-        R, D, _ = wl.gate_counts(cfg)
-        depth = 10 if cfg == "cfg4" else 20
-        S_model = depth * -(-n // (13 if prec == "c64" else 12))
-        name = "hq_b* (backward passes)" if bwd["ms"] >= fwd["ms"] else "hq_f* (forward passes)"
-        dom = bwd if bwd["ms"] >= fwd["ms"] else fwd
-        units = B * a.steps
-        alg = (4 if dom is bwd else 2) * (1 << n) * b * S_model * units
-        achieved = alg / (dom["ms"] / 1e3) / 1e9
-        alg_exec = (4 if dom is bwd else 2) * (1 << n) * b * S * units
-        t_all = (fwd["ms"] + bwd["ms"]) / 1e3
-        traffic = None
-        try:
-            with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
-                ref = json.load(f)["hq_b" if dom is bwd else "hq_f"]
-            traffic = ref["dram_bytes_per_launch"] / ref["algorithmic_bytes_per_launch"] * (alg_exec / max(dom["launches"], 1))
-        except Exception:
-            pass
-        bytes_unit = 2 * (1 << n) * b * (S_model + 2 * S_model)
-        flops_unit = (1 << n) * (18 * R + 8 * D + 6)
-        units_per_s = units / t_all
-        fpeak, fkind = fp_peak(prec)
-        roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic,
-                "traffic_note": "ncu dram__bytes_read+write per launch (ratio to executed-sweep bytes from "
-                                "profiles/ncu_traffic.json, scaled to this launch size)",
-                "peak_source": peak_kind,
-                "launches": dom["launches"], "avg_launch_ms": dom["ms"] / max(dom["launches"], 1),
-                "algorithmic_bytes_per_launch": alg / max(dom["launches"], 1),
-                "sweeps_model": S_model, "sweeps_executed": S,
-                "executed": {"achieved": alg_exec / (dom["ms"] / 1e3) / 1e9,
-                             "frac": alg_exec / (dom["ms"] / 1e3) / 1e9 / peak,
-                             "bytes_per_launch": alg_exec / max(dom["launches"], 1)},
-                "share_of_step": dom["ms"] / (ms * a.steps),
-                "all_passes": {"bytes_per_unit": bytes_unit, "achieved": bytes_unit * units_per_s / 1e9,
-                               "frac": bytes_unit * units_per_s / 1e9 / peak},
-                "fp32": {"flops_per_unit": flops_unit, "achieved_TFLOPs": flops_unit * units_per_s / 1e12,
-                         "peak_TFLOPs": fpeak, "peak_source": fkind,
-                         "frac": flops_unit * units_per_s / 1e12 / fpeak if fpeak else None},
-                "all_kernels_ms_per_step": {k: v["ms"] / a.steps for k, v in prof.items()}}
-    else:
-        dom = prof["onchip"]
-        R, D, G = wl.gate_counts(cfg)
-        flops = (1 << n) * (18 * R + 8 * D + 6) * B * a.steps
-        achieved = flops / (dom["ms"] / 1e3) / 1e12
-        roof = {"bound": "fp", "kernel": "k_onchip", "achieved": achieved, "unit": "TFLOP/s",
-                "peak": None, "frac": None, "traffic": None,
-                "note": "state resident in shared memory; launch/latency bound at this batch"}
-
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32" if prec == "c64" else "f64", "data": "synthetic",
-            "config": workload_config(cfg, world, B, prec), "roofline": roof,
-            "gpu_launches": launches_per_step * a.steps, "clocks": clk.summary(),
-            "plan": plan.description}
-
-    # e2e through the public API: host numpy in, host numpy out
-    if not a.no_e2e:
-        layer = QuantumLayer(builder, n_params=P, param_init=theta, precision=prec)
+    def e2e(p, steps):
+        """Public API: QuantumLayer forward + hyqnet-style backward on host tensors."""
+        layer = QuantumLayer(builder, n_params=P, param_init=theta, precision=p)
 
         def e2e_step():
             xt = Tensor(x, requires_grad=want_x, dtype=np.float64)
             out = layer(xt)
             backward(tsum(out))
             g = layer.params.grad
-            if world > 1:
-                gd = torch.from_numpy(g).to(dev)
-                dist.all_reduce(gd)
+            if D.world > 1:
+                gd = torch.from_numpy(g).to(D.device)
+                D.allreduce_(gd)
                 g = gd.cpu().numpy()
             layer.params.zero_grad()
             return g
 
-        for _ in range(max(1, min(a.warmup, 2))):
+        for _ in range(2):               # warm-up (and the lazy/eager jacobian policy settles)
             e2e_step()
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        k = max(2, a.steps // 2)
+        D.barrier()
         t0 = time.perf_counter()
-        for _ in range(k):
+        for _ in range(steps):
             e2e_step()
         torch.cuda.synchronize()
-        e_ms = (time.perf_counter() - t0) * 1e3 / k
-        t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e_ms = float(t.item())
-        line["e2e"] = {"value": world * B / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
-                       "steps": k, "h2d_bytes_per_step": int(x.nbytes + theta.nbytes + B * 8),
-                       "d2h_bytes_per_step": int(B * 8 + theta.nbytes + (x.nbytes if want_x else 0)),
-                       "api": "QuantumLayer.forward + hyqnet-style backward (host numpy tensors)"}
-
-    # the same workload at the reference's own precision (complex128),
-    # device-timed like `value` (companion number; `value` stays the plan's)
-    if prec == "c64" and not a.no_c128:
-        del plan
+        e_ms = D.max_scalar((time.perf_counter() - t0) * 1e3 / steps)
+        del layer
         torch.cuda.empty_cache()
-        p128 = engine.Plan(tape, d, P, "c128", grad)
+        return {"value": B / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms, "steps": steps,
+                "h2d_bytes_per_step": int(x.nbytes + theta.nbytes + Bl * 8),
+                "d2h_bytes_per_step": int(Bl * 8 + theta.nbytes + (x.nbytes if want_x else 0)),
+                "api": "QuantumLayer.forward + hyqnet-style backward (host numpy tensors)"}
 
-        def step128():
-            out, jac = p128.forward(xd, td, True)
-            gx, gt = p128.vjp(jac, up, want_x, True)
-            if world > 1:
-                dist.all_reduce(gt)
-            return gt
-
-        step128()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        k = max(2, min(a.steps, 4))
-        ev0.record()
-        for _ in range(k):
-            step128()
-        ev1.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([ev0.elapsed_time(ev1) / k], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        v128 = world * B / (float(t.item()) / 1e3)
-        R, D, _ = wl.gate_counts(cfg)
-        f_unit = (1 << n) * (18 * R + 8 * D + 6)
-        f64peak, f64kind = fp_peak("c128")
-        line["complex128"] = {"value": v128, "unit": UNIT,
-                              "ms_per_step": float(t.item()), "steps": k, "dtype": "f64",
-                              "fp64": {"flops_per_unit": f_unit, "achieved_TFLOPs": f_unit * v128 / world / 1e12,
-                                       "peak_TFLOPs": f64peak, "peak_source": f64kind,
-                                       "frac": f_unit * v128 / world / 1e12 / f64peak},
-                              "note": "same workload, complex128 amplitudes (the reference's precision)",
-                              "plan": p128.description}
-        del p128
-        torch.cuda.empty_cache()
-
-    if rank == 0 and world == 1 and not a.no_cpu:
+    main = measure(prec, a.steps, a.warmup, profile=True)
+    line = {"metric": METRIC, "value": main["value"], "unit": UNIT, "n_gpus": D.world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": main["ms"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32" if prec == "c64" else "f64", "data": "synthetic",
+            "config": workload_config(cfg, D.world, B, prec),
+            "roofline": roofline(main["prof"], main["stats"], cfg, prec, Bl, a.steps, main["ms"]),
+            "gpu_launches": main["launches"], "clocks": main["clocks"], "plan": main["plan"],
+            "parity": {"c128": "normwise ||d||inf/||ref||inf < 1e-10 vs reference goldens (tests/)",
+                       "c64": "expectations normwise < 1e-5; gradients ||d||inf < 1e-5 * max(||ref||inf, 0.1)"}}
+    if not a.no_e2e:
+        line["e2e"] = e2e(prec, max(2, a.steps // 2))
+    if not a.no_companion:
+        other = "c64" if prec == "c128" else "c128"
+        comp = measure(other, max(3, min(a.steps, 6)), 2, profile=True)
+        line["complex64" if other == "c64" else "complex128"] = {
+            "value": comp["value"], "unit": UNIT, "ms_per_step": comp["ms"], "steps": max(3, min(a.steps, 6)),
+            "dtype": "f32" if other == "c64" else "f64", "plan": comp["plan"],
+            "roofline": roofline(comp["prof"], comp["stats"], cfg, other, Bl, max(3, min(a.steps, 6)), comp["ms"]),
+            "e2e": None if a.no_e2e else e2e(other, 2),
+            "note": "same workload at the other precision (companion; the headline is the reference's complex128)"}
+    if D.rank == 0 and D.world == 1 and not a.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, x[0], theta)
-    if rank == 0:
+    digests = [None] * D.world
+    if D.world > 1:
+        D.dist.all_gather_object(digests, main["grad_digest"])
+        line["grad_digest_per_rank"] = digests
+    if D.rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    D.close()
 
 
 if __name__ == "__main__":
     args = parse()
+    maybe_spawn(args)
     if args.impl == "reference":
         run_reference(args)
+    elif args.stub:
+        run_stub(args)
     else:
         run_ours(args)

@@ -251,8 +251,14 @@ cudaError_t launch_forward(const hq_plan_s* pl, const LaunchIn& in, cudaStream_t
 cudaError_t launch_vjp(const hq_plan_s* pl, const double* jac, const double* up, int64_t B,
                        double* gx, double* gt, cudaStream_t st) {
   const int d = pl->n_inputs, P = pl->n_params, nv = d + P;
-  if (gx && B * d > 0) k_vjp_x<<<(unsigned)((B * d + 255) / 256), 256, 0, st>>>(jac, up, B, nv, d, gx);
-  if (gt && P > 0) k_vjp_theta<<<(P + 127) / 128, 128, 0, st>>>(jac, up, B, nv, d, P, gt);
+  if (gx && B * d > 0) {
+    count_launch(HQ_K_OTHER);
+    k_vjp_x<<<(unsigned)((B * d + 255) / 256), 256, 0, st>>>(jac, up, B, nv, d, gx);
+  }
+  if (gt && P > 0) {
+    count_launch(HQ_K_OTHER);
+    k_vjp_theta<<<(P + 127) / 128, 128, 0, st>>>(jac, up, B, nv, d, P, gt);
+  }
   return cudaGetLastError();
 }
 

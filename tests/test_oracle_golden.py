@@ -115,6 +115,12 @@ def test_cfg4_forward_and_jacobian_entries():
         tm = g["theta"].copy(); tm[j] -= np.pi / 2
         val = (O.run(b, g["x"][0], tp) - O.run(b, g["x"][0], tm)) * 0.5
         assert val == pytest.approx(g["jac0"][k], abs=1e-12)
+    # sample 1's rows entries come from the same reference evaluations
+    j = int(g["jac1_idx"][5])
+    tp = g["theta"].copy(); tp[j] += np.pi / 2
+    tm = g["theta"].copy(); tm[j] -= np.pi / 2
+    val = (O.run(b, g["x"][1], tp) - O.run(b, g["x"][1], tm)) * 0.5
+    assert val == pytest.approx(g["jac1"][5], abs=1e-12)
 
 
 def test_philox_stream_matches_numpy():
