@@ -192,6 +192,40 @@ hq_status hq_noisy(hq_plan plan, const double* x, int64_t ldx, const double* the
                    double* out, double* jac, uint64_t* counts, void* workspace, size_t workspace_bytes,
                    void* stream);
 
+/* ---- amplitude-sharded execution ----------------
+ *
+ * A circuit too large for one GPU is split by amplitude: index bits >= L are
+ * the rank.  The host scheduler (shard.py) cuts the tape into local segments
+ * separated by global<->local qubit exchanges (NCCL all-to-all of contiguous
+ * chunks).  Each segment runs as a SEGMENT plan over the L local qubits:
+ * every pass in place on the caller's shard, no readout, no folding, no
+ * global-phase bookkeeping (phases common to all ranks are global phases).
+ * Replaces, for n > 24 (beyond the reference, qsim.py:17): simulate
+ * (qsim.py:179-191) and the df_p closure (qnn.py:145-153) of one circuit. */
+
+/* like hq_plan_create; grad_mode may only use HQ_GRAD_ZERO / HQ_GRAD_ADJOINT */
+hq_status hq_plan_create_segment(const hq_plan_desc* desc, hq_plan* out);
+size_t hq_seg_workspace_bytes(hq_plan plan, int64_t batch);
+/* psi: [batch, 2^n] amplitudes in the plan's precision (interleaved complex),
+ * updated in place: psi <- U_segment psi */
+hq_status hq_seg_forward(hq_plan plan, const double* x, int64_t ldx, const double* theta, int64_t batch,
+                         void* psi, void* workspace, size_t workspace_bytes, void* stream);
+/* adjoint sweep over the segment: psi <- U^-1 psi, lam <- U^† lam, and
+ * jac[b, v] (row stride n_inputs + n_params) = factor_v · 2 Re<lam|dG_v|psi>
+ * at each differentiated gate (0 for variables the segment does not touch);
+ * summed over segments and ranks this is the df_p row (qnn.py:145-153). */
+hq_status hq_seg_backward(hq_plan plan, const double* x, int64_t ldx, const double* theta, int64_t batch,
+                          void* psi, void* lam, double* jac, void* workspace, size_t workspace_bytes,
+                          void* stream);
+/* this rank's EXACT_PROB partial  e_out[0] = Σ_j w(j)|psi_j|^2  over one shard
+ * of 2^n_local amplitudes, w(j) = w0 + Σ_i wk[i]·bit(j, pos[i]) (pos/wk: host
+ * arrays; local measured qubits, 2^i weights; w0: the measured rank bits);
+ * fixed-order reduction; lam (optional) <- w·psi.  e_out is device memory. */
+size_t hq_shard_readout_workspace_bytes(void);
+hq_status hq_shard_readout(const void* psi, int32_t precision, int32_t n_local, const int32_t* pos,
+                           const double* wk, int32_t k, double w0, double* e_out, void* lam, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
 /* ---- introspection / measurement ---------------------------------------- */
 
 typedef struct {

@@ -22,7 +22,9 @@ KIND_CODE = {"H": 0, "X": 1, "Y": 2, "Z": 3, "RX": 4, "RY": 5, "RZ": 6, "CNOT": 
 EXPORTS = ("hq_abi_version", "hq_last_error", "hq_plan_create", "hq_plan_destroy",
            "hq_plan_describe", "hq_workspace_bytes", "hq_forward", "hq_vjp", "hq_state",
            "hq_stats", "hq_profile_enable", "hq_profile_read", "hq_sample_workspace_bytes", "hq_sample",
-           "hq_shot_uniforms", "hq_noisy_workspace_bytes", "hq_noisy", "hq_launch_counts")
+           "hq_shot_uniforms", "hq_noisy_workspace_bytes", "hq_noisy", "hq_launch_counts",
+           "hq_plan_create_segment", "hq_seg_workspace_bytes", "hq_seg_forward", "hq_seg_backward",
+           "hq_shard_readout_workspace_bytes", "hq_shard_readout")
 K_CLASSES = ("onchip", "pass_fwd", "pass_bwd", "other")
 
 
@@ -118,6 +120,20 @@ def lib():
     h.hq_noisy.restype = ctypes.c_int
     h.hq_launch_counts.argtypes = [_P]
     h.hq_launch_counts.restype = None
+    h.hq_plan_create_segment.argtypes = [ctypes.POINTER(HqPlanDesc), ctypes.POINTER(_P)]
+    h.hq_plan_create_segment.restype = ctypes.c_int
+    h.hq_seg_workspace_bytes.argtypes = [_P, ctypes.c_int64]
+    h.hq_seg_workspace_bytes.restype = ctypes.c_size_t
+    h.hq_seg_forward.argtypes = [_P, _P, ctypes.c_int64, _P, ctypes.c_int64, _P, _P, ctypes.c_size_t, _P]
+    h.hq_seg_forward.restype = ctypes.c_int
+    h.hq_seg_backward.argtypes = [_P, _P, ctypes.c_int64, _P, ctypes.c_int64, _P, _P, _P, _P, ctypes.c_size_t,
+                                  _P]
+    h.hq_seg_backward.restype = ctypes.c_int
+    h.hq_shard_readout_workspace_bytes.argtypes = []
+    h.hq_shard_readout_workspace_bytes.restype = ctypes.c_size_t
+    h.hq_shard_readout.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, _P, _P, ctypes.c_int32, ctypes.c_double,
+                                   _P, _P, _P, ctypes.c_size_t, _P]
+    h.hq_shard_readout.restype = ctypes.c_int
     if h.hq_abi_version() != 2:
         raise NativeError(f"libhq ABI {h.hq_abi_version()} != 2")
     _lib = h

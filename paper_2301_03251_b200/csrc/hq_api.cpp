@@ -643,11 +643,17 @@ const T* rebase(const T* rel, char* base) {
 
 // opts: kNoFold (no folded prefixes), kOnchipOk (small circuits may use the
 // shared-memory interpreter when the specialised kernels are unavailable)
-enum { kNoFold = 1, kPreferOnchip = 2, kSmallPasses = 4 };
+// kSegment: a segment plan of the amplitude-sharded executor (in-place passes
+// on a caller-owned state, no readout, no folding, specialised kernels only)
+enum { kNoFold = 1, kPreferOnchip = 2, kSmallPasses = 4, kSegment = 8 };
 static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts);
 
 extern "C" hq_status hq_plan_create(const hq_plan_desc* d, hq_plan* out) {
   return plan_create_impl(d, out, 0);
+}
+
+extern "C" hq_status hq_plan_create_segment(const hq_plan_desc* d, hq_plan* out) {
+  return plan_create_impl(d, out, kSegment | kNoFold);
 }
 
 namespace {
@@ -701,12 +707,18 @@ constexpr int kMaxFoldPerQubit = 32;
 }  // namespace
 
 static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts) {
-  const bool allow_fold = !(opts & kNoFold);
+  const bool seg = (opts & kSegment) != 0;
+  const bool allow_fold = !(opts & kNoFold) && !seg;
   if (!out) return fail(HQ_E_CONFIG, "null output");
   *out = nullptr;
   hq_status st = validate(d);
   if (st != HQ_OK) return st;
+  if (seg && d->n_preps > 0) return fail(HQ_E_CONFIG, "segment plans take no state loads");
+  if (seg && d->grad_mode)
+    for (int v = 0; v < d->n_inputs + d->n_params; ++v)
+      if (d->grad_mode[v] == HQ_GRAD_TWOPOINT) return fail(HQ_E_CONFIG, "segment plans differentiate by adjoint only");
   auto pl = new hq_plan_s();
+  pl->seg = seg;
   const int n = d->n_qubits;
   const int nvars = d->n_inputs + d->n_params;
   pl->n_qubits = n;
@@ -787,7 +799,7 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
   // forward+backward kernel, 3-7x faster than the interpreter (n = 9..13,
   // tools/onchip_vs_stream.py).  Without NVRTC the interpreter takes over.
   const int stream_min = reg_bits_for(d->precision) + 5;
-  pl->onchip = n <= onchip_max_qubits(d->precision) && !(force && force[0] == '1') &&
+  pl->onchip = !seg && n <= onchip_max_qubits(d->precision) && !(force && force[0] == '1') &&
                (n < stream_min || (opts & kPreferOnchip));
   std::vector<int32_t> pass_slots, pass_dlist, pass_local;
   if (pl->onchip) {
@@ -1027,6 +1039,10 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
   if (!pl->onchip) {
     std::string why;
     const hq_status js = hq::jit_build(pl, why);
+    if (js != HQ_OK && seg) {
+      delete pl;
+      return fail(js, "segment plans need the specialised kernels: " + why);
+    }
     if (js != HQ_OK && pl->reg_bits != reg_bits_for(d->precision)) {
       delete pl;
       return fail(HQ_E_CONFIG, "HQ_REG_BITS needs the specialised kernels: " + why);
@@ -1057,7 +1073,7 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
   }
 
   std::ostringstream os;
-  os << "n=" << n << " " << (d->precision == HQ_C64 ? "c64" : "c128") << " gates=" << gates.size()
+  os << (seg ? "segment " : "") << "n=" << n << " " << (d->precision == HQ_C64 ? "c64" : "c128") << " gates=" << gates.size()
      << " slots=" << d->n_slots << " preps=" << d->n_preps << " adjoint_slots=" << pl->n_adj
      << " twopoint_vars=" << pl->n_tp;
   if (pl->onchip) {
@@ -1316,6 +1332,49 @@ extern "C" hq_status hq_state(hq_plan pl, const double* x, int64_t ldx, const do
   char* w = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
   double* out = reinterpret_cast<double*>(w + L.scratch);
   return run(pl, x, ldx, theta, batch, 0, out, nullptr, state, init, init_rows, ws, ws_bytes, stream);
+}
+
+// ---- segment plans (amplitude-sharded executor) ----------------------------
+static int32_t seg_chunks(const hq_plan_s* pl, int64_t B) {
+  const int64_t n_tiles = 1ll << (pl->n_qubits - pl->tile_bits);
+  const int64_t want = (1184 + B - 1) / B;   // >= ~8 CTAs per SM per launch
+  int64_t nc = 16;
+  while (nc < want) nc <<= 1;
+  return (int32_t)std::min<int64_t>(nc, n_tiles);
+}
+
+extern "C" size_t hq_seg_workspace_bytes(hq_plan pl, int64_t batch) {
+  if (!pl || batch <= 0) return 256;
+  return align_up((size_t)batch * (size_t)std::max(pl->n_adj, 1) * (size_t)seg_chunks(pl, batch) * 8) + 512;
+}
+
+static hq_status seg_run(hq_plan pl, const double* x, int64_t ldx, const double* theta, int64_t batch, void* psi,
+                         void* lam, double* jac, void* ws, size_t ws_bytes, void* stream) {
+  if (!pl) return fail(HQ_E_CONFIG, "null plan");
+  if (!pl->seg) return fail(HQ_E_CONFIG, "not a segment plan (hq_plan_create_segment)");
+  if (batch < 0) return fail(HQ_E_DIMENSION, "negative batch");
+  if (batch == 0) return HQ_OK;
+  if (!psi) return fail(HQ_E_CONFIG, "null state");
+  if (pl->n_inputs > 0 && (!x || ldx < pl->n_inputs))
+    return fail(HQ_E_DIMENSION, "input rows narrower than the circuit's inputs");
+  if (pl->n_params > 0 && !theta) return fail(HQ_E_DIMENSION, "missing parameters");
+  if (ws_bytes < hq_seg_workspace_bytes(pl, batch)) return fail(HQ_E_CONFIG, "workspace too small");
+  double* dpart = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+  const cudaError_t e = hq::launch_segment(pl, x, ldx, theta, batch, psi, lam, dpart, seg_chunks(pl, batch), jac,
+                                           static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(HQ_E_CUDA, std::string("segment launch: ") + cudaGetErrorString(e));
+  return HQ_OK;
+}
+
+extern "C" hq_status hq_seg_forward(hq_plan pl, const double* x, int64_t ldx, const double* theta, int64_t batch,
+                                    void* psi, void* ws, size_t ws_bytes, void* stream) {
+  return seg_run(pl, x, ldx, theta, batch, psi, nullptr, nullptr, ws, ws_bytes, stream);
+}
+
+extern "C" hq_status hq_seg_backward(hq_plan pl, const double* x, int64_t ldx, const double* theta, int64_t batch,
+                                     void* psi, void* lam, double* jac, void* ws, size_t ws_bytes, void* stream) {
+  if (!lam || !jac) return fail(HQ_E_CONFIG, "null adjoint state / jacobian output");
+  return seg_run(pl, x, ldx, theta, batch, psi, lam, jac, ws, ws_bytes, stream);
 }
 
 extern "C" hq_status hq_vjp(hq_plan pl, const double* jac, const double* upstream, int64_t batch,

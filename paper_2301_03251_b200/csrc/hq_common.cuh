@@ -33,6 +33,8 @@ struct ProfScope {
 
 
 cudaError_t run_stream(const hq_plan_s* pl, const KArgs& a, const StreamWs& ws, cudaStream_t st);
+cudaError_t run_segment(const hq_plan_s* pl, const KArgs& a, void* psi, void* lam, int32_t n_chunks, bool backward,
+                        cudaStream_t st);
 
 // E per virtual sample from per-chunk readout partials (fixed order)
 __global__ void k_readout_fold(const double* __restrict__ rpart, int64_t v0, int64_t nv,

@@ -96,6 +96,7 @@ struct hq_plan_s {
   int32_t precision = HQ_C128;
   int32_t n_inputs = 0, n_params = 0;
   bool onchip = true;
+  bool seg = false;                       // segment plan (hq_plan_create_segment): in-place passes, no readout
   int32_t tile_bits = 0;                  // streaming path
   int32_t fixed_bits = 0;                 // low qubits always in the tile (contiguous HBM runs)
   int32_t reg_bits = 0;                   // amplitudes per thread = 2^reg_bits (register windows)

@@ -806,7 +806,10 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   const int tbits = g.Q - g.RB;
   const int n = pl->n_qubits;
   const int np = (int)pl->passes.size();
-  const bool first = pi == 0, last = pi == np - 1;
+  // segment plans (amplitude-sharded execution) apply every pass in place to a
+  // caller-owned state: no initial-state load, no readout / λ init, and the
+  // first backward pass un-applies all of its gates and stores ψ and λ
+  const bool first = pi == 0 && !pl->seg, last = pi == np - 1 && !pl->seg;
   // (a folding plan with folded gradients un-applies λ through the whole first
   // pass: its start is where k_fold_grad reads λ)
   const bool fold_end = bwd && first && pl->fold_grad;
@@ -1578,8 +1581,9 @@ hq_status jit_build(hq_plan_s* pl, std::string& err) {
   std::vector<Unit> units(np);
   std::string dump;
   for (int i = 0; i < np; ++i) {
+    const bool fused_i = i == np - 1 && !pl->seg;
     units[i].src = small ? head + gen_small(pl)
-                         : head + gen_pass(pl, i, 0) + gen_pass(pl, i, 1) + (i == np - 1 ? gen_pass(pl, i, 2) : "");
+                         : head + gen_pass(pl, i, 0) + gen_pass(pl, i, 1) + (fused_i ? gen_pass(pl, i, 2) : "");
     units[i].hash = fnv1a(units[i].src);
     if (std::getenv("HQ_JIT_DUMP")) dump += units[i].src;
   }
@@ -1663,11 +1667,11 @@ hq_status jit_build(hq_plan_s* pl, std::string& err) {
     const std::string s = std::to_string(i);
     if (cudaLibraryGetKernel(&pl->jit.fwd[i], lib, ("hq_f" + s).c_str()) != cudaSuccess ||
         cudaLibraryGetKernel(&pl->jit.bwd[i], lib, ("hq_b" + s).c_str()) != cudaSuccess ||
-        (i == np - 1 && cudaLibraryGetKernel(&pl->jit.fused, lib, ("hq_fb" + s).c_str()) != cudaSuccess)) {
+        (i == np - 1 && !pl->seg && cudaLibraryGetKernel(&pl->jit.fused, lib, ("hq_fb" + s).c_str()) != cudaSuccess)) {
       err = "generated kernel missing";
       return HQ_E_CUDA;
     }
-    for (int mode = 0; mode < (i == np - 1 ? 3 : 2); ++mode) {
+    for (int mode = 0; mode < (i == np - 1 && !pl->seg ? 3 : 2); ++mode) {
       const JitLayout L = jit_layout(pl, i, mode != 0, mode == 2);
       cudaKernel_t k = mode == 0 ? pl->jit.fwd[i] : (mode == 1 ? pl->jit.bwd[i] : pl->jit.fused);
       cudaError_t ce = cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);

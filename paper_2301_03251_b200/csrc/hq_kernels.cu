@@ -248,6 +248,29 @@ cudaError_t launch_forward(const hq_plan_s* pl, const LaunchIn& in, cudaStream_t
   return e;
 }
 
+cudaError_t launch_segment(const hq_plan_s* pl, const double* x, int64_t ldx, const double* theta, int64_t B,
+                           void* psi, void* lam, double* dpart, int32_t n_chunks, double* jac, cudaStream_t st) {
+  KArgs a{};
+  a.p = pl->dev;
+  a.x = x;
+  a.ldx = ldx;
+  a.theta = theta;
+  a.B = B;
+  a.V = B;
+  a.dpart = dpart;
+  a.n_parts = n_chunks;
+  a.want_adj = lam != nullptr;
+  a.prep_off = pl->d_prep_off;
+  cudaError_t e = run_segment(pl, a, psi, lam, n_chunks, lam != nullptr, st);
+  if (e != cudaSuccess || !lam || !jac) return e;
+  const int64_t tot = B * pl->dev.n_vars;
+  if (tot > 0) {
+    ProfScope ps(pl, st, HQ_K_OTHER, (double)tot * 8.0);
+    k_jac<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->dev, B, dpart, n_chunks, nullptr, jac);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_vjp(const hq_plan_s* pl, const double* jac, const double* up, int64_t B,
                        double* gx, double* gt, cudaStream_t st) {
   const int d = pl->n_inputs, P = pl->n_params, nv = d + P;

@@ -40,6 +40,8 @@ size_t onchip_smem_bytes(const hq_plan_s* pl);
 size_t stream_smem_bytes(const hq_plan_s* pl, int pass, bool bwd);   // generic window kernels
 int onchip_parts(const hq_plan_s* pl);
 cudaError_t launch_forward(const hq_plan_s* pl, const LaunchIn& in, cudaStream_t st);
+cudaError_t launch_segment(const hq_plan_s* pl, const double* x, int64_t ldx, const double* theta, int64_t B,
+                           void* psi, void* lam, double* dpart, int32_t n_chunks, double* jac, cudaStream_t st);
 cudaError_t launch_vjp(const hq_plan_s* pl, const double* jac, const double* up, int64_t B,
                        double* gx, double* gt, cudaStream_t st);
 

@@ -622,4 +622,34 @@ cudaError_t run_stream(const hq_plan_s* pl, const KArgs& a, const StreamWs& ws, 
   return pl->precision == HQ_C64 ? run_stream_t<float>(pl, a, ws, st) : run_stream_t<double>(pl, a, ws, st);
 }
 
+// Segment plans (amplitude-sharded execution): every pass in place on the
+// caller's state rows psi [B, 2^n] (and λ rows for the backward direction).
+// Forward: passes 0..np-1; backward: passes np-1..0 un-applying ψ, applying
+// G† to λ and writing per-CTA derivative partials into a.dpart.
+cudaError_t run_segment(const hq_plan_s* pl, const KArgs& a, void* psi, void* lam, int32_t n_chunks, bool backward,
+                        cudaStream_t st) {
+  const int n = pl->n_qubits;
+  const int64_t n_tiles = 1ll << (n - pl->tile_bits);
+  const int tpc = (int)(n_tiles / n_chunks);
+  const int np = (int)pl->passes.size();
+  const double vec = (double)a.B * (double)(pl->precision == HQ_C64 ? 8 : 16) * (double)(1ll << n);
+  SArgs sa;
+  sa.v0 = 0;
+  sa.nv = a.B;
+  sa.n_chunks = n_chunks;
+  sa.tpc = tpc;
+  sa.psi = psi;
+  sa.lam = backward ? lam : nullptr;
+  sa.rpart = nullptr;
+  for (int k = 0; k < np; ++k) {
+    const int i = backward ? np - 1 - k : k;
+    sa.ps = wpass(pl, i);
+    JPass jp = jpass(pl, i, sa);   // psi_out = psi: in place
+    ProfScope prof(pl, st, backward ? HQ_K_PASS_BWD : HQ_K_PASS_FWD, vec * (backward ? 4.0 : 2.0));
+    cudaError_t e = jit_launch_pass(pl, i, backward ? 1 : 0, a, jp, (unsigned)(a.B * n_chunks), st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
+}
+
 }  // namespace hq

@@ -51,7 +51,7 @@ class Plan:
     """One immutable device plan for a tape + gradient spec + precision."""
 
     def __init__(self, tape: tr.Tape, n_inputs: int, n_params: int, precision: str = "c128",
-                 grad=None, shift: float = math.pi / 2, grad_scale: float = 0.5):
+                 grad=None, shift: float = math.pi / 2, grad_scale: float = 0.5, segment: bool = False):
         if precision not in _PREC:
             raise ConfigError(f"precision must be c64 or c128, got {precision!r}")
         L = nat.lib()
@@ -117,7 +117,9 @@ class Plan:
             self.grad_mode = np.zeros(self.n_vars, np.int32)
         d.shift, d.grad_scale = float(shift), float(grad_scale)
         h = ctypes.c_void_p()
-        nat.check(L.hq_plan_create(ctypes.byref(d), ctypes.byref(h)), "plan")
+        self.segment = bool(segment)
+        create = L.hq_plan_create_segment if segment else L.hq_plan_create
+        nat.check(create(ctypes.byref(d), ctypes.byref(h)), "plan")
         self._h = h
         self._lib = L
         self.description = L.hq_plan_describe(h).decode()
@@ -203,6 +205,45 @@ class Plan:
                                          ws.numel(), st), "state")
         return st_out
 
+
+    # -- segment plans (amplitude-sharded execution, shard.py) -------------------
+    def _seg_ws(self, B):
+        torch = _torch()
+        n = int(self._lib.hq_seg_workspace_bytes(self._h, int(B)))
+        return torch.empty(max(n, 256), dtype=torch.uint8, device=f"cuda:{self.device}")
+
+    def _seg_check(self, psi, B):
+        amp = 16 if self.precision in ("c128", "complex128") else 8
+        if not psi.is_contiguous() or psi.numel() * psi.element_size() != B * amp << self.n_qubits:
+            raise DimensionError(f"state rows must be contiguous [{B}, 2^{self.n_qubits}] amplitudes")
+
+    def seg_forward(self, x, theta, psi):
+        """psi (cuda, [B, 2^n] amplitudes of the plan's precision) <- U psi, in place."""
+        if not self.segment:
+            raise ConfigError("seg_forward needs a segment plan")
+        B = int(x.shape[0])
+        self._seg_check(psi, B)
+        st = self._on_device(x, theta, psi)
+        ws = self._seg_ws(B)
+        with _torch().cuda.device(self.device):
+            nat.check(self._lib.hq_seg_forward(self._h, _ptr(x), int(x.stride(0)), _ptr(theta), B, _ptr(psi),
+                                               _ptr(ws), ws.numel(), st), "seg_forward")
+
+    def seg_backward(self, x, theta, psi, lam):
+        """psi <- U^-1 psi, lam <- U^† lam in place; -> jac [B, n_vars] (this segment's dots)."""
+        if not self.segment:
+            raise ConfigError("seg_backward needs a segment plan")
+        torch = _torch()
+        B = int(x.shape[0])
+        self._seg_check(psi, B)
+        self._seg_check(lam, B)
+        st = self._on_device(x, theta, psi, lam)
+        jac = torch.empty((B, self.n_vars), dtype=torch.float64, device=f"cuda:{self.device}")
+        ws = self._seg_ws(B)
+        with _torch().cuda.device(self.device):
+            nat.check(self._lib.hq_seg_backward(self._h, _ptr(x), int(x.stride(0)), _ptr(theta), B, _ptr(psi),
+                                                _ptr(lam), _ptr(jac), _ptr(ws), ws.numel(), st), "seg_backward")
+        return jac
 
     def noisy(self, x, theta, sites, shots: int, seed: int, want_jac: bool, want_counts: bool = False):
         """NOISY trajectories (hq_noisy): -> (E [B], jac [B, nv] | None, counts [B, 2^m] | None)."""
@@ -473,6 +514,23 @@ def run_per_sample(builder, xd, pd, want_x, want_p, precision, shift, grad_scale
 
 # ------------------------------------------------------------------------------
 # SHOT_SAMPLING (qsim.py:222-248): device sampling of final states
+def shard_readout(psi, n_local: int, precision: str, pos, wk, w0: float, lam=None):
+    """This rank's EXACT_PROB partial Σ_j w(j)|psi_j|² (device f64 [1]) and,
+    optionally, lam <- w·psi (hq_shard_readout)."""
+    torch = _torch()
+    L = nat.lib()
+    k = len(pos)
+    pa = (ctypes.c_int32 * max(k, 1))(*[int(p) for p in pos])
+    wa = (ctypes.c_double * max(k, 1))(*[float(w) for w in wk])
+    e = torch.empty(1, dtype=torch.float64, device=psi.device)
+    ws = torch.empty(int(L.hq_shard_readout_workspace_bytes()), dtype=torch.uint8, device=psi.device)
+    with torch.cuda.device(psi.device):
+        nat.check(L.hq_shard_readout(_ptr(psi), _PREC[precision], int(n_local), pa, wa, k, float(w0), _ptr(e),
+                                     _ptr(lam), _ptr(ws), ws.numel(),
+                                     torch.cuda.current_stream(psi.device).cuda_stream), "shard_readout")
+    return e
+
+
 def sample_states(states, n_qubits: int, measured, shots: int, seed: int, want_counts: bool = False):
     """states: cuda f64 [rows, 2^n, 2] -> (expectation [rows] cuda, counts [rows, 2^m] | None)."""
     torch = _torch()

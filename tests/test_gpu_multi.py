@@ -1,43 +1,91 @@
-"""GPU side of the multi-GPU layer on ONE device: amplitude sharding with
-virtual ranks whose local segments run through the sm_100a plans (the
-exchange is the host permutation of shard.swap_exchange), checked against
-the oracle; batch sharding through the same evaluator the ranks use."""
+"""GPU side of the multi-GPU layer on ONE device.
+
+Amplitude sharding: every rank's local segments run as segment plans
+(hq_plan_create_segment / hq_seg_forward / hq_seg_backward /
+hq_shard_readout) on device shards; ranks are virtual (rows of one tensor,
+exchanged by the in-place block swap that stands in for the NCCL all-to-all —
+one GPU never runs ranks that wait on each other).  Checked against the CPU
+oracle: E, the full adjoint gradient and the final state.  Batch sharding:
+the evaluator the ranks use."""
+
+import math
 
 import numpy as np
 import pytest
 
+from conftest import normwise_error, parity_log
 from oracle import hq_oracle as O
 from paper_2301_03251_b200 import dist as D
 from paper_2301_03251_b200 import shard as S
 from paper_2301_03251_b200 import workloads as wl
+from shard_numpy import hea_builder, oracle_reference, random_param_builder, same_up_to_phase, sharded
 
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("n,g", [(8, 2), (11, 3), (15, 1)])
-def test_amplitude_sharding_gpu_local_segments(n, g):
-    rng = np.random.default_rng(n)
-    kinds = ["H", "X", "Y", "Z", "RX", "RY", "RZ", "CNOT", "CZ", "CR", "SWAP"]
-    ops = []
-    for _ in range(60):
-        k = kinds[rng.integers(len(kinds))]
-        if k in ("CNOT", "CZ", "CR", "SWAP"):
-            a, b = rng.choice(n, 2, replace=False)
-            ops.append((k, (int(a), int(b)), float(rng.uniform(-6, 6)) if k == "CR" else None))
-        else:
-            ops.append((k, (int(rng.integers(n)),), float(rng.uniform(-6, 6)) if k[0] == "R" else None))
-    sch = S.schedule(n, g, ops, [0, n - 1])
-    shards, E = S.run_virtual(sch, S.gpu_apply_local(n - g))
-    full = O.Circuit(n)
-    for kind, t, a in ops:
-        full.add(O.Op(kind, t, a))
-    full.measure(0, n - 1)
-    np.testing.assert_allclose(S.gather_state(shards, n - g, sch.final_layout), O.simulate(full), atol=1e-11)
-    assert E == pytest.approx(O.expectation(full), abs=1e-11)
+@pytest.mark.parametrize("n,g,seed", [(10, 1, 0), (12, 2, 1), (12, 3, 2), (14, 3, 3), (16, 2, 4)])
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+def test_amplitude_sharding_segment_plans_vs_oracle(n, g, seed, prec):
+    import torch
+    b, P = random_param_builder(n, 120, seed)
+    theta = np.random.default_rng(seed).uniform(-3, 3, P)
+    sc = sharded(b, P, theta, g, prec)
+    ex = S.GpuExecutor(torch.device("cuda"))
+    E, grad, _ = S.run_virtual(sc, theta, torch.device("cuda"), ex=ex)
+    E0, g0, psi0 = oracle_reference(b, theta)
+    tol = 1e-10 if prec == "c128" else 1e-5
+    parity_log(f"shard.n{n}g{g}.E:{prec}", normwise=abs(E - E0) / max(abs(E0), 1.0))
+    parity_log(f"shard.n{n}g{g}.grad:{prec}", normwise=normwise_error(grad, g0, floor=1.0))
+    assert abs(E - E0) < tol * max(abs(E0), 1.0)
+    assert normwise_error(grad, g0, floor=1.0) < tol
+    _, _, sh = S.run_virtual(sc, theta, torch.device("cuda"), want_grad=False, ex=ex)
+    got = S.gather_state(sh.cpu().numpy().astype(np.complex128), sc.L, sc.sched.final_layout)
+    same_up_to_phase(got, psi0, 1e-11 if prec == "c128" else 2e-6)
+
+
+@pytest.mark.parametrize("n", [14, 18])
+def test_cfg5_shape_sharded_forward_and_adjoint(n):
+    """cfg5's layer structure (depth 20, g = 3) on segment plans vs the oracle."""
+    import torch
+    b, P = hea_builder(n, 20 if n <= 14 else 6)
+    theta = np.random.default_rng(n).uniform(0, 2 * math.pi, P)
+    sc = sharded(b, P, theta, 3)
+    E, grad, _ = S.run_virtual(sc, theta, torch.device("cuda"))
+    E0, g0, _ = oracle_reference(b, theta)
+    assert abs(E - E0) < 1e-10
+    assert normwise_error(grad, g0) < 1e-10
+
+
+def test_sharded_matches_unsharded_plan_at_full_depth():
+    """n = 20, depth 20 (cfg5's shape at 20 qubits): the sharded forward + adjoint
+    against the single-GPU plan of the same tape (E and all 800 derivatives)."""
+    import torch
+    from paper_2301_03251_b200 import engine, tracer as tr
+    b, P = hea_builder(20, 20)
+    theta = wl.params_for("cfg5")[:P]
+    sc = sharded(b, P, theta, 3)
+    E, grad, _ = S.run_virtual(sc, theta, torch.device("cuda"))
+    tape = sc.tape
+    plan = engine.Plan(tape, 0, P, "c128", tr.classify(tape, P, [True] * P, math.pi / 2, 0.5))
+    out, jac = plan.forward(torch.zeros((1, 1), dtype=torch.float64, device="cuda"),
+                            torch.tensor(theta, device="cuda"), True)
+    assert abs(E - float(out[0])) < 1e-12
+    assert normwise_error(grad, jac[0].cpu().numpy()) < 1e-10
+
+
+def test_segment_plan_errors():
+    import torch
+    from paper_2301_03251_b200 import ConfigError, engine, qsim, tracer as tr
+    b, P = hea_builder(10, 2)
+    tape, _ = tr.trace(b, np.zeros((1, 0)), np.zeros(P))
+    plan = engine.Plan(tape, 0, P, "c128")
+    with pytest.raises(ConfigError):
+        plan.seg_forward(torch.zeros((1, 1), dtype=torch.float64, device="cuda"),
+                         torch.zeros(P, dtype=torch.float64, device="cuda"),
+                         torch.zeros(1 << 10, dtype=torch.complex128, device="cuda"))
 
 
 def test_batch_sharding_evaluator_on_gpu():
-    import math
     import torch
     from paper_2301_03251_b200 import engine, qsim, templates as T, tracer as tr
     b = wl.make_builder("cfg1", qsim, T)
@@ -50,38 +98,3 @@ def test_batch_sharding_evaluator_on_gpu():
     np.testing.assert_allclose(out, o, atol=1e-12)
     np.testing.assert_allclose(gx, gxo, atol=1e-12)
     np.testing.assert_allclose(gp, gpo, atol=1e-12)
-
-
-@pytest.mark.parametrize("n,g", [(10, 2), (14, 3)])
-def test_amplitude_sharding_device_resident_executor(n, g):
-    """The executor ``run_nccl`` uses on GPUs (``gpu_apply_local_dev``: shards
-    stay complex128 CUDA tensors, no host round trip), driven through the
-    virtual-rank schedule, against the oracle."""
-    import torch
-    rng = np.random.default_rng(100 + n)
-    kinds = ["H", "X", "Y", "Z", "RX", "RY", "RZ", "CNOT", "CZ", "CR", "SWAP"]
-    ops = []
-    for _ in range(80):
-        k = kinds[rng.integers(len(kinds))]
-        if k in ("CNOT", "CZ", "CR", "SWAP"):
-            a, b = rng.choice(n, 2, replace=False)
-            ops.append((k, (int(a), int(b)), float(rng.uniform(-6, 6)) if k == "CR" else None))
-        else:
-            ops.append((k, (int(rng.integers(n)),), float(rng.uniform(-6, 6)) if k[0] == "R" else None))
-    sch = S.schedule(n, g, ops, [1, n - 2])
-    dev_exec = S.gpu_apply_local_dev(n - g)
-    calls = []
-
-    def apply_local(shard, lops):
-        out = dev_exec(torch.from_numpy(shard).to("cuda"), lops)
-        assert out.is_cuda and out.dtype == torch.complex128
-        calls.append(1)
-        return out.cpu().numpy()
-    shards, E = S.run_virtual(sch, apply_local)
-    assert calls
-    full = O.Circuit(n)
-    for kind, t, a in ops:
-        full.add(O.Op(kind, t, a))
-    full.measure(1, n - 2)
-    np.testing.assert_allclose(S.gather_state(shards, n - g, sch.final_layout), O.simulate(full), atol=1e-11)
-    assert E == pytest.approx(O.expectation(full), abs=1e-11)

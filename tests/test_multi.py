@@ -74,116 +74,107 @@ def test_batch_sharding_gloo_world2_matches_single_process():
 
 
 # ---------------------------------------------------------------------------
-def _random_ops(n, depth, rng):
-    kinds = ["H", "X", "Y", "Z", "RX", "RY", "RZ", "CNOT", "CZ", "CR", "SWAP"]
-    ops = []
-    for _ in range(depth):
-        k = kinds[rng.integers(len(kinds))]
-        if k in ("CNOT", "CZ", "CR", "SWAP"):
-            a, b = rng.choice(n, 2, replace=False)
-            ops.append((k, (int(a), int(b)), float(rng.uniform(-6, 6)) if k == "CR" else None))
-        else:
-            ops.append((k, (int(rng.integers(n)),), float(rng.uniform(-6, 6)) if k[0] == "R" else None))
-    return ops
+# amplitude sharding (shard.py): the driver with a NumPy segment executor
+from shard_numpy import (NumpyExecutor, hea_builder, oracle_reference, random_param_builder,  # noqa: E402
+                         same_up_to_phase, sharded)
 
 
-def _oracle_apply(L):
-    def apply_local(shard, ops):
-        c = O.Circuit(L)
-        for kind, t, a in ops:
-            c.add(O.Op(kind, t, a))
-        return O.simulate(c, initial=shard)
-    return apply_local
+@pytest.mark.parametrize("n,g,seed", [(6, 1, 0), (8, 2, 1), (9, 3, 2), (10, 3, 3), (10, 2, 4)])
+def test_amplitude_sharding_virtual_ranks_match_oracle(n, g, seed):
+    """E, the full adjoint gradient and the final state of random circuits
+    (all 11 gate kinds) vs the oracle, ranks simulated in one process."""
+    import torch
+    b, P = random_param_builder(n, 90, seed)
+    theta = np.random.default_rng(seed).uniform(-3, 3, P)
+    sc = sharded(b, P, theta, g)
+    E, grad, shards = S.run_virtual(sc, theta, torch.device("cpu"), ex=NumpyExecutor())
+    E0, g0, psi0 = oracle_reference(b, theta)
+    assert E == pytest.approx(E0, abs=1e-12)
+    np.testing.assert_allclose(grad, g0, atol=1e-12)
+    # forward-only run: the final state, gathered through the final layout
+    _, _, sh = S.run_virtual(sc, theta, torch.device("cpu"), want_grad=False, ex=NumpyExecutor())
+    same_up_to_phase(S.gather_state(sh.numpy(), sc.L, sc.sched.final_layout), psi0, 1e-12)
 
 
-@pytest.mark.parametrize("n,g", [(5, 1), (7, 2), (8, 3), (10, 3)])
-def test_amplitude_sharding_virtual_ranks_match_full_state(n, g):
-    rng = np.random.default_rng(n * 10 + g)
-    for trial in range(3):
-        ops = _random_ops(n, 80, rng)
-        measured = [int(q) for q in rng.choice(n, 3, replace=False)]
-        sch = S.schedule(n, g, ops, measured)
-        shards, E = S.run_virtual(sch, _oracle_apply(n - g))
-        full = O.Circuit(n)
-        for kind, t, a in ops:
-            full.add(O.Op(kind, t, a))
-        full.measure(*measured)
-        want = O.simulate(full)
-        got = S.gather_state(shards, n - g, sch.final_layout)
-        np.testing.assert_allclose(got, want, atol=1e-12)
-        assert E == pytest.approx(O.expectation(full), abs=1e-12)
-        assert any(s[0] == "swap" for s in sch.steps) or g == 0
+def test_schedule_invariants():
+    """Every op lands in exactly one segment (or is a dropped trailing global
+    diagonal), segments only touch local positions after resolution, and the
+    SWAPs that stage victims are the only additions."""
+    b, P = random_param_builder(10, 200, 7)
+    sc = sharded(b, P, np.zeros(P), 3)
+    n_ops = len(sc.tape.ops)
+    placed = sum(1 for seg in sc.sched.segments for op in seg if not (op[0] == "SWAP" and op[2] == -1
+                                                                      and op not in sc.tape.ops))
+    assert placed + sc.sched.dropped >= n_ops - sum(1 for op in sc.tape.ops if op[0] == "SWAP")
+    for i in range(len(sc.sched.segments)):
+        for r in range(sc.world):
+            for kind, t, _ in sc.segment(i, r)[0].ops:
+                assert all(0 <= q < sc.L for q in t)
 
 
-def test_cfg5_shape_schedule_swap_count_bounded():
-    # the cfg5 layer structure at a small size: swaps stay O(layers)
-    n, g, depth = 12, 3, 6
-    th = np.random.default_rng(1).uniform(0, 2 * math.pi, depth * 2 * n)
-    ops, k = [], 0
-    for _ in range(depth):
-        for q in range(n):
-            ops.append(("RY", (q,), th[k])); ops.append(("RZ", (q,), th[k + 1])); k += 2
-        for q in range(n - 1):
-            ops.append(("CNOT", (q, q + 1), None))
-    sch = S.schedule(n, g, ops, [0])
-    n_swaps = sum(1 for s in sch.steps if s[0] == "swap")
-    assert n_swaps <= 2 * (depth * g + g)   # lower bound: g per layer
-    shards, E = S.run_virtual(sch, _oracle_apply(n - g))
-    c = O.Circuit(n)
-    for kind, t, a in ops:
-        c.add(O.Op(kind, t, a))
-    c.measure(0)
-    assert E == pytest.approx(O.expectation(c), abs=1e-12)
+@pytest.mark.parametrize("n,most", [(12, 5), (16, 3), (20, 3), (28, 1), (32, 1)])
+def test_cfg5_shape_exchange_count(n, most):
+    """cfg5's layer structure: the frontier runs ahead of the exchange as a
+    staircase, so at n = 32 the whole depth-20 forward needs ONE all-to-all
+    (the adjoint replays it) instead of one per layer."""
+    b, P = hea_builder(n, 20)
+    sc = sharded(b, P, np.zeros(P), 3)
+    assert 1 <= sc.sched.exchanges <= most
+    assert sc.stats()["exchange_bytes_per_gpu_each_way"] == 7 / 8 * 16 * 2 ** (n - 3)
+
+
+def test_cfg5_shape_small_matches_oracle():
+    import torch
+    b, P = hea_builder(11, 6)
+    theta = np.random.default_rng(5).uniform(0, 2 * math.pi, P)
+    sc = sharded(b, P, theta, 3)
+    E, grad, _ = S.run_virtual(sc, theta, torch.device("cpu"), ex=NumpyExecutor())
+    E0, g0, _ = oracle_reference(b, theta)
+    assert E == pytest.approx(E0, abs=1e-12)
+    np.testing.assert_allclose(grad, g0, atol=1e-12)
 
 
 def _shard_worker(rank, world, port, n, seed, q):
+    import sys
     import torch
     import torch.distributed as dist
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from shard_numpy import NumpyExecutor as NE, random_param_builder as rpb, sharded as shd
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         g = world.bit_length() - 1
-        rng = np.random.default_rng(seed)
-        ops = _random_ops(n, 60, rng)
-        measured = [int(x) for x in rng.choice(n, 2, replace=False)]
-        sch = S.schedule(n, g, ops, measured)
-        L = n - g
-        oracle_apply = _oracle_apply(L)
-
-        def apply_local_dev(shard, lops):   # CPU executor standing in for the GPU plan
-            out = oracle_apply(shard.numpy(), lops)
-            return torch.from_numpy(np.ascontiguousarray(out))
-        shard, E = S.run_nccl(sch, apply_local_dev, rank, world, torch.device("cpu"))
-        q.put((rank, shard.numpy(), E, sch.final_layout))
+        b, P = rpb(n, 90, seed)
+        theta = np.random.default_rng(seed).uniform(-3, 3, P)
+        sc = shd(b, P, theta, g)
+        E, grad, shard = S.run_nccl(sc, theta, rank, world, torch.device("cpu"), ex=NE())
+        _, _, shard_f = S.run_nccl(sc, theta, rank, world, torch.device("cpu"), want_grad=False, ex=NE())
+        q.put((rank, E, grad, shard_f.numpy().copy(), sc.sched.final_layout))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_amplitude_sharding_real_processes_gloo(world):
-    # run_nccl's exchange path (pairwise isend/irecv of half shards, per-rank
-    # phases, all-reduced readout) with real processes over gloo
+    """run_nccl with real processes over gloo: all-to-all exchanges on both ψ
+    and λ, the all-reduced readout and gradient, vs the oracle."""
     import torch.multiprocessing as mp
-    n, seed = 7, 11 + world
+    n, seed = 10, 11 + world
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29600 + (os.getpid() % 500) + world
     procs = [ctx.Process(target=_shard_worker, args=(r, world, port, n, seed, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted([q.get(timeout=300) for _ in procs], key=lambda t: t[0])
+    res = sorted([q.get(timeout=600) for _ in procs], key=lambda t: t[0])
     for p in procs:
         p.join(timeout=60)
-    rng = np.random.default_rng(seed)
-    ops = _random_ops(n, 60, rng)
-    measured = [int(x) for x in rng.choice(n, 2, replace=False)]
-    full = O.Circuit(n)
-    for kind, t, a in ops:
-        full.add(O.Op(kind, t, a))
-    full.measure(*measured)
-    want = O.simulate(full)
+    b, P = random_param_builder(n, 90, seed)
+    theta = np.random.default_rng(seed).uniform(-3, 3, P)
+    E0, g0, psi0 = oracle_reference(b, theta)
+    for _, E, grad, _, _ in res:
+        assert E == pytest.approx(E0, abs=1e-12)
+        np.testing.assert_allclose(grad, g0, atol=1e-12)
+    np.testing.assert_array_equal(res[0][2], res[-1][2])          # identical on every rank
     L = n - (world.bit_length() - 1)
-    got = S.gather_state([r[1] for r in res], L, res[0][3])
-    np.testing.assert_allclose(got, want, atol=1e-12)
-    for r in res:
-        assert r[2] == pytest.approx(O.expectation(full), abs=1e-12)
+    same_up_to_phase(S.gather_state([r[3] for r in res], L, res[0][4]), psi0, 1e-12)
