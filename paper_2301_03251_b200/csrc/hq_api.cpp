@@ -488,6 +488,31 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
   // bit of a bank class out of the thread bits are skipped.
   const char* wg = std::getenv("HQ_WIN_GREEDY");
   const bool lookahead = !(wg && wg[0] == '1');
+  // Shuffle transitions (generator: hq_jit.cpp): a window whose register bits
+  // differ from the previous window's only by qubits that were LANE bits there
+  // is reached with warp shuffles (each swapped bit moves half of a thread's
+  // amplitudes to the partner lane; no shared-memory round trip, no barrier).
+  // The lookahead prefers such register sets by kShflBonus score points
+  // (= half an admitted op each).
+  const bool shfl = hq::shfl_enabled();
+  int shfl_bonus = 3;
+  if (const char* e = std::getenv("HQ_SHFL_BONUS")) shfl_bonus = std::atoi(e);
+  std::vector<int> pR, pS;            // previous window's register / thread bits
+  bool have_prev = false;
+  const int n_lanes = std::min(5, q - RB);
+  auto lane_mask_prev = [&]() {
+    uint32_t m = 0;
+    for (int s2 = 0; s2 < n_lanes && s2 < (int)pS.size(); ++s2) m |= 1u << pS[s2];
+    return m;
+  };
+  auto reg_mask_prev = [&]() {
+    uint32_t m = 0;
+    for (int b : pR) m |= 1u << b;
+    return m;
+  };
+  auto shfl_able = [&](uint32_t R) {
+    return shfl && have_prev && (R & ~reg_mask_prev() & ~lane_mask_prev()) == 0;
+  };
   auto class_ok = [&](uint32_t m) {
     for (int cls = 0; cls < 4; ++cls) {
       int c = 0, tot = 0;
@@ -531,7 +556,7 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
           if (!class_ok(R)) continue;
           // ties: keep the fixed low bits (HBM-contiguous lanes) out of the registers
           const uint32_t fmask = fixed >= 32 ? ~0u : ((1u << fixed) - 1u);
-          const int sc = 2 * admitted(R) + ((R & fmask) ? 0 : 1);
+          const int sc = 2 * admitted(R) + ((R & fmask) ? 0 : 1) + (shfl_able(R) ? shfl_bonus : 0);
           if (sc > best) { best = sc; bestR = R; }
         }
         if (best > 1) Rm = bestR;
@@ -566,6 +591,14 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
             if (!(m >> b & 1u) && (b & 3) == cls) ++c;
           return c;
         };
+        // (shuffle transitions: the previous window's register bits first,
+        // then its lane bits, so the transition stays a set of lane swaps)
+        if (shfl && have_prev) {
+          const uint32_t pref[2] = {reg_mask_prev(), lane_mask_prev()};
+          for (uint32_t pm : pref)
+            for (int b = q - 1; b >= 0 && popc(Rm) < RB; --b)
+              if ((pm >> b & 1u) && !(Rm >> b & 1u) && class_left(Rm, b & 3) > 1) Rm |= 1u << b;
+        }
         for (int pass2 = 0; pass2 < 2; ++pass2)
           for (int b = q - 1; b >= 0 && popc(Rm) < RB; --b)
             if (!(Rm >> b & 1u) && (pass2 == 1 || class_left(Rm, b & 3) > 1)) Rm |= 1u << b;
@@ -594,10 +627,39 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
       }
       if (best >= 0) { S.push_back(rest[best]); used[best] = 1; }
     };
-    for (int cls = 0; cls < 4 && (int)S.size() < 5; ++cls) pick(cls);
-    while ((int)S.size() < 5 && S.size() < rest.size()) pick(-1);
-    for (size_t i = 0; i < rest.size(); ++i)
-      if (!used[i]) S.push_back(rest[i]);
+    bool shuffled = false;
+    if (shfl_able(Rm)) {
+      // keep the previous thread-bit slots; each qubit entering the registers
+      // from lane slot s hands that slot to a qubit leaving the registers
+      std::vector<int> S2(pS), out;
+      for (int b : pR)
+        if (!(Rm >> b & 1u)) out.push_back(b);
+      size_t oi = 0;
+      for (int s2 = 0; s2 < n_lanes; ++s2)
+        if (Rm >> S2[s2] & 1u) S2[s2] = out[oi++];
+      int cls = 0;
+      for (int s2 = 0; s2 < n_lanes; ++s2) cls |= 1 << (S2[s2] & 3);
+      if (oi == out.size() && (cls == 15 || q - RB < 5)) {
+        S = S2;
+        shuffled = true;
+      }
+    }
+    if (!shuffled) {
+      for (int cls = 0; cls < 4 && (int)S.size() < 5; ++cls) pick(cls);
+      while ((int)S.size() < 5 && S.size() < rest.size()) pick(-1);
+      for (size_t i = 0; i < rest.size(); ++i)
+        if (!used[i]) S.push_back(rest[i]);
+    }
+    if (std::getenv("HQ_WIN_DEBUG")) {
+      std::fprintf(stderr, "win ops=%zu %s R=", exec.size(), shuffled ? "shfl" : "smem");
+      for (int b : R) std::fprintf(stderr, "%d,", b);
+      std::fprintf(stderr, " S=");
+      for (int b : S) std::fprintf(stderr, "%d,", b);
+      std::fprintf(stderr, "\n");
+    }
+    pR = R;
+    pS = S;
+    have_prev = true;
     (void)all;
     hq::WinDev w{};
     w.op0 = (int16_t)ps.wops.size();

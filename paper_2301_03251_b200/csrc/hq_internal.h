@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -89,6 +90,12 @@ namespace hq {
 hq_status fail_status(hq_status s, const std::string& msg);
 // process-wide launch counters per kernel class (hq_launch_counts)
 void count_launch(int cls);
+// warp-shuffle register-window transitions (plan_windows / the JIT generator);
+// HQ_SHFL=0 disables them
+inline bool shfl_enabled() {
+  const char* e = std::getenv("HQ_SHFL");
+  return !(e && e[0] == '0');
+}
 }  // namespace hq
 
 struct hq_plan_s {

@@ -894,6 +894,73 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   };
   auto hi_off = [&](int i) { return goff((uint32_t)(i * g.T)); };
 
+  // Warp-shuffle transition A -> B (plan_windows builds such pairs): B equals
+  // A with some register bits exchanged with lane bits, every other thread
+  // slot unchanged.  sw: (register bit r of A, lane s); perm[r2] = A-register
+  // bit that holds B's register qubit r2 after the swaps.
+  const bool use_shfl = shfl_enabled() && !std::getenv("HQ_ABLATE");
+  auto shfl_ok = [&](const WinDev& A, const WinDev& B, std::vector<std::pair<int, int>>& sw,
+                     std::vector<int>& perm) -> bool {
+    if (!use_shfl) return false;
+    const std::vector<int> RA = Rbits(A), RB2 = Rbits(B), SA = Sbits(A), SB = Sbits(B);
+    const int lanes = std::min(5, tbits);
+    for (int s2 = lanes; s2 < tbits; ++s2)
+      if (SA[s2] != SB[s2]) return false;
+    sw.clear();
+    std::vector<int> after(RA);
+    for (int s2 = 0; s2 < lanes; ++s2) {
+      if (SA[s2] == SB[s2]) continue;
+      const auto it = std::find(RA.begin(), RA.end(), SB[s2]);
+      if (it == RA.end() || std::find(RB2.begin(), RB2.end(), SA[s2]) == RB2.end()) return false;
+      const int r = (int)(it - RA.begin());
+      sw.push_back({r, s2});
+      after[r] = SA[s2];
+    }
+    if (sw.empty()) return false;
+    perm.assign(g.RB, -1);
+    for (int r2 = 0; r2 < g.RB; ++r2) {
+      const auto it = std::find(after.begin(), after.end(), RB2[r2]);
+      if (it == after.end()) return false;
+      perm[r2] = (int)(it - after.begin());
+    }
+    return true;
+  };
+  // emit the swaps on p (and l), then rename to B's register order and move
+  // the variables to the identity mapping (the next window starts canonical)
+  auto emit_shfl = [&](const std::vector<std::pair<int, int>>& sw, const std::vector<int>& perm, bool both) {
+    for (const auto& rs : sw) {
+      const int r = rs.first, s2 = rs.second;
+      o << "{ const bool h_ = (tid >> " << s2 << ") & 1;\n";
+      for (int i = 0; i < g.N; ++i) {
+        if (i >> r & 1) continue;
+        const int i1 = i | 1 << r;
+        for (int set = 0; set < (both ? 2 : 1); ++set) {
+          const std::string A = set ? g.L(i) : g.P(i), B = set ? g.L(i1) : g.P(i1);
+          o << "{ C s_; s_.x = h_ ? " << A << ".x : " << B << ".x; s_.y = h_ ? " << A << ".y : " << B << ".y; "
+            << "s_.x = __shfl_xor_sync(0xffffffffu, s_.x, " << (1 << s2) << "); s_.y = __shfl_xor_sync(0xffffffffu, "
+            << "s_.y, " << (1 << s2) << "); if (h_) " << A << " = s_; else " << B << " = s_; }\n";
+        }
+      }
+      o << "}\n";
+    }
+    std::vector<int> src(g.N);
+    for (int i2 = 0; i2 < g.N; ++i2) {
+      int i = 0;
+      for (int r2 = 0; r2 < g.RB; ++r2)
+        if (i2 >> r2 & 1) i |= 1 << perm[r2];
+      src[i2] = g.map[i];
+    }
+    for (int set = 0; set < (both ? 2 : 1); ++set) {
+      const char* v = set ? "l" : "p";
+      o << "{ const C";
+      for (int i2 = 0; i2 < g.N; ++i2) o << (i2 ? ", " : " ") << "m" << i2 << "_ = " << v << src[i2];
+      o << ";\n";
+      for (int i2 = 0; i2 < g.N; ++i2) o << v << i2 << " = m" << i2 << "_; ";
+      o << "}\n";
+    }
+    identity_map();
+  };
+
   // ---- header / prologue
   // occupancy hint: ~128 registers per thread for ψ+λ kernels, ~80 for forward
   int minb = std::max(1, 65536 / (g.T * (bwd ? 128 : 80)));
@@ -1131,20 +1198,30 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       o << "__syncthreads();\n";
     }
     // -- forward windows
+    bool fwd_shfl_in = false;   // this window's registers arrive by shuffles
     for (int w = 0; w < nwin; ++w) {
       const WinDev& W = P.wins[w];
       o << "{ // window " << w << "\n";
       g.ph_decl = false;
       g.win_tb(W, tbits);
-      if (!(w == 0 && regs_live)) {
+      if (!(w == 0 && regs_live) && !fwd_shfl_in) {
         identity_map();
         g.load_regs(W, "p", "tp");
       }
+      fwd_shfl_in = false;
       g.pending = false;
       std::vector<int> ks;
       for (int k = W.op0; k < W.op1; ++k) ks.push_back(k);
       hoist(ks);
-      if (w < nwin - 1) {
+      std::vector<std::pair<int, int>> sw;
+      std::vector<int> perm;
+      if (w < nwin - 1 && shfl_ok(W, P.wins[w + 1], sw, perm)) {
+        // registers stay live across the transition: declared outside the window block
+        emit_steps(ks, 0, false, [&] { g.flush_vph(false); g.flush_pending(false); emit_shfl(sw, perm, false); }, ubudget);
+        o << "}\n";
+        identity_map();   // every branch path ended canonical
+        fwd_shfl_in = true;
+      } else if (w < nwin - 1) {
         emit_steps(ks, 0, false, [&] { g.flush_vph(false); g.flush_pending(false); sync(); g.store_regs(W, "p", "tp"); sync(); }, ubudget);
         o << "}\n";
       } else if (fused) {
@@ -1250,6 +1327,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         regs_live = false;
       }
     }
+    bool bwd_shfl_in = false;   // this window's registers arrive by shuffles
     for (int wi = 0; wi < nwin; ++wi) {
       const int w = nwin - 1 - wi;
       if (first && w < stop_win) break;
@@ -1259,12 +1337,15 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         o << "{ // window " << w << " (adjoint)\n";
         g.ph_decl = false;
         g.win_tb(W, tbits);
-        identity_map();
-        if (!(ablate & 1)) {
-          g.load_regs(W, "p", "tp");
-          g.load_regs(W, "l", "tl");
+        if (!bwd_shfl_in) {
+          identity_map();
+          if (!(ablate & 1)) {
+            g.load_regs(W, "p", "tp");
+            g.load_regs(W, "l", "tl");
+          }
         }
       }
+      bwd_shfl_in = false;
       g.pending = false;
       const int lo = std::max<int>(W.op0, first ? stop_op : 0);
       std::vector<int> ks;
@@ -1376,17 +1457,26 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         o << "}\n";
         break;
       }
+      std::vector<std::pair<int, int>> sw;
+      std::vector<int> perm;
+      const bool to_shfl = w > 0 && shfl_ok(W, P.wins[w - 1], sw, perm);
       emit_steps(ks, 0, true, [&] {
         g.flush_batch();
         g.flush_vph(true);
         g.flush_pending(true);
         if (ablate & 1) return;
+        if (to_shfl) {
+          emit_shfl(sw, perm, true);
+          return;
+        }
         sync();
         g.store_regs(W, "p", "tp");
         g.store_regs(W, "l", "tl");
         sync();
       }, ubudget);
       o << "}\n";
+      if (to_shfl) identity_map();   // every branch path ended canonical
+      bwd_shfl_in = to_shfl;
     }
   }
   o << "__syncthreads();\n}\n";  // tile loop

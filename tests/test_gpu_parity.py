@@ -332,7 +332,7 @@ def test_lazy_jacobian_forward_only_launches_no_backward():
     b = wl.make_builder("cfg2", qsim, T)
     th = wl.params_for("cfg2")
     x = wl.inputs_for("cfg2", 32)
-    layer = QuantumLayer(b, n_params=60, param_init=th)
+    layer = QuantumLayer(b, n_params=60, param_init=th.copy())
     n0 = _bwd_launches()
     out = layer(Tensor(x, requires_grad=True, dtype=np.float64))
     assert "stream" in layer.last_info["plan"].description

@@ -113,23 +113,30 @@ def main():
         dev = torch.device("cuda:0")
         ex = TimedExecutor(S.GpuExecutor(dev))
         ex.inner.prepare(sc, range(sc.world))            # JIT every segment plan outside the timings
-        E, grad, _ = S.run_virtual(sc, theta, dev, want_grad=False, ex=ex)   # warm-up
+        E, grad, st_ = S.run_virtual(sc, theta, dev, want_grad=False, ex=ex)   # warm-up
+        del st_
+        torch.cuda.empty_cache()
         ex.per_rank()
         res = {}
         for mode in ("forward", "forward+adjoint"):
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record()
-            E, grad, _ = S.run_virtual(sc, theta, dev, want_grad=mode != "forward", ex=ex)
+            E, grad, st_ = S.run_virtual(sc, theta, dev, want_grad=mode != "forward", ex=ex)
             ev1.record()
             torch.cuda.synchronize()
+            del st_
+            torch.cuda.empty_cache()
             pr = ex.per_rank()
             local = max(sum(v.values()) for v in pr.values())
             n_x = sc.sched.exchanges * (1 if mode == "forward" else 3)   # adjoint replays on psi and lam
             model = local + n_x * xbytes / (a.nvlink_gbs * 1e9) * 1e3
+            passes = sum(int(ex.inner._plan(sc, i, 0).stats(1)["n_passes"]) for i in range(len(sc.sched.segments)))
+            shard = amp * (1 << sc.L)
+            hbm = passes * shard * (2 if mode == "forward" else 6)    # fwd: ψ r+w; +bwd: ψ, λ r+w
             res[mode] = {"virtual_total_ms": ev0.elapsed_time(ev1), "max_rank_local_ms": local,
                          "per_rank_local_ms": {r: round(sum(v.values()), 3) for r, v in sorted(pr.items())},
-                         "exchanges": n_x, "modeled_8gpu_ms": model,
-                         "hbm_bytes_per_rank_local": None, "E": E,
+                         "exchanges": n_x, "modeled_8gpu_ms": model, "local_passes_per_rank": passes,
+                         "hbm_bytes_per_rank_local": hbm, "local_hbm_GBps": hbm / (local / 1e3) / 1e9, "E": E,
                          "grad_norm": None if grad is None else float(np.linalg.norm(grad))}
         print(json.dumps({"workload": f"cfg5: n={a.n} depth={a.depth} {a.precision}, {sc.world} virtual ranks on 1 GPU",
                           "schedule": st, "nvlink_bytes_per_gpu_per_exchange_each_way": xbytes,
