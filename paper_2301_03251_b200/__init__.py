@@ -11,7 +11,7 @@ from .errors import (AdapterError, CircuitError, ConfigError, ContractError, Dim
 from .tensor import (GraphNode, Tensor, backward, no_grad, tensor, tmean, tsum)
 from .rng import manual_seed
 from .nn import Module, Parameter
-from .qsim import (MAX_QUBITS, Circuit, Counts, GateOp, StatePrepOp, StateVector,
+from .qsim import (MAX_QUBITS, Circuit, Counts, GateOp, StatePrepOp, StateVector, apply_gate,
                    format_circuit_text, gate_matrix, parse_circuit_text, probabilities, simulate)
 from .templates import (amplitude_embedding, angle_embedding, basis_embedding, ccz, cry, crz,
                         cswap, toffoli)

@@ -90,11 +90,14 @@ namespace hq {
 hq_status fail_status(hq_status s, const std::string& msg);
 // process-wide launch counters per kernel class (hq_launch_counts)
 void count_launch(int cls);
-// warp-shuffle register-window transitions (plan_windows / the JIT generator);
-// HQ_SHFL=0 disables them
+// warp-shuffle register-window transitions (plan_windows / the JIT generator),
+// opt-in with HQ_SHFL=1: measured slower on cfg4 (complex128 backward 286 ->
+// 294 ms, complex64 124 -> 145 ms at B=1024, profiles/r02_shfl.log): the
+// shuffle-friendly register sets need more windows, and transitions are only
+// ~22% (c128) / ~4% (c64) of the backward passes (HQ_ABLATE=1)
 inline bool shfl_enabled() {
   const char* e = std::getenv("HQ_SHFL");
-  return !(e && e[0] == '0');
+  return e && e[0] == '1';
 }
 }  // namespace hq
 

@@ -181,6 +181,28 @@ def simulate(circuit, initial: StateVector | None = None, precision: str = "c128
     return StateVector.from_amplitudes(amps)
 
 
+def apply_gate(state: StateVector, op) -> None:
+    """Apply one gate to ``state`` in place (``qsim.py:150-176``), on the GPU."""
+    from . import engine
+    if max(op.targets) >= state.n_qubits:
+        raise CircuitError(f"{op.kind} targets {op.targets} exceed {state.n_qubits} qubits")
+    c = Circuit(state.n_qubits)
+    c.add(op)
+    state.amplitudes[:] = engine.simulate_circuit(c, state.amplitudes)
+
+
+def measure_shots(state: StateVector, qubits, shots: int, seed: int):
+    """``qsim.py:236-248`` (device sampling; see ``qnn.measure_shots``)."""
+    from .qnn import measure_shots as _ms
+    return _ms(state, qubits, shots, seed)
+
+
+def shot_rng(seed: int, shot: int):
+    """``qsim.py:222-224``."""
+    from .qnn import shot_rng as _sr
+    return _sr(seed, shot)
+
+
 def probabilities(state: StateVector, qubits) -> np.ndarray:
     """Marginal Born distribution over ``qubits``; outcome bit i = qubits[i]
     (``qsim.py:194-211``).  Host-side: the state is already a host copy."""
