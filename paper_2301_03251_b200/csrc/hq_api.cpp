@@ -810,6 +810,37 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
     touched |= op_mask(op);
     gates.push_back(op);
   }
+  // ---- trailing diagonal gates: a diagonal gate (Z, RZ, CZ, CR) followed only
+  // by monomial gates (X, Y, CNOT, SWAP) and other diagonals acts before a
+  // basis permutation-with-phases and the diagonal EXACT_PROB readout, so it
+  // changes neither E nor any other derivative (|P D ψ|² is |ψ|² permuted).  It
+  // is dropped; the derivatives of variables that enter only dropped gates
+  // are 0, which is also the reference's two-point value (E does not depend on
+  // them).  hq_state (amplitudes) runs on the unfolded twin, which keeps them.
+  std::vector<char> dropped_slot(d->n_slots > 0 ? d->n_slots : 1, 0);
+  if (allow_fold && !std::getenv("HQ_NO_DROP")) {
+    std::vector<char> drop(gates.size(), 0);
+    size_t nd = 0;
+    for (size_t k = gates.size(); k-- > 0;) {
+      const int kd = gates[k].kind;
+      if (kd == HQ_GATE_X || kd == HQ_GATE_Y || kd == HQ_GATE_CNOT || kd == HQ_GATE_SWAP) continue;
+      if (kd == HQ_GATE_Z || kd == HQ_GATE_RZ || kd == HQ_GATE_CZ || kd == HQ_GATE_CR) {
+        drop[k] = 1;
+        ++nd;
+        continue;
+      }
+      break;
+    }
+    if (nd > 0 && nd < gates.size()) {
+      std::vector<hq_op> kept;
+      for (size_t k = 0; k < gates.size(); ++k) {
+        if (!drop[k]) { kept.push_back(gates[k]); continue; }
+        if (gates[k].slot >= 0) dropped_slot[gates[k].slot] = 1;
+      }
+      gates.swap(kept);
+      pl->dropped = (int32_t)nd;
+    }
+  }
   pl->has_preps = d->n_preps > 0;
   std::vector<int32_t> prep_off(d->n_preps);
   for (int p = 0; p < d->n_preps; ++p) { prep_off[p] = pl->prep_total; pl->prep_total += d->prep_len[p]; }
@@ -821,6 +852,7 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
   if (d->grad_mode) {
     for (int v = 0; v < nvars; ++v) {
       var_mode[v] = d->grad_mode[v];
+      if (var_mode[v] == HQ_GRAD_ADJOINT && dropped_slot[d->grad_slot[v]]) var_mode[v] = HQ_GRAD_ZERO;
       if (var_mode[v] == HQ_GRAD_ADJOINT) {
         const int s = d->grad_slot[v];
         auto it = dsl_of_slot.find(s);
@@ -1143,6 +1175,7 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
   } else {
     os << " path=stream kernels=" << (pl->jit.ok ? "jit" : "generic") << " tile_bits=" << pl->tile_bits
        << " reg_bits=" << pl->reg_bits << " folded=" << pl->fold_ops << (pl->fold_grad ? "(grad)" : "")
+       << " dropped_diag=" << pl->dropped
        << " readout_perm=" << pl->perm_ops
        << " passes=" << pl->passes.size() << " [";
     for (size_t i = 0; i < pl->passes.size(); ++i)
@@ -1329,9 +1362,10 @@ static hq_status run(hq_plan pl, const double* x, int64_t ldx, const double* the
     return fail(HQ_E_DIMENSION, "input rows narrower than the circuit's inputs");
   if (pl->n_params > 0 && !theta) return fail(HQ_E_DIMENSION, "missing parameters");
   if (init && pl->has_preps) return fail(HQ_E_CIRCUIT, "initial state and state loads are exclusive");
-  if (init && pl->fold) {
-    // a caller-provided initial state replaces the folded product state: run
-    // the same tape unfolded (same workspace layout for hq_state)
+  if ((init && pl->fold) || (state && pl->dropped > 0)) {
+    // a caller-provided initial state replaces the folded product state, and
+    // amplitudes need the dropped trailing diagonal gates: run the same tape
+    // unfolded (same workspace layout for hq_state)
     hq_plan tw = nullptr;
     {
       std::lock_guard<std::mutex> lk(pl->twin_mu);

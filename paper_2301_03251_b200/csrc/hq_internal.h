@@ -146,6 +146,7 @@ struct hq_plan_s {
   std::vector<uint64_t> perm_mask;
   std::vector<int32_t> perm_const;
   int32_t perm_ops = 0;
+  int32_t dropped = 0;                    // trailing diagonal gates dropped (readout-invariant)
   int64_t fold_ops = 0;
   // hq_state with a caller-provided initial state runs on an unfolded twin
   std::shared_ptr<void> desc_copy;
