@@ -810,26 +810,42 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
     touched |= op_mask(op);
     gates.push_back(op);
   }
-  // ---- trailing diagonal gates: a diagonal gate (Z, RZ, CZ, CR) followed only
-  // by monomial gates (X, Y, CNOT, SWAP) and other diagonals acts before a
-  // basis permutation-with-phases and the diagonal EXACT_PROB readout, so it
-  // changes neither E nor any other derivative (|P D ψ|² is |ψ|² permuted).  It
-  // is dropped; the derivatives of variables that enter only dropped gates
-  // are 0, which is also the reference's two-point value (E does not depend on
-  // them).  hq_state (amplitudes) runs on the unfolded twin, which keeps them.
+  // ---- readout-invariant diagonal gates: a diagonal gate (Z, RZ, CZ, CR)
+  // that commutes to the end of the circuit — past gates on other qubits,
+  // other diagonals, and monomial gates (X, Y, CNOT, SWAP), which keep it
+  // diagonal while widening its support (CNOT with a target in the support
+  // adds the control; SWAP moves it) — acts before a permutation-with-phases
+  // and the diagonal EXACT_PROB readout, so it changes neither E nor any other
+  // derivative (|P D ψ|² is |ψ|² permuted).  It is dropped; the derivatives of
+  // variables that enter only dropped gates are 0, which is also the
+  // reference's two-point value (E does not depend on them).  hq_state
+  // (amplitudes) runs on the unfolded twin, which keeps every gate.
   std::vector<char> dropped_slot(d->n_slots > 0 ? d->n_slots : 1, 0);
   if (allow_fold && !std::getenv("HQ_NO_DROP")) {
+    auto diag = [](int k) { return k == HQ_GATE_Z || k == HQ_GATE_RZ || k == HQ_GATE_CZ || k == HQ_GATE_CR; };
     std::vector<char> drop(gates.size(), 0);
     size_t nd = 0;
-    for (size_t k = gates.size(); k-- > 0;) {
-      const int kd = gates[k].kind;
-      if (kd == HQ_GATE_X || kd == HQ_GATE_Y || kd == HQ_GATE_CNOT || kd == HQ_GATE_SWAP) continue;
-      if (kd == HQ_GATE_Z || kd == HQ_GATE_RZ || kd == HQ_GATE_CZ || kd == HQ_GATE_CR) {
-        drop[k] = 1;
-        ++nd;
-        continue;
+    for (size_t k = 0; k < gates.size(); ++k) {
+      if (!diag(gates[k].kind)) continue;
+      uint64_t S = op_mask(gates[k]);
+      bool ok = true;
+      for (size_t j = k + 1; j < gates.size() && ok; ++j) {
+        const hq_op& g = gates[j];
+        const uint64_t m = op_mask(g);
+        if (!(m & S) || diag(g.kind) || g.kind == HQ_GATE_X || g.kind == HQ_GATE_Y) continue;
+        if (g.kind == HQ_GATE_CNOT) {
+          if (S >> g.q1 & 1ull) S |= 1ull << g.q0;
+        } else if (g.kind == HQ_GATE_SWAP) {
+          const uint64_t a = 1ull << g.q0, b = 1ull << g.q1;
+          const bool ha = S & a, hb = S & b;
+          S &= ~(a | b);
+          if (ha) S |= b;
+          if (hb) S |= a;
+        } else {
+          ok = false;   // H / RX / RY on the support: not readout-invariant
+        }
       }
-      break;
+      if (ok) { drop[k] = 1; ++nd; }
     }
     if (nd > 0 && nd < gates.size()) {
       std::vector<hq_op> kept;
@@ -1329,7 +1345,7 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
   pl->dev = dv;
   pl->d_tape = rebase(r_tape, base);
   pl->n_tape = d->n_ops;
-  if (pl->fold) pl->desc_copy = std::make_shared<DescCopy>(d);
+  if (pl->fold || pl->dropped > 0) pl->desc_copy = std::make_shared<DescCopy>(d);
   pl->d_wops = rebase(r_wops, base);
 
   *out = pl;
