@@ -642,7 +642,7 @@ struct Gen {
     for (int lv = 0; lv < Lv; ++lv) o << " + ((ln_ & " << split_m[lv] << "u) ? " << (1 << (Lv - 1 - lv)) << " : 0)";
     o << ";\nint s_ = " << bq[0] << ";";
     for (int j = 1; j < K; ++j) o << " if (d_ == " << j << ") s_ = " << bq[j] << ";";
-    o << "\nif (d_ < " << K << " && (ln_ & " << red << "u) == 0) dacc[s_ * " << bstride << " + (tid >> 5) * " << bgroup
+    o << "\nif (d_ < " << K << " && (ln_ & " << red << "u) == 0) dacc[s_ * " << bstride << " + (tidw >> 5) * " << bgroup
       << " + (ln_ & " << (bgroup - 1) << "u)] += z_; }\n";
     bq.clear();
   }
@@ -693,6 +693,10 @@ typedef unsigned long size_t;
 
 const char* kHelpers = R"(
 __device__ __forceinline__ void bar_na() { asm volatile("barrier.sync 0;" ::: "memory"); }
+// named barriers of the ping-pong kernels (ids 1-2: a tile group, 3-4: the token)
+__device__ __forceinline__ void bar_id(int id, int n) { asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_id_na(int id, int n) { asm volatile("barrier.sync %0, %1;" :: "r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive_na(int id, int n) { asm volatile("barrier.arrive %0, %1;" :: "r"(id), "r"(n) : "memory"); }
 namespace hq {
 __device__ __forceinline__ uint32_t jpad(uint32_t j) { return j + (j >> 4) + (j >> 8); }
 // packed FP32x2 (sm_100 FFMA2/FMUL2/FADD2): a complex64 amplitude is one
@@ -739,15 +743,33 @@ size_t a16(size_t v) { return (v + 15) & ~(size_t)15; }
 }  // namespace
 
 // shared-memory layout of generated kernels (host and generator agree)
+// Ping-pong backward kernels (HQ_PINGPONG=1): one CTA holds TWO tile groups of
+// T threads (each with its own transposition buffers and named barriers) that
+// take turns: while one group runs a window's gate math, the other does its
+// shared-memory window transition or HBM load / store.  A token passed through
+// two named barriers (bar.arrive / bar.sync over 2T threads) enforces the
+// alternation, so the FP64 / FMA pipe is not left idle while a lone group
+// transposes.  Needs the derivative partials in registers or in group mode,
+// and no tile-local folded gradients.
+bool pingpong_for(const hq_plan_s* pl, int i, bool bwd, bool fused) {
+  const char* e = std::getenv("HQ_PINGPONG");
+  if (!(e && e[0] == '1') || !bwd || fused) return false;
+  if (i == 0 && pl->fold_grad && !pl->fold_local.empty()) return false;
+  return true;
+}
+
 JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd, bool fused) {
   const Pass& P = pl->passes[i];
   const int RB = pl->reg_bits;
   const int T = 1 << (pl->tile_bits - RB);
   const size_t amp = pl->precision == HQ_C64 ? 8 : 16, rsz = amp / 2;
   JitLayout L{};
+  L.pp = pingpong_for(pl, i, bwd, fused);
+  L.block = L.pp ? 2 * T : T;
+  const int nwt = L.block / 32;                        // warps per CTA
   const size_t tnp = (size_t)1 << pl->tile_bits;
   const size_t padded = tnp + tnp / 16 + tnp / 256;   // pad(TN-1)+1
-  size_t o = a16((bwd ? 2 : 1) * amp * padded);
+  size_t o = a16((bwd ? 2 : 1) * amp * padded) * (L.pp ? 2 : 1);
   L.lut = o;
   L.trig = o; o = a16(o + P.slots.size() * 8 * rsz);
   L.extra = o;
@@ -755,19 +777,20 @@ JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd, bool fused) {
     // largest lane group whose partials fit: a dot costs log2(32/group)
     // shuffles plus one shared read-modify-write per tile
     L.group = 32;
-    while (L.group > 1 && (size_t)P.n_dslots_pass * (T / 32) * L.group * rsz > 40 * 1024) L.group >>= 1;
+    while (L.group > 1 && (size_t)P.n_dslots_pass * nwt * L.group * rsz > 40 * 1024) L.group >>= 1;
     L.per_thread = L.group == 32;
     if (!L.per_thread) L.group = std::min(L.group, 4);   // batched reduction keeps 4 partials per warp
     // group mode: a batch updates 8 slots at once; a stride of nw·G + 4 puts
-    // consecutive slots on different banks
-    L.slot_stride = L.per_thread ? T : (T / 32) * L.group + 4;
-    o = a16(o + (size_t)P.n_dslots_pass * L.slot_stride * rsz);
+    // consecutive slots on different banks.  Ping-pong per-thread mode keeps
+    // every partial in registers and reduces per warp at the end.
+    L.slot_stride = L.per_thread ? (L.pp ? nwt : T) : nwt * L.group + 4;
+    o = a16(o + (size_t)P.n_dslots_pass * L.slot_stride * (L.pp && L.per_thread ? 8 : rsz));
   }
   L.extra2 = o;
   if (!bwd || fused)
     o = a16(o + (96 + (size_t)(i == 0 ? ((pl->prep_total + 1) & ~1) : 0)) * 8);
   L.fred = o;   // first backward pass of a plan with folded gradients: per-warp tile contractions
-  if (bwd && i == 0 && pl->fold_grad) o = a16(o + (size_t)(T / 32) * (2 + 4 * pl->fold_local.size()) * 8);
+  if (bwd && i == 0 && pl->fold_grad) o = a16(o + (size_t)nwt * (2 + 4 * pl->fold_local.size()) * 8);
   L.fz = o;
   if (i == 0 && pl->fold) o = a16(o + ((size_t)pl->n_qubits * 2 + ((size_t)1 << RB)) * amp);
   L.total = o;
@@ -815,7 +838,11 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   const bool fold_end = bwd && first && pl->fold_grad;
   const int f = pl->fixed_bits;
   const JitLayout L = jit_layout(pl, pi, bwd, fused);
+  const bool pp = L.pp;
   const int nw = g.T / 32;
+  const int nwt = L.block / 32;   // warps per CTA (both tile groups in ping-pong kernels)
+  const size_t pp_buf = ((size_t)(bwd ? 2 : 1) * (c64 ? 8 : 16) *
+                         (((size_t)1 << g.Q) + ((size_t)1 << g.Q) / 16 + ((size_t)1 << g.Q) / 256) + 15) & ~(size_t)15;
   const int nwin = (int)P.wins.size();
   std::ostringstream& o = g.o;
 
@@ -965,17 +992,20 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   // occupancy hint: ~128 registers per thread for ψ+λ kernels, ~80 for forward
   int minb = std::max(1, 65536 / (g.T * (bwd ? 128 : 80)));
   if (const char* e = std::getenv(bwd ? "HQ_BWD_MINB" : "HQ_FWD_MINB")) minb = std::max(1, std::atoi(e));
-  o << "extern \"C\" __global__ void __launch_bounds__(" << g.T << ", " << minb << ") "
+  if (pp) minb = 1;
+  o << "extern \"C\" __global__ void __launch_bounds__(" << L.block << ", " << minb << ") "
     << (fused ? "hq_fb" : (bwd ? "hq_b" : "hq_f")) << pi << "(const hq::KArgs a, const hq::JPass ps) {\n"
     << "using namespace hq;\n"
     << "typedef " << g.R() << " R; typedef " << (c64 ? "float2" : "double2") << " C;\n"
     << "constexpr int T = " << g.T << ", Q = " << g.Q << ";\n"
     << "const R HH = (R)0.70710678118654752440;\n(void)HH;\n"
     << "extern __shared__ __align__(16) unsigned char smem[];\n"
-    << "const DevPlan& p = a.p;\nconst int tid = threadIdx.x;\n"
+    << "const DevPlan& p = a.p;\nconst int tidw = threadIdx.x;\n"
+    << (pp ? "const int tid = tidw & (T - 1);\nconst int grp = tidw / T;\n" : "const int tid = tidw;\nconst int grp = 0;\n")
+    << "(void)grp;\n"
     << "const int64_t vl = blockIdx.x / ps.n_chunks;\nconst int chunk = (int)(blockIdx.x - vl * ps.n_chunks);\n"
     << "const int64_t v = ps.v0 + vl;\nconst VSample vs = decode_vsample(p, v, a.B);\n"
-    << "C* tp = reinterpret_cast<C*>(smem);\n"
+    << "C* tp = reinterpret_cast<C*>(smem + (size_t)grp * " << (pp ? pp_buf : 0) << ");\n"
     << (bwd ? "C* tl = tp + ((1 << Q) + (1 << Q) / 16 + (1 << Q) / 256);\n(void)tl;\n" : "")
     << "const uint32_t tpad = (uint32_t)tid + ((uint32_t)tid >> 4) + ((uint32_t)tid >> 8);\n(void)tpad;\n"
     << "R* trig = reinterpret_cast<R*>(smem + " << L.trig << ");\n";
@@ -984,7 +1014,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   o << ";\n(void)ot;\n";
   if (bwd)
     o << "R* dacc = reinterpret_cast<R*>(smem + " << L.extra << ");\n"
-      << "for (int i = tid; i < " << P.n_dslots_pass * L.slot_stride << "; i += T) dacc[i] = (R)0;\n";
+      << "for (int i = tidw; i < " << P.n_dslots_pass * L.slot_stride << "; i += " << L.block << ") dacc[i] = (R)0;\n";
   if (fwd)
     o << "double* dx = reinterpret_cast<double*>(smem + " << L.extra2 << ");\n"
       << "double* red = dx; double* inv = dx + 32; double* wt = dx + 64; double* sval = dx + 96;\n"
@@ -998,7 +1028,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       << "auto cm_ = [](C u, C w) { C r; r.x = u.x * w.x - u.y * w.y; r.y = u.x * w.y + u.y * w.x; return r; };\n"
       << "(void)cm_;\n";
   }
-  o << "load_trig8<R>(a, vs, ps.slots, ps.n_slots, trig, tid, T);\n";
+  o << "load_trig8<R>(a, vs, ps.slots, ps.n_slots, trig, tidw, " << L.block << ");\n";
   if (fwd && first) o << "if (p.n_preps > 0) load_prep_values(a, vs, sval, tid, T);\n";
   if (mode == 0 && last)
     o << "__shared__ double gph[2];\nif (a.state && tid == 0) { const double* xr = a.x + vs.b * a.ldx; double fph = 0.0; "
@@ -1054,6 +1084,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     int cap = 56;
     if (const char* e = std::getenv("HQ_REG_ACC")) cap = std::atoi(e);
     if (P.n_dslots_pass <= cap && L.per_thread) reg_acc = P.n_dslots_pass;
+    if (pp && L.per_thread) reg_acc = P.n_dslots_pass;   // ping-pong keeps no per-thread partials in shared memory
     for (int k = 0; k < reg_acc; ++k) o << "R da" << k << " = (R)0;\n";
     if (!L.per_thread) o << "R dq0, dq1, dq2, dq3, dq4, dq5, dq6, dq7;\n";
     if (fold_end && !pl->fold_local.empty()) o << "double lacc_x = 0.0, lacc_y = 0.0;\n";
@@ -1080,7 +1111,24 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     if (const char* e = std::getenv("HQ_UBRANCH0")) ubudget = std::atoi(e);
   }
   bool na = false;
-  auto sync = [&]() { o << (na ? "bar_na();\n" : "__syncthreads();\n"); };
+  auto sync = [&]() {
+    if (pp) o << (na ? "bar_id_na(1 + grp, T);\n" : "bar_id(1 + grp, T);\n");
+    else o << (na ? "bar_na();\n" : "__syncthreads();\n");
+  };
+  // tile-loop barrier outside any branch (the whole CTA, or one tile group)
+  auto gsync = [&]() { o << (pp ? "bar_id(1 + grp, T);\n" : "__syncthreads();\n"); };
+  // ping-pong token: before a window's gate math wait for the other group's
+  // math to end (the first window of group 0 starts at once); after it, hand
+  // the token over (the last window of group 1 has nobody left to hand to)
+  auto pp_acquire = [&]() {
+    if (pp) o << "if (pp_on) { if (grp == 1 || !pp_first) bar_id_na(4 - grp, " << L.block << "); pp_first = false; }\n";
+  };
+  auto pp_release = [&](bool last_window) {
+    if (!pp) return;
+    o << "if (pp_on";
+    if (last_window) o << " && !(grp == 1 && tt + 2 >= ps.tpc)";
+    o << ") bar_arrive_na(3 + grp, " << L.block << ");\n";
+  };
   std::function<void(const std::vector<int>&, size_t, bool, const std::function<void()>&, int)> emit_steps;
   emit_steps = [&](const std::vector<int>& ks, size_t i, bool adj, const std::function<void()>& tail, int budget) {
     for (; i < ks.size(); ++i) {
@@ -1088,7 +1136,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       const WOp& op = P.wops[k];
       g.prepare(op, adj);
       if (adj) {
-        if (!(ablate & 4)) g.dot(op, L.per_thread, L.group, nw, reg_acc);
+        if (!(ablate & 4)) g.dot(op, L.per_thread, L.group, nwt, reg_acc);
         if (first && !fold_end && k == stop_op && op.dl >= 0) continue;
       }
       const bool uni = op.kind == HQ_GATE_CNOT && !Gen::is_reg(op.a) && (op.a >= 64 || op.a - 16 >= 5);
@@ -1156,8 +1204,12 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   };
 
   // ---- tile loop
-  o << "for (int tt = 0; tt < ps.tpc; ++tt) {\n"
-    << "const uint64_t t = (uint64_t)chunk * ps.tpc + tt;\n"
+  if (pp)
+    o << "const bool pp_on = ps.tpc >= 2;\nbool pp_first = true;\n(void)pp_first;\n"
+      << "for (int tt = pp_on ? grp : (grp ? ps.tpc : 0); tt < ps.tpc; tt += pp_on ? 2 : 1) {\n";
+  else
+    o << "for (int tt = 0; tt < ps.tpc; ++tt) {\n";
+  o << "const uint64_t t = (uint64_t)chunk * ps.tpc + tt;\n"
     << "const uint64_t base = 0ull";
   for (size_t i = 0; i < nonlocal.size(); ++i) o << " | (((t >> " << i << ") & 1ull) << " << nonlocal[i] << ")";
   o << ";\n";
@@ -1323,7 +1375,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         for (int i = 0; i < g.N; ++i) o << "l" << i << " = glam[base | ot | " << hex64(hi_off(i)) << "];\n";
         for (int i = 0; i < g.N; ++i) o << "tp[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u] = p" << i << ";\n";
         for (int i = 0; i < g.N; ++i) o << "tl[tpad + " << Gen::pad((uint32_t)(i * g.T)) << "u] = l" << i << ";\n";
-        o << "__syncthreads();\n";
+        gsync();
         regs_live = false;
       }
     }
@@ -1352,11 +1404,13 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       for (int k = W.op1 - 1; k >= lo; --k) ks.push_back(k);
       hoist(ks);
       const bool end = first ? (wi == nwin - 1 || w == stop_win) : (w == 0);
+      pp_acquire();
       if (end) {
         emit_steps(ks, 0, true, [&] {
           g.flush_batch();
           g.flush_vph(true);
           g.flush_pending(true);
+          pp_release(true);
           if (fold_end) {
             // λ at the circuit start (all first-pass gates un-applied), contracted
             // with the tile's initial factors z_q (fz):
@@ -1419,11 +1473,12 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
             }
             o << "#pragma unroll\nfor (int k_ = 0; k_ < " << NV << "; ++k_) vv_[k_] = warp_sum<double>(vv_[k_]);\n";
             sync();
-            o << "if ((tid & 31) == 0) { for (int k_ = 0; k_ < " << NV << "; ++k_) fred[(tid >> 5) * " << NV
+            o << "if ((tid & 31) == 0) { for (int k_ = 0; k_ < " << NV << "; ++k_) fred[(tidw >> 5) * " << NV
               << " + k_] = vv_[k_]; }\n";
             sync();
             o << "if (tid < " << NV / 2 << ") { double ax = 0.0, ay = 0.0; for (int k = 0; k < " << nw
-              << "; ++k) { ax += fred[k * " << NV << " + 2 * tid]; ay += fred[k * " << NV << " + 2 * tid + 1]; }\n"
+              << "; ++k) { ax += fred[(grp * " << nw << " + k) * " << NV << " + 2 * tid]; ay += fred[(grp * " << nw
+              << " + k) * " << NV << " + 2 * tid + 1]; }\n"
               << "if (tid == 0) { double* dst = a.lamN + 2 * (vl * ((int64_t)1 << " << nonlocal.size()
               << ") + (int64_t)t); dst[0] = ax; dst[1] = ay; }\n";
             if (nlq) {
@@ -1464,6 +1519,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         g.flush_batch();
         g.flush_vph(true);
         g.flush_pending(true);
+        pp_release(false);
         if (ablate & 1) return;
         if (to_shfl) {
           emit_shfl(sw, perm, true);
@@ -1479,18 +1535,29 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       bwd_shfl_in = to_shfl;
     }
   }
-  o << "__syncthreads();\n}\n";  // tile loop
+  gsync();
+  o << "}\n";  // tile loop
   if (fwd && last)
     o << "e = block_sum<R>(e, red, tid, T);\nif (tid == 0) ps.rpart[vl * ps.n_chunks + chunk] = e;\n";
   if (fold_end && !pl->fold_local.empty())
     o << "if (tid >= 1 && tid < " << 1 + 2 * pl->fold_local.size() << ") { double* dst = a.locpart + 2 * ((vl * ps.n_chunks + "
          "chunk) * " << 2 * pl->fold_local.size() << " + (tid - 1)); dst[0] = lacc_x; dst[1] = lacc_y; }\n";
-  if (bwd) {
-    const int width = nw * L.group;
+  if (bwd && pp && L.per_thread) {
+    // ping-pong, per-thread mode: every partial is in registers (reg_acc ==
+    // n_dslots): per-warp sums, then one warp per slot folds the CTA's warps
+    for (int k = 0; k < reg_acc; ++k)
+      o << "{ const double s_ = warp_sum<double>((double)da" << k << "); if ((tid & 31) == 0) dacc[" << k << " * "
+        << nwt << " + (tidw >> 5)] = (R)s_; }\n";
+    o << "__syncthreads();\n{ const int lane_ = tid & 31;\nfor (int i = tidw >> 5; i < " << P.n_dslots_pass
+      << "; i += " << nwt << ") { double s = 0.0; for (int k = lane_; k < " << nwt
+      << "; k += 32) s += (double)dacc[i * " << nwt << " + k]; s = warp_sum<double>(s); "
+      << "if (lane_ == 0) a.dpart[((int64_t)v * p.n_adj + ps.dlist[i]) * a.n_parts + chunk] = s; } }\n";
+  } else if (bwd) {
+    const int width = nwt * L.group;
     for (int k = 0; k < reg_acc; ++k) o << "dacc[" << k << " * T + tid] = da" << k << ";\n";
     // one warp per slot: lanes sum strided partials in double, then a shuffle tree
-    o << "__syncthreads();\n{ const int lane_ = tid & 31;\nfor (int i = tid >> 5; i < " << P.n_dslots_pass
-      << "; i += " << nw << ") { double s = 0.0; for (int k = lane_; k < " << width
+    o << "__syncthreads();\n{ const int lane_ = tid & 31;\nfor (int i = tidw >> 5; i < " << P.n_dslots_pass
+      << "; i += " << nwt << ") { double s = 0.0; for (int k = lane_; k < " << width
       << "; k += 32) s += (double)dacc[i * " << L.slot_stride << " + k]; s = warp_sum<double>(s); "
       << "if (lane_ == 0) a.dpart[((int64_t)v * p.n_adj + ps.dlist[i]) * a.n_parts + chunk] = s; } }\n";
   }
@@ -1516,7 +1583,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     decl = d.str();
     const int K = (int)g.ptab.size();
     b << "__shared__ C ptab_[" << K << "];\n"
-      << "for (int j_ = tid; j_ < " << K << "; j_ += T) { R x_ = (R)1, y_ = (R)0;\n"
+      << "for (int j_ = tidw; j_ < " << K << "; j_ += " << L.block << ") { R x_ = (R)1, y_ = (R)0;\n"
       << "  for (int m_ = " << nm << "_pto[j_]; m_ < " << nm << "_pto[j_ + 1]; ++m_) { const int s_ = " << nm
       << "_pts[m_], k_ = " << nm << "_ptk[m_];\n"
       << "    if (s_ < 0) { x_ = -x_; y_ = -y_; continue; }\n"
@@ -1786,8 +1853,7 @@ cudaError_t jit_launch_pass(const hq_plan_s* pl, int i, int mode, const KArgs& a
   const bool bwd = mode != 0;
   const JitLayout L = jit_layout(pl, i, bwd, mode == 2);
   cudaKernel_t k = mode == 0 ? pl->jit.fwd[i] : (mode == 1 ? pl->jit.bwd[i] : pl->jit.fused);
-  const int RB = pl->reg_bits;
-  const int T = 1 << (pl->tile_bits - RB);
+  const int T = L.block;
   KArgs ac = a;
   JPass pc = ps;
   void* args[] = {&ac, &pc};

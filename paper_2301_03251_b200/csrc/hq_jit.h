@@ -14,7 +14,12 @@ struct JitLayout {
   bool per_thread;  // bwd: per-thread derivative accumulators (group == 32)
   int group;        // bwd: derivative partials kept per group of 32/group lanes (1 = per warp)
   int slot_stride;  // bwd: floats between derivative slots' partials (padded in group mode: no bank conflicts)
+  bool pp;          // ping-pong: two tile groups per CTA alternating math / transition phases
+  int block;        // threads per CTA (T, or 2T in ping-pong kernels)
 };
+
+// ping-pong backward kernels (HQ_PINGPONG=1): see gen_pass
+bool pingpong_for(const hq_plan_s* pl, int pass, bool bwd, bool fused);
 
 JitLayout jit_layout(const hq_plan_s* pl, int pass, bool bwd, bool fused = false);
 // compile (or fetch from the in-process / on-disk cache) the plan's pass kernels
