@@ -17,7 +17,7 @@ from .templates import (amplitude_embedding, angle_embedding, basis_embedding, c
                         cswap, toffoli)
 from .qnn import (EXACT_PROB, NOISY, SHOT_SAMPLING, NoiseQuantumLayer, QAELayer, QuantumLayer,
                   expectation_from_counts, measure_shots, parameter_shift_grad, shot_rng)
-from .noise import (CHANNEL_NAMES, Channel, NoiseModel, amplitude_damping, bit_flip, depolarizing,
-                    phase_flip, simulate_noisy)
+from .noise import (CHANNEL_NAMES, Channel, NoiseModel, amplitude_damping, apply_channel, bit_flip,
+                    depolarizing, phase_flip, run_trajectory, simulate_noisy)
 
 __version__ = "0.1.0"

@@ -151,3 +151,30 @@ def _to_oracle(c):
         oc.add(O.Op(op.kind, tuple(op.targets), op.angle))
     oc.measure(*c.measured_qubits)
     return oc
+
+
+def test_host_level_trajectory_helpers_match_oracle():
+    """apply_channel / run_trajectory (noise.py:93-138) with a caller's NumPy
+    generator: the same draws as the oracle's restatement, the same final
+    states (gates on the GPU, damping jumps on the host copy)."""
+    g = golden("noise")
+    circuits = _circuits(g)
+    ours, theirs = _models(g, N), _models(g, O)
+    for k, c in enumerate(circuits):
+        mi = int(g["model"][k])
+        oc = O.Circuit(c.n_qubits)
+        for op in c.ops:
+            oc.add(O.Op(op.kind, op.targets, op.angle))
+        for seed in (0, 7):
+            st = N.run_trajectory(c, ours[mi], np.random.default_rng(seed))
+            want = O.run_trajectory(oc, theirs[mi], np.random.default_rng(seed))
+            np.testing.assert_allclose(st.amplitudes, want, atol=1e-12)
+    # a single channel application on a prepared state
+    c = Circuit(2)
+    c.h(0); c.cnot(0, 1)
+    from paper_2301_03251_b200 import simulate
+    st = simulate(c)
+    N.apply_channel(st, 1, N.amplitude_damping(0.4), np.random.default_rng(3))
+    psi = O.simulate(O.Circuit(2, ops=[O.Op("H", (0,)), O.Op("CNOT", (0, 1))]))
+    O.apply_channel(psi, 2, 1, O.Channel("amplitude_damping", 0.4), np.random.default_rng(3))
+    np.testing.assert_allclose(st.amplitudes, psi, atol=1e-12)
