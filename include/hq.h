@@ -226,6 +226,27 @@ hq_status hq_shard_readout(const void* psi, int32_t precision, int32_t n_local, 
                            const double* wk, int32_t k, double w0, double* e_out, void* lam, void* workspace,
                            size_t workspace_bytes, void* stream);
 
+/* ---- multi-GPU communicator (one process per GPU; NCCL loaded at run time) --
+ * The library's own NCCL communicator for the two collectives of SURVEY.md
+ * §8(e): the [P] gradient all-reduce of the sample-sharded layer and the
+ * global<->local qubit all-to-all of the amplitude-sharded executor. */
+typedef struct hq_comm_s* hq_comm;
+size_t hq_comm_id_bytes(void);                           /* ncclUniqueId size (128) */
+hq_status hq_comm_unique_id(void* id_out);               /* on one rank; share it with the others */
+hq_status hq_comm_init(const void* id, int32_t rank, int32_t world, hq_comm* out);
+void hq_comm_destroy(hq_comm comm);
+/* in-place sum over ranks (device buffer) */
+hq_status hq_comm_allreduce_f64(hq_comm comm, double* buf, int64_t count, void* stream);
+/* chunk j of send -> rank j; chunk from rank j -> chunk j of recv (contiguous,
+ * bytes_per_rank each; send != recv) */
+hq_status hq_comm_alltoall(hq_comm comm, const void* send, void* recv, int64_t bytes_per_rank, void* stream);
+/* one data-parallel step: hq_forward(HQ_WANT_JAC) + hq_vjp + all-reduce of
+ * grad_theta (replaces qnn.py:131,147-152 across ranks); comm may be NULL
+ * (single rank).  grad_x optional. */
+hq_status hq_backward_dp(hq_plan plan, const double* x, int64_t ldx, const double* theta, int64_t batch,
+                         const double* upstream, double* out, double* jac, double* grad_x, double* grad_theta,
+                         hq_comm comm, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- introspection / measurement ---------------------------------------- */
 
 typedef struct {

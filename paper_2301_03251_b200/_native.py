@@ -24,7 +24,8 @@ EXPORTS = ("hq_abi_version", "hq_last_error", "hq_plan_create", "hq_plan_destroy
            "hq_stats", "hq_profile_enable", "hq_profile_read", "hq_sample_workspace_bytes", "hq_sample",
            "hq_shot_uniforms", "hq_noisy_workspace_bytes", "hq_noisy", "hq_launch_counts",
            "hq_plan_create_segment", "hq_seg_workspace_bytes", "hq_seg_forward", "hq_seg_backward",
-           "hq_shard_readout_workspace_bytes", "hq_shard_readout")
+           "hq_shard_readout_workspace_bytes", "hq_shard_readout", "hq_comm_id_bytes", "hq_comm_unique_id",
+           "hq_comm_init", "hq_comm_destroy", "hq_comm_allreduce_f64", "hq_comm_alltoall", "hq_backward_dp")
 K_CLASSES = ("onchip", "pass_fwd", "pass_bwd", "other")
 
 
@@ -134,6 +135,21 @@ def lib():
     h.hq_shard_readout.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, _P, _P, ctypes.c_int32, ctypes.c_double,
                                    _P, _P, _P, ctypes.c_size_t, _P]
     h.hq_shard_readout.restype = ctypes.c_int
+    h.hq_comm_id_bytes.argtypes = []
+    h.hq_comm_id_bytes.restype = ctypes.c_size_t
+    h.hq_comm_unique_id.argtypes = [_P]
+    h.hq_comm_unique_id.restype = ctypes.c_int
+    h.hq_comm_init.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_P)]
+    h.hq_comm_init.restype = ctypes.c_int
+    h.hq_comm_destroy.argtypes = [_P]
+    h.hq_comm_destroy.restype = None
+    h.hq_comm_allreduce_f64.argtypes = [_P, _P, ctypes.c_int64, _P]
+    h.hq_comm_allreduce_f64.restype = ctypes.c_int
+    h.hq_comm_alltoall.argtypes = [_P, _P, _P, ctypes.c_int64, _P]
+    h.hq_comm_alltoall.restype = ctypes.c_int
+    h.hq_backward_dp.argtypes = [_P, _P, ctypes.c_int64, _P, ctypes.c_int64, _P, _P, _P, _P, _P, _P, _P,
+                                 ctypes.c_size_t, _P]
+    h.hq_backward_dp.restype = ctypes.c_int
     if h.hq_abi_version() != 2:
         raise NativeError(f"libhq ABI {h.hq_abi_version()} != 2")
     _lib = h

@@ -989,8 +989,10 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   };
 
   // ---- header / prologue
-  // occupancy hint: ~128 registers per thread for ψ+λ kernels, ~80 for forward
-  int minb = std::max(1, 65536 / (g.T * (bwd ? 128 : 80)));
+  // occupancy hint: ~128 registers per thread for ψ+λ kernels, 64 for forward
+  // (4 CTAs/SM at 256 threads: cfg4 forward 95.8 -> 94.4 ms c128, 39.3 -> 38.1
+  // ms c64 vs 80 registers / 3 CTAs, profiles/r02_fwdminb.log)
+  int minb = std::max(1, 65536 / (g.T * (bwd ? 128 : 64)));
   if (const char* e = std::getenv(bwd ? "HQ_BWD_MINB" : "HQ_FWD_MINB")) minb = std::max(1, std::atoi(e));
   if (pp) minb = 1;
   o << "extern \"C\" __global__ void __launch_bounds__(" << L.block << ", " << minb << ") "

@@ -136,3 +136,88 @@ class DataParallelQuantumLayer:
                     return t.cpu().numpy()
                 node.df = df
         return out
+
+
+class LibComm:
+    """The library's own NCCL communicator (``hq_comm_*`` in include/hq.h):
+    one per process, rank / world taken from ``torch.distributed`` (the
+    ncclUniqueId is made on rank 0 and broadcast through the process group) or
+    a single-rank communicator when no group is initialised."""
+
+    def __init__(self, device=None, group=None):
+        import ctypes
+        import torch
+        from . import _native as nat
+        self._nat = nat
+        L = nat.lib()
+        dist = _dist()
+        if dist.is_initialized():
+            self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        else:
+            self.rank, self.world = 0, 1
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        nid = int(L.hq_comm_id_bytes())
+        buf = (ctypes.c_char * nid)()
+        if self.rank == 0:
+            nat.check(L.hq_comm_unique_id(ctypes.cast(buf, ctypes.c_void_p)), "comm id")
+        if self.world > 1:
+            obj = [bytes(buf)]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            ctypes.memmove(buf, obj[0], nid)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            nat.check(L.hq_comm_init(ctypes.cast(buf, ctypes.c_void_p), self.rank, self.world, ctypes.byref(h)),
+                      "comm init")
+        self._h = h
+        self._lib = L
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.hq_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _stream(self):
+        import torch
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def allreduce_(self, t):
+        """In-place sum over ranks of a contiguous f64 CUDA tensor."""
+        import torch
+        if t.dtype != torch.float64 or not t.is_contiguous() or t.device != self.device:
+            raise ValueError("allreduce_ needs a contiguous float64 tensor on the communicator's device")
+        self._nat.check(self._lib.hq_comm_allreduce_f64(self._h, t.data_ptr(), t.numel(), self._stream()), "allreduce")
+        return t
+
+    def alltoall(self, send, recv):
+        """Chunk j of ``send`` -> rank j, chunk from rank j -> chunk j of ``recv``."""
+        nbytes = send.numel() * send.element_size()
+        if nbytes % self.world or recv.numel() * recv.element_size() != nbytes:
+            raise ValueError("alltoall needs equal-size buffers divisible by the world size")
+        self._nat.check(self._lib.hq_comm_alltoall(self._h, send.data_ptr(), recv.data_ptr(), nbytes // self.world,
+                                                   self._stream()), "alltoall")
+        return recv
+
+    def backward_dp(self, plan, x, theta, upstream, want_x=False):
+        """hq_backward_dp: this rank's forward + jacobian + vjp, then ONE
+        all-reduce of the [P] parameter gradient.  -> (out, grad_x | None, grad_theta)."""
+        import torch
+        B = int(x.shape[0])
+        dev = x.device
+        out = torch.empty(B, dtype=torch.float64, device=dev)
+        jac = torch.empty((B, plan.n_vars), dtype=torch.float64, device=dev)
+        gx = torch.empty((B, plan.n_inputs), dtype=torch.float64, device=dev) if want_x else None
+        gt = torch.empty(max(plan.n_params, 1), dtype=torch.float64, device=dev)
+        st = plan._on_device(x, theta, upstream)
+        ws, _ = plan._ws(B, self._nat.HQ_WANT_JAC)
+        with torch.cuda.device(plan.device):
+            self._nat.check(self._lib.hq_backward_dp(
+                plan._h, x.data_ptr(), int(x.stride(0)), theta.data_ptr(), B, upstream.data_ptr(), out.data_ptr(),
+                jac.data_ptr(), gx.data_ptr() if gx is not None else None, gt.data_ptr(), self._h, ws.data_ptr(),
+                ws.numel(), st), "backward_dp")
+        return out, gx, gt[:plan.n_params]

@@ -98,3 +98,34 @@ def test_batch_sharding_evaluator_on_gpu():
     np.testing.assert_allclose(out, o, atol=1e-12)
     np.testing.assert_allclose(gx, gxo, atol=1e-12)
     np.testing.assert_allclose(gp, gpo, atol=1e-12)
+
+
+def test_library_communicator_single_rank():
+    """hq_comm_* with one rank (the only size one GPU allows): all-reduce is
+    the identity, the all-to-all copies the single chunk, and hq_backward_dp
+    equals hq_forward + hq_vjp."""
+    import torch
+    from paper_2301_03251_b200 import engine, qsim, templates as T, tracer as tr
+    comm = D.LibComm()
+    assert comm.world == 1
+    t = torch.arange(10, dtype=torch.float64, device="cuda")
+    comm.allreduce_(t)
+    torch.testing.assert_close(t, torch.arange(10, dtype=torch.float64, device="cuda"))
+    src = torch.randn(1 << 12, dtype=torch.complex128, device="cuda")
+    dst = torch.empty_like(src)
+    comm.alltoall(src, dst)
+    torch.cuda.synchronize()
+    assert torch.equal(src, dst)
+    b = wl.make_builder("cfg2", qsim, T)
+    x, th = wl.inputs_for("cfg2", 24), wl.params_for("cfg2")
+    tape, _ = tr.trace(b, x, th)
+    plan = engine.Plan(tape, 10, 60, "c128", tr.classify(tape, 70, [True] * 70, math.pi / 2, 0.5))
+    xd, td = torch.tensor(x, device="cuda"), torch.tensor(th, device="cuda")
+    up = torch.linspace(0.5, 1.5, 24, dtype=torch.float64, device="cuda")
+    out, gx, gt = comm.backward_dp(plan, xd, td, up, want_x=True)
+    o2, jac = plan.forward(xd, td, True)
+    gx2, gt2 = plan.vjp(jac, up, True, True)
+    torch.testing.assert_close(out, o2, rtol=0, atol=0)
+    torch.testing.assert_close(gx, gx2, rtol=0, atol=0)
+    torch.testing.assert_close(gt, gt2, rtol=0, atol=0)
+    comm.close()

@@ -773,3 +773,45 @@ def test_deferred_rz_phases_vs_oracle(prec, mode, monkeypatch):
     j = jac.cpu().numpy()
     check_vals(j[:, :2], jx, prec, grad=True, floor=1.0)
     check_vals(j[:, 2:], jp, prec, grad=True, floor=1.0)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_readout_invariant_diagonals_dropped(prec, monkeypatch):
+    """Diagonal gates that commute to the readout through monomial gates are
+    dropped from the readout plan (derivative 0 = the two-point value), while
+    amplitude output (hq_state, the unfolded twin) keeps them."""
+    monkeypatch.setenv("HQ_FORCE_STREAM", "1")
+    monkeypatch.setenv("HQ_TILE_BITS", "9")
+
+    def b(inputs, params, Circ=Circuit):
+        c = Circ(11)
+        for q in range(11):
+            c.ry(q, inputs[q % 2] + params[q])
+        for q in range(10):
+            c.cnot(q, q + 1)
+        c.rz(3, params[11])            # diagonal ...
+        c.cr(2, 7, params[12])
+        c.cnot(3, 5)                   # ... through a CNOT whose target is not in its support
+        c.rz(5, params[13])            # support {5}: CNOT(3,5) later widens it
+        c.cnot(3, 5)
+        c.x(7)
+        c.swap(1, 7)
+        c.cz(1, 4)
+        c.measure(0, 5, 7)
+        return c
+    rng = np.random.default_rng(11)
+    x = rng.uniform(-2, 2, (3, 2))
+    th = rng.uniform(0, 6, 14)
+    res, jac, info = engine.run_batch(b, x, th, True, True, prec, cache=engine.PlanCache(2))
+    assert "dropped_diag=4" in info["plan"].description
+    ob = lambda i, p: b(i, p, Circ=O.Circuit)
+    out, jx, jp, _, _ = O.layer(ob, x, th)
+    check_vals(res, out, prec, floor=1.0)
+    j = jac.cpu().numpy()
+    check_vals(j[:, :2], jx, prec, grad=True, floor=1.0)
+    check_vals(j[:, 2:], jp, prec, grad=True, floor=1.0)
+    assert np.all(j[:, 2 + 11:] == 0.0)                     # the dropped gates' parameters
+    # amplitudes keep every gate
+    c = b(list(x[0]), list(th))
+    st = engine.final_states([c], prec)[0]
+    np.testing.assert_allclose(st, O.simulate(ob(list(x[0]), list(th))), atol=1e-11 if prec == "c128" else 2e-6)

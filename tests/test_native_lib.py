@@ -19,7 +19,7 @@ from paper_2301_03251_b200.errors import CircuitError, ConfigError, EncodingErro
 
 def header_symbols():
     text = open(os.path.join(REPO, "include", "hq.h")).read()
-    return sorted(set(re.findall(r"\b(hq_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(hq_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_library_exports_header_symbols():
