@@ -16,6 +16,12 @@ def builder_for(n, depth, rng):
         two = k in ("CNOT", "CZ", "CR", "SWAP")
         tg = tuple(int(q) for q in rng.choice(n, 2 if two else 1, replace=False))
         plan.append((k, tg, int(rng.integers(0, 6))))
+    if rng.random() < 0.5:   # trailing diagonal / monomial gates (readout-invariant diagonals are dropped)
+        for _ in range(int(rng.integers(1, 8))):
+            k = ["RZ", "CZ", "CR", "Z", "X", "CNOT", "SWAP", "Y"][rng.integers(8)]
+            two = k in ("CNOT", "CZ", "CR", "SWAP")
+            tg = tuple(int(q) for q in rng.choice(n, 2 if two else 1, replace=False))
+            plan.append((k, tg, int(rng.integers(0, 6))))
     if rng.random() < 0.5:   # trailing permutation layer
         for q in range(n - 1):
             plan.append(("CNOT", (q, q + 1), 0))
