@@ -12,8 +12,8 @@ through the host.  :class:`TorchQuantumLayer` keeps everything on the device:
 * the builder is traced per input width (first call with that width, using
   the batch's first/last rows and a random probe — the same checks as the host
   layer, which reject value-dependent control flow).  With ``recheck=True``
-  (default) every later batch re-runs the builder on its own first and last
-  rows (a 2-row device->host copy) and raises ``CircuitError`` if the tape
+  (default) every later batch re-runs the builder once, on its own last row
+  (a 1-row device->host copy), and raises ``CircuitError`` if the tape
   changed; inside CUDA-graph capture, or with ``recheck=False``, the cached
   plan runs without any host synchronisation so forward+backward can be
   captured in a CUDA graph.
@@ -99,7 +99,11 @@ class TorchQuantumLayer(torch.nn.Module):
         if tape is None:
             tape = self._tapes[d] = self._trace(x)
         elif self.recheck and not torch.cuda.is_current_stream_capturing():
-            if not tape.same_as(self._trace(x)):
+            # cheap per-batch check: one traced builder call on the batch's last
+            # row (a 1-row device->host copy) against the cached tape
+            row = x[-1].detach().to("cpu", torch.float64).numpy()
+            other = tr.traced_call(self.circuit_builder, row, self.params.detach().cpu().numpy())
+            if not tape.same_as(other):
                 raise CircuitError("circuit builder produced a different circuit for this batch than "
                                    "the traced one (structure or angle expressions changed)")
         if x.device.type != "cuda":

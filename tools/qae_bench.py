@@ -13,12 +13,12 @@ for trash, total, B in ((2, 7, 256), (2, 12, 64)):
         out = layer(Tensor(x, dtype=np.float64))
         backward(tsum(out))
         layer.params.zero_grad()
-    step(); torch.cuda.synchronize()
-    t0 = time.perf_counter(); k = 3
-    for _ in range(k): step()
-    torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / k
+    step(); step(); torch.cuda.synchronize()       # the first call runs lazily, the second eagerly
+    ts = []
+    for _ in range(7):
+        t0 = time.perf_counter(); step(); torch.cuda.synchronize(); ts.append(time.perf_counter() - t0)
+    dt = float(np.median(ts))
     info = getattr(layer, "last_info", None)
     print(json.dumps({"trash": trash, "total": total, "batch": B, "params": int(layer.params.data.size),
-                      "s_per_step": dt, "samples_per_s": B / dt,
+                      "s_per_step": dt, "samples_per_s": B / dt, "stat": "median of 7 steps",
                       "plan": (info["plan"].description[:160] if info and "plan" in info else None)}), flush=True)
