@@ -191,9 +191,27 @@ struct Gen {
       vph[v].clear();
     }
   }
+  // complex128 shear-form phases (HQ_SHEAR_FLUSH, default on): the table
+  // holds (t, u) = (-tan(φ'/2), sin φ') of the folded angle |φ'| ≤ π/2 plus a
+  // sign word; a multiply by e^{iφ} is then 3 DFMA (x += t y; y += u x;
+  // x += t y) and a sign flip of the high words (LOP3, off the FP64 pipe)
+  // instead of 2 DMUL + 2 DFMA
+  bool shear_ph = false;
   void flush_one(int v, const std::map<int, int>& m, bool both) {
     if (m.empty()) return;
     const int k = ptab_find(m);
+    if (shear_ph) {
+      o << "{ const C ph_ = ptab_[" << k << "]; const int ng_ = ptsg_[" << k << "];\n";
+      for (int set = 0; set < (both ? 2 : 1); ++set) {
+        const std::string a = (set ? "l" : "p") + std::to_string(v);
+        o << a << ".x = fma(ph_.x, " << a << ".y, " << a << ".x); " << a << ".y = fma(ph_.y, " << a << ".x, " << a
+          << ".y); " << a << ".x = fma(ph_.x, " << a << ".y, " << a << ".x);\n"
+          << a << ".x = __hiloint2double(__double2hiint(" << a << ".x) ^ ng_, __double2loint(" << a << ".x)); "
+          << a << ".y = __hiloint2double(__double2hiint(" << a << ".y) ^ ng_, __double2loint(" << a << ".y));\n";
+      }
+      o << "}\n";
+      return;
+    }
     o << "{ const C ph_ = ptab_[" << k << "];\n";
     cmul_amp("p" + std::to_string(v), "ph_.x", "ph_.y");
     if (both) cmul_amp("l" + std::to_string(v), "ph_.x", "ph_.y");
@@ -820,6 +838,10 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   g.c64 = c64;
   g.packed = c64 && !std::getenv("HQ_NO_F32X2");
   g.exact = false;  // hq_state corrects the dropped RZ phases / rotation signs in the last pass
+  {
+    const char* e = std::getenv("HQ_SHEAR_FLUSH");
+    g.shear_ph = !c64 && !(e && e[0] == '0');
+  }
   {
     const char* e = std::getenv("HQ_DEFER_RZ");
     g.defer = !(e && e[0] == '0');
@@ -1584,7 +1606,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     arr("signed char", "_ptk", mu);
     decl = d.str();
     const int K = (int)g.ptab.size();
-    b << "__shared__ C ptab_[" << K << "];\n"
+    b << "__shared__ C ptab_[" << K << "];\n" << (g.shear_ph ? "__shared__ int ptsg_[" + std::to_string(K) + "];\n" : "")
       << "for (int j_ = tidw; j_ < " << K << "; j_ += " << L.block << ") { R x_ = (R)1, y_ = (R)0;\n"
       << "  for (int m_ = " << nm << "_pto[j_]; m_ < " << nm << "_pto[j_ + 1]; ++m_) { const int s_ = " << nm
       << "_pts[m_], k_ = " << nm << "_ptk[m_];\n"
@@ -1592,7 +1614,12 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       << "    const R c_ = trig[8 * s_ + 2], sn_ = k_ < 0 ? -trig[8 * s_ + 3] : trig[8 * s_ + 3];\n"
       << "    for (int r_ = 0; r_ < (k_ < 0 ? -k_ : k_); ++r_) { const R t_ = x_ * c_ - y_ * sn_; y_ = x_ * sn_ + y_ * c_; "
          "x_ = t_; } }\n"
-      << "  ptab_[j_].x = x_; ptab_[j_].y = y_; }\n__syncthreads();\n";
+      << (g.shear_ph
+              ? "  { double f_ = atan2((double)y_, (double)x_); int ng_ = 0;\n"
+                "    if (f_ > 1.5707963267948966) { f_ -= 3.141592653589793; ng_ = (int)0x80000000; }\n"
+                "    else if (f_ < -1.5707963267948966) { f_ += 3.141592653589793; ng_ = (int)0x80000000; }\n"
+                "    ptab_[j_].x = (R)(-tan(0.5 * f_)); ptab_[j_].y = (R)sin(f_); ptsg_[j_] = ng_; } }\n__syncthreads();\n"
+              : "  ptab_[j_].x = x_; ptab_[j_].y = y_; }\n__syncthreads();\n");
     build = b.str();
   }
   body.replace(body.find("/*HQ_PTAB_BUILD*/"), std::strlen("/*HQ_PTAB_BUILD*/"), build);
