@@ -191,7 +191,7 @@ struct Gen {
       vph[v].clear();
     }
   }
-  // complex128 shear-form phases (HQ_SHEAR_FLUSH, default on): the table
+  // complex128 shear-form phases (HQ_SHEAR_FLUSH=1, opt-in): the table
   // holds (t, u) = (-tan(φ'/2), sin φ') of the folded angle |φ'| ≤ π/2 plus a
   // sign word; a multiply by e^{iφ} is then 3 DFMA (x += t y; y += u x;
   // x += t y) and a sign flip of the high words (LOP3, off the FP64 pipe)
@@ -839,8 +839,11 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   g.packed = c64 && !std::getenv("HQ_NO_F32X2");
   g.exact = false;  // hq_state corrects the dropped RZ phases / rotation signs in the last pass
   {
+    // opt-in: fewer FP64 ops (b2: 3,172 -> 3,009) but more ALU ones, and
+    // measured slower (cfg4 B=1024 fwd / bwd 96.0 / 285 -> 98.6 / 292.7 ms,
+    // profiles/r02_shear.log)
     const char* e = std::getenv("HQ_SHEAR_FLUSH");
-    g.shear_ph = !c64 && !(e && e[0] == '0');
+    g.shear_ph = !c64 && e && e[0] == '1';
   }
   {
     const char* e = std::getenv("HQ_DEFER_RZ");
