@@ -348,7 +348,9 @@ class GpuExecutor:
     def _plan(self, sc, i, rank):
         from . import engine
         tape, grad = sc.segment(i, rank)
-        key = (id(sc), engine.tape_key(tape), tuple(grad[0]))
+        # everything a plan depends on (not the ShardedCircuit's identity)
+        key = (engine.tape_key(tape), sc.n_inputs, sc.n_params, sc.precision, tuple(grad[0]), tuple(grad[1]),
+               tuple(grad[2]), sc.shift, sc.grad_scale)
         if key not in self.plans:
             import torch
             with torch.cuda.device(self.device):
@@ -411,7 +413,7 @@ def run_nccl(sc: ShardedCircuit, theta, rank: int, world: int, device, x_row=(),
     if rank == 0:
         psi[0] = 1.0
     lam = [torch.empty_like(psi)] if want_grad else None
-    spare = [torch.empty_like(psi)]
+    spare = [torch.empty_like(psi) if sc.sched.exchanges else None]   # all-to-all needs a second buffer
 
     def exchange(bufs):
         # all g rank bits <-> the top g local bits: contiguous equal chunks
