@@ -160,6 +160,14 @@ hq_status hq_sample(const double* state, int64_t rows, int32_t n_qubits, const i
                     int32_t n_measured, int64_t shots, uint64_t seed, uint64_t* counts,
                     double* expectation, void* workspace, size_t workspace_bytes, void* stream);
 
+/* marginal Born probabilities of each row of `state` ([rows, 2^n, 2]
+ * complex128, device) over `measured` (host list, outcome bit i =
+ * measured[i]): probs [rows, 2^m] (device), fixed-order sums.
+ * Replaces probabilities (qsim.py:194-211) for device-resident states. */
+size_t hq_marginal_workspace_bytes(int64_t rows, int32_t n_qubits, int32_t n_measured);
+hq_status hq_marginal(const double* state, int64_t rows, int32_t n_qubits, const int32_t* measured,
+                      int32_t n_measured, double* probs, void* workspace, size_t workspace_bytes, void* stream);
+
 /* u_s for s in [shot0, shot0 + count): the per-shot uniform stream of shot_rng (qsim.py:222-224) */
 hq_status hq_shot_uniforms(uint64_t seed, int64_t shot0, int64_t count, double* out, void* stream);
 

@@ -25,7 +25,8 @@ EXPORTS = ("hq_abi_version", "hq_last_error", "hq_plan_create", "hq_plan_destroy
            "hq_shot_uniforms", "hq_noisy_workspace_bytes", "hq_noisy", "hq_launch_counts",
            "hq_plan_create_segment", "hq_seg_workspace_bytes", "hq_seg_forward", "hq_seg_backward",
            "hq_shard_readout_workspace_bytes", "hq_shard_readout", "hq_comm_id_bytes", "hq_comm_unique_id",
-           "hq_comm_init", "hq_comm_destroy", "hq_comm_allreduce_f64", "hq_comm_alltoall", "hq_backward_dp")
+           "hq_comm_init", "hq_comm_destroy", "hq_comm_allreduce_f64", "hq_comm_alltoall", "hq_backward_dp",
+           "hq_marginal_workspace_bytes", "hq_marginal")
 K_CLASSES = ("onchip", "pass_fwd", "pass_bwd", "other")
 
 
@@ -150,6 +151,10 @@ def lib():
     h.hq_backward_dp.argtypes = [_P, _P, ctypes.c_int64, _P, ctypes.c_int64, _P, _P, _P, _P, _P, _P, _P,
                                  ctypes.c_size_t, _P]
     h.hq_backward_dp.restype = ctypes.c_int
+    h.hq_marginal_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32]
+    h.hq_marginal_workspace_bytes.restype = ctypes.c_size_t
+    h.hq_marginal.argtypes = [_P, ctypes.c_int64, ctypes.c_int32, _P, ctypes.c_int32, _P, _P, ctypes.c_size_t, _P]
+    h.hq_marginal.restype = ctypes.c_int
     if h.hq_abi_version() != 2:
         raise NativeError(f"libhq ABI {h.hq_abi_version()} != 2")
     _lib = h

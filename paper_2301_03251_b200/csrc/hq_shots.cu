@@ -186,3 +186,57 @@ extern "C" hq_status hq_shot_uniforms(uint64_t seed, int64_t shot0, int64_t coun
   return e == cudaSuccess ? HQ_OK
                           : hq::fail_status(HQ_E_CUDA, std::string("hq_shot_uniforms launch: ") + cudaGetErrorString(e));
 }
+
+// ---- marginal Born probabilities on the device (qsim.py:194-211) ----------
+namespace hq {
+__global__ void k_marginal_fold(const double* part, int64_t rows, int32_t m, int32_t chunk_bits, double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nout = 1ll << m, nch = 1ll << chunk_bits;
+  if (i >= rows * nout) return;
+  double p = 0.0;
+  for (int64_t c = 0; c < nch; ++c) p += part[i * nch + c];   // fixed chunk order
+  out[i] = p;
+}
+}  // namespace hq
+
+extern "C" size_t hq_marginal_workspace_bytes(int64_t rows, int32_t n_qubits, int32_t n_measured) {
+  if (rows <= 0 || n_measured < 1 || n_measured > n_qubits) return 256;
+  const int cb = chunk_bits_for(rows, n_qubits, n_measured);
+  return (size_t)rows * ((size_t)1 << n_measured) * ((size_t)1 << cb) * 8 + 256;
+}
+
+extern "C" hq_status hq_marginal(const double* state, int64_t rows, int32_t n_qubits, const int32_t* measured,
+                                 int32_t n_measured, double* probs, void* ws, size_t ws_bytes, void* stream) {
+  if (rows <= 0) return HQ_OK;
+  if (!state || !probs) return hq::fail_status(HQ_E_CONFIG, "hq_marginal: null state / output");
+  if (n_qubits < 1 || n_qubits > 34 || n_measured < 1 || n_measured > n_qubits || !measured)
+    return hq::fail_status(HQ_E_CIRCUIT, "hq_marginal: need 1 <= n_measured <= n_qubits <= 34 and a measured list");
+  if (!ws || ws_bytes < hq_marginal_workspace_bytes(rows, n_qubits, n_measured))
+    return hq::fail_status(HQ_E_CONFIG, "hq_marginal: workspace too small");
+  hq::SampleArgs a{};
+  a.state = state;
+  a.rows = rows;
+  a.n = n_qubits;
+  a.m = n_measured;
+  uint64_t mask = 0;
+  for (int k = 0; k < n_measured; ++k) {
+    if (measured[k] < 0 || measured[k] >= n_qubits || (mask >> measured[k] & 1))
+      return hq::fail_status(HQ_E_CIRCUIT, "hq_marginal: measured qubit out of range or repeated");
+    mask |= 1ull << measured[k];
+    a.measured[k] = measured[k];
+  }
+  int u = 0;
+  for (int q = 0; q < n_qubits; ++q)
+    if (!(mask >> q & 1)) a.unmeasured[u++] = q;
+  a.chunk_bits = chunk_bits_for(rows, n_qubits, n_measured);
+  a.part = static_cast<double*>(ws);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t t1 = (int64_t)rows << (n_measured + a.chunk_bits);
+  hq::count_launch(HQ_K_OTHER);
+  hq::k_marginal_part<<<(unsigned)((t1 + 255) / 256), 256, 0, st>>>(a);
+  const int64_t t2 = (int64_t)rows << n_measured;
+  hq::count_launch(HQ_K_OTHER);
+  hq::k_marginal_fold<<<(unsigned)((t2 + 255) / 256), 256, 0, st>>>(a.part, rows, n_measured, a.chunk_bits, probs);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? HQ_OK : hq::fail_status(HQ_E_CUDA, std::string("hq_marginal launch: ") + cudaGetErrorString(e));
+}

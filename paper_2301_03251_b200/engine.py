@@ -531,6 +531,24 @@ def shard_readout(psi, n_local: int, precision: str, pos, wk, w0: float, lam=Non
     return e
 
 
+def marginal_probabilities(states, n_qubits: int, measured):
+    """states: cuda f64 [rows, 2^n, 2] -> cuda f64 [rows, 2^m] (hq_marginal;
+    outcome bit i = measured[i], qsim.py:194-211)."""
+    torch = _torch()
+    L = nat.lib()
+    rows = int(states.shape[0])
+    m = len(measured)
+    meas = (ctypes.c_int32 * max(m, 1))(*[int(q) for q in measured])
+    out = torch.empty((rows, 1 << m), dtype=torch.float64, device=states.device)
+    nb = int(L.hq_marginal_workspace_bytes(rows, n_qubits, m))
+    ws = torch.empty(nb, dtype=torch.uint8, device=states.device)
+    st = states.contiguous()
+    with torch.cuda.device(states.device):
+        nat.check(L.hq_marginal(_ptr(st), rows, int(n_qubits), meas, m, _ptr(out), _ptr(ws), nb,
+                                torch.cuda.current_stream(states.device).cuda_stream), "marginal")
+    return out
+
+
 def sample_states(states, n_qubits: int, measured, shots: int, seed: int, want_counts: bool = False):
     """states: cuda f64 [rows, 2^n, 2] -> (expectation [rows] cuda, counts [rows, 2^m] | None)."""
     torch = _torch()

@@ -203,9 +203,14 @@ def shot_rng(seed: int, shot: int):
     return _sr(seed, shot)
 
 
-def probabilities(state: StateVector, qubits) -> np.ndarray:
+def probabilities(state, qubits):
     """Marginal Born distribution over ``qubits``; outcome bit i = qubits[i]
-    (``qsim.py:194-211``).  Host-side: the state is already a host copy."""
+    (``qsim.py:194-211``).  A host ``StateVector`` (the reference's type) is
+    reduced on the host copy; a device state — a CUDA tensor of amplitudes
+    ([2^n] complex, or [rows, 2^n] / [rows, 2^n, 2] batches) — is reduced on
+    the GPU by ``hq_marginal`` and the result stays on the device."""
+    if hasattr(state, "is_cuda") and state.is_cuda:
+        return _device_probabilities(state, qubits)
     qubits = [int(q) for q in qubits]
     if len(set(qubits)) != len(qubits):
         raise CircuitError(f"duplicate qubits in {qubits}")
@@ -218,6 +223,29 @@ def probabilities(state: StateVector, qubits) -> np.ndarray:
     for i, q in enumerate(qubits):
         outcome |= ((idx >> q) & 1) << i
     return np.bincount(outcome, weights=p, minlength=1 << len(qubits))
+
+
+def _device_probabilities(state, qubits):
+    import torch
+    from . import engine
+    if state.is_complex():                      # [2^n] or [rows, 2^n]
+        single = state.dim() == 1
+        t = torch.view_as_real(state.to(torch.complex128).contiguous())
+    else:                                       # [2^n, 2] or [rows, 2^n, 2]
+        single = state.dim() == 2
+        t = state.to(torch.float64)
+    t = t.reshape(1 if single else t.shape[0], -1, 2)
+    n = int(t.shape[1]).bit_length() - 1
+    if 1 << n != t.shape[1]:
+        raise CircuitError(f"{t.shape[1]} amplitudes is not a power of two")
+    qubits = [int(q) for q in qubits]
+    if len(set(qubits)) != len(qubits):
+        raise CircuitError(f"duplicate qubits in {qubits}")
+    for q in qubits:
+        if not 0 <= q < n:
+            raise CircuitError(f"qubit {q} out of range for {n} qubits")
+    p = engine.marginal_probabilities(t.contiguous(), n, qubits)
+    return p[0] if single else p
 
 
 def readout_weights(n_qubits: int, measured) -> list:

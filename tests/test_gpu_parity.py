@@ -815,3 +815,22 @@ def test_readout_invariant_diagonals_dropped(prec, monkeypatch):
     c = b(list(x[0]), list(th))
     st = engine.final_states([c], prec)[0]
     np.testing.assert_allclose(st, O.simulate(ob(list(x[0]), list(th))), atol=1e-11 if prec == "c128" else 2e-6)
+
+
+def test_device_probabilities_match_host():
+    """qsim.probabilities on a device state (hq_marginal) equals the host
+    reduction of the reference's StateVector path, outcome bit order included."""
+    import torch
+    rng = np.random.default_rng(5)
+    for n, meas in ((3, [2, 0]), (9, [4]), (12, [0, 11, 5])):
+        z = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+        z /= np.linalg.norm(z)
+        host = qsim.probabilities(qsim.StateVector.from_amplitudes(z), meas)
+        dev = qsim.probabilities(torch.tensor(z, device="cuda"), meas)
+        assert dev.is_cuda
+        np.testing.assert_allclose(dev.cpu().numpy(), host, rtol=0, atol=1e-15)
+        batch = torch.tensor(np.stack([z, z[::-1].copy()]), device="cuda")
+        both = qsim.probabilities(batch, meas).cpu().numpy()
+        np.testing.assert_allclose(both[0], host, atol=1e-15)
+        np.testing.assert_allclose(both[1], qsim.probabilities(qsim.StateVector.from_amplitudes(z[::-1].copy()), meas),
+                                   atol=1e-15)
