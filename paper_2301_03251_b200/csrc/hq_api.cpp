@@ -284,6 +284,9 @@ std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int 
   // qubit top-up): cfg4 17 -> 8 passes, 4,676 -> 5,646 samples/s
   size_t max_ops = op_cap;   // HQ_MAX_PASS_OPS: test hook (code size per pass kernel)
   if (const char* e = std::getenv("HQ_MAX_PASS_OPS")) max_ops = std::max<size_t>(8, std::min<size_t>(kMaxPassOps, std::atoll(e)));
+  // HQ_FIRST_PASS_OPS: cap of the first pass only (its kernels are the largest)
+  size_t first_ops = max_ops;
+  if (const char* e = std::getenv("HQ_FIRST_PASS_OPS")) first_ops = std::max<size_t>(8, std::min<size_t>(max_ops, std::atoll(e)));
   const char* pla = std::getenv("HQ_PASS_LOOKAHEAD");
   const bool lookahead = !(pla && pla[0] == '0');
   const bool depth2 = pla && pla[0] == '2';
@@ -417,7 +420,7 @@ std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int 
         const uint64_t qs = op_mask(ops[k]);
         if (qs & blocked) { blocked |= qs; continue; }
         const uint64_t ex = exch_mask(ops[k]);
-        if (ps.op_ids.size() >= max_ops) { blocked |= qs; continue; }
+        if (ps.op_ids.size() >= (passes.empty() ? first_ops : max_ops)) { blocked |= qs; continue; }
         const uint64_t excl = passes.empty() ? excl0 : 0;
         if (!(ex & excl) && ((ex & ~L) == 0 || popc(L | ex) <= q)) {
           L |= ex;
