@@ -275,7 +275,7 @@ namespace {
 // excl0: qubits that must stay out of the first pass's tile (their folded
 // gates' gradients are read from λ contracted over that tile)
 std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int q, int f, uint64_t excl0 = 0,
-                                      size_t op_cap = kMaxPassOps) {
+                                      size_t op_cap = kMaxPassOps, size_t first_cap = 0) {
   std::vector<hq::Pass> passes;
   std::vector<char> done(ops.size(), 0);
   size_t left = ops.size();
@@ -285,7 +285,7 @@ std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int 
   size_t max_ops = op_cap;   // HQ_MAX_PASS_OPS: test hook (code size per pass kernel)
   if (const char* e = std::getenv("HQ_MAX_PASS_OPS")) max_ops = std::max<size_t>(8, std::min<size_t>(kMaxPassOps, std::atoll(e)));
   // HQ_FIRST_PASS_OPS: cap of the first pass only (its kernels are the largest)
-  size_t first_ops = max_ops;
+  size_t first_ops = first_cap ? std::min(first_cap, max_ops) : max_ops;
   if (const char* e = std::getenv("HQ_FIRST_PASS_OPS")) first_ops = std::max<size_t>(8, std::min<size_t>(max_ops, std::atoll(e)));
   const char* pla = std::getenv("HQ_PASS_LOOKAHEAD");
   const bool lookahead = !(pla && pla[0] == '0');
@@ -994,11 +994,55 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
     // (profiles/r01_c128_pass_cap.log).
     const size_t op_cap = (opts & kSmallPasses) ? 48 : kMaxPassOps;
     const bool try_cap = !(opts & kSmallPasses) && d->precision == HQ_C128;
+    // register windows a schedule needs (plan_windows on each pass's ops)
+    auto count_windows = [&](const std::vector<hq::Pass>& sched) {
+      size_t w = 0;
+      for (const auto& ps : sched) {
+        int pos[kMaxQubits];
+        for (int b = 0; b < n; ++b) pos[b] = ~b;
+        for (int i = 0; i < (int)ps.local.size(); ++i) pos[ps.local[i]] = i;
+        std::vector<hq::DOp> pops;
+        for (int k : ps.op_ids) {
+          const hq_op& g = gates[k];
+          hq::DOp o{};
+          o.kind = g.kind;
+          o.a = pos[g.q0];
+          o.b = two_qubit(g.kind) ? pos[g.q1] : -1;
+          o.slot = -1;
+          o.dslot = -1;
+          pops.push_back(o);
+        }
+        hq::Pass tmp = ps;
+        plan_windows(tmp, pops, pl->tile_bits, RB, f);
+        w += tmp.wins.size();
+      }
+      return w;
+    };
+    // Schedule search: the first pass's op cap (and, for complex128, the
+    // 140-op cap of every pass) is chosen by a cost model over register
+    // windows and passes — each window transition and each HBM sweep costs
+    // about the same in the complex128 kernels (cfg4, B=1024: ~2.4 ms each),
+    // while complex64 passes are ~8x a window (HBM-bound sweeps): cost =
+    // windows + k·passes, k = 1 (c128) / 8 (c64).  cfg4 c128: first pass
+    // 140 -> 120 ops, 57 -> 53 windows, 379.6 -> 369.8 ms forward+adjoint
+    // (profiles/r02_firstpass.log).  HQ_PLAN_SEARCH=0: the round-1 rule.
+    const char* ps_env = std::getenv("HQ_PLAN_SEARCH");
+    const bool search = !(ps_env && ps_env[0] == '0') && !(opts & kSmallPasses) && !std::getenv("HQ_FIRST_PASS_OPS");
+    const size_t pass_w = d->precision == HQ_C64 ? 8 : 1;
     auto schedule = [&](uint64_t excl0) {
       auto best = schedule_passes(gates, n, pl->tile_bits, f, excl0, op_cap);
       if (try_cap) {
         auto capped = schedule_passes(gates, n, pl->tile_bits, f, excl0, kC128PassOps);
         if (capped.size() < best.size()) best.swap(capped);
+      }
+      const size_t first = best.empty() ? 0 : best[0].op_ids.size();
+      if (!search || best.size() < 4 || first < 64) return best;   // small plans: nothing to gain
+      size_t best_cost = count_windows(best) + pass_w * best.size();
+      const size_t oc = (try_cap && best[0].op_ids.size() <= kC128PassOps) ? kC128PassOps : op_cap;
+      for (int pct : {95, 91, 87, 83, 79, 75}) {
+        auto cand = schedule_passes(gates, n, pl->tile_bits, f, excl0, oc, first * pct / 100);
+        const size_t cost = count_windows(cand) + pass_w * cand.size();
+        if (cost < best_cost) { best_cost = cost; best.swap(cand); }
       }
       return best;
     };
