@@ -461,7 +461,7 @@ uint16_t swz_host(uint32_t j) { return (uint16_t)(j ^ (((j >> 4) ^ (j >> 8)) & 1
 // Split one pass's ops (tile-bit operands) into register windows (see
 // hq_window.cuh): same greedy as the pass scheduler, capacity kRegBits, over
 // the exchange qubits; controls / diagonal qubits may be thread bits.
-void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, int fixed) {
+void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, int fixed, bool rollout = true) {
   auto exch = [](const hq::DOp& o) -> uint32_t {
     switch (o.kind) {
       case HQ_GATE_H: case HQ_GATE_X: case HQ_GATE_Y: case HQ_GATE_RX: case HQ_GATE_RY:
@@ -525,11 +525,11 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
     }
     return true;
   };
-  auto admitted = [&](uint32_t R) {
+  auto admitted_in = [&](uint32_t R, const std::vector<char>& dn) {
     int cnt = 0;
     uint32_t blocked = 0;
     for (size_t k = 0; k < ops.size(); ++k) {
-      if (done[k]) continue;
+      if (dn[k]) continue;
       const uint32_t qs = qmask(ops[k]);
       if (qs & blocked) { blocked |= qs; continue; }
       if ((exch(ops[k]) & ~R) == 0) ++cnt;
@@ -537,9 +537,96 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
     }
     return cnt;
   };
+  auto admitted = [&](uint32_t R) { return admitted_in(R, done); };
+  const uint32_t fmask_all = fixed >= 32 ? ~0u : ((1u << fixed) - 1u);
+  // lookahead candidates: (score, register set), best first
+  auto candidates = [&](const std::vector<char>& dn, bool with_shfl) {
+    std::vector<std::pair<int, uint32_t>> out;
+    uint32_t cand = 0;
+    int seen = 0;
+    for (size_t k = 0; k < ops.size() && seen < 48; ++k)
+      if (!dn[k]) { cand |= exch(ops[k]); ++seen; }
+    std::vector<int> cb;
+    for (int b = 0; b < q; ++b)
+      if (cand >> b & 1u) cb.push_back(b);
+    if ((int)cb.size() <= RB || cb.size() > 16) return out;
+    const int nc = (int)cb.size();
+    for (uint32_t sel = 0; sel < (1u << nc); ++sel) {
+      if (popc(sel) != RB) continue;
+      uint32_t R = 0;
+      for (int i = 0; i < nc; ++i)
+        if (sel >> i & 1u) R |= 1u << cb[i];
+      if (!class_ok(R)) continue;
+      const int sc = 2 * admitted_in(R, dn) + ((R & fmask_all) ? 0 : 1) + (with_shfl && shfl_able(R) ? shfl_bonus : 0);
+      if (sc > 1) out.push_back({sc, R});
+    }
+    std::stable_sort(out.begin(), out.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    return out;
+  };
+  auto class_left_of = [&](uint32_t m, int cls) {
+    int c = 0;
+    for (int b = 0; b < q; ++b)
+      if (!(m >> b & 1u) && (b & 3) == cls) ++c;
+    return c;
+  };
+  // admit ops into a window with register set Rm (scan, top-up, rescan) — the
+  // rollout's copy of the main loop below, without emitting anything
+  auto admit_sim = [&](uint32_t Rm, std::vector<char>& dn) {
+    bool progress = true, first_scan = true;
+    size_t n_adm = 0;
+    while (progress) {
+      progress = false;
+      uint32_t blocked = 0;
+      for (size_t k = 0; k < ops.size(); ++k) {
+        if (dn[k]) continue;
+        const uint32_t qs = qmask(ops[k]);
+        if (qs & blocked) { blocked |= qs; continue; }
+        const uint32_t ex = exch(ops[k]);
+        if ((ex & ~Rm) == 0 || popc(Rm | ex) <= RB) { Rm |= ex; dn[k] = 1; ++n_adm; progress = true; }
+        else blocked |= qs;
+      }
+      if (first_scan) {
+        for (int pass2 = 0; pass2 < 2; ++pass2)
+          for (int b = q - 1; b >= 0 && popc(Rm) < RB; --b)
+            if (!(Rm >> b & 1u) && (pass2 == 1 || class_left_of(Rm, b & 3) > 1)) Rm |= 1u << b;
+        first_scan = false;
+        progress = true;
+      }
+    }
+    return n_adm;
+  };
+  // windows the greedy lookahead needs to finish from state dn
+  auto rollout_windows = [&](std::vector<char> dn) {
+    int w = 0;
+    for (;;) {
+      bool any = false;
+      for (char c : dn) if (!c) { any = true; break; }
+      if (!any) return w;
+      auto cs = candidates(dn, false);
+      if (admit_sim(cs.empty() ? 0u : cs[0].second, dn) == 0) return w + 1000;   // no progress: give up
+      ++w;
+    }
+  };
+  // Window rollouts (opt-in, HQ_WIN_ROLLOUT = number of candidates): the best
+  // few lookahead register sets are each followed by a greedy rollout of the
+  // rest of the pass and the one finishing in the fewest windows wins.  On
+  // cfg4 the lookahead is already at the rollout optimum (c128: same 53
+  // windows with 4 or 8 candidates; c64: 34 -> 33), so it stays off.
+  int n_roll = 0;
+  if (const char* e = std::getenv("HQ_WIN_ROLLOUT")) n_roll = std::atoi(e);
+  if (!rollout || shfl) n_roll = 0;
   do {
     uint32_t Rm = 0;
-    if (lookahead) {
+    if (lookahead && n_roll > 1) {
+      auto cs = candidates(done, false);
+      int best_w = 1 << 30, best_sc = -1;
+      for (int c = 0; c < (int)cs.size() && c < n_roll; ++c) {
+        std::vector<char> dn(done);
+        if (admit_sim(cs[c].second, dn) == 0) continue;
+        const int w = 1 + rollout_windows(dn);
+        if (w < best_w || (w == best_w && cs[c].first > best_sc)) { best_w = w; best_sc = cs[c].first; Rm = cs[c].second; }
+      }
+    } else if (lookahead) {
       uint32_t cand = 0;
       int seen = 0;
       for (size_t k = 0; k < ops.size() && seen < 48; ++k)
@@ -1013,7 +1100,7 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
           pops.push_back(o);
         }
         hq::Pass tmp = ps;
-        plan_windows(tmp, pops, pl->tile_bits, RB, f);
+        plan_windows(tmp, pops, pl->tile_bits, RB, f, false);
         w += tmp.wins.size();
       }
       return w;
