@@ -286,6 +286,19 @@ std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int 
   if (const char* e = std::getenv("HQ_MAX_PASS_OPS")) max_ops = std::max<size_t>(8, std::min<size_t>(kMaxPassOps, std::atoll(e)));
   // HQ_FIRST_PASS_OPS: cap of the first pass only (its kernels are the largest)
   size_t first_ops = first_cap ? std::min(first_cap, max_ops) : max_ops;
+  // HQ_PASS_CAPS="c0,c1,...": per-pass op caps (planner experiments; 0 = none)
+  std::vector<size_t> pass_caps;
+  if (const char* e = std::getenv("HQ_PASS_CAPS")) {
+    std::string v(e);
+    size_t p0 = 0;
+    while (p0 <= v.size()) {
+      const size_t p1 = v.find(',', p0);
+      pass_caps.push_back((size_t)std::atoll(v.substr(p0, p1 == std::string::npos ? std::string::npos : p1 - p0).c_str()));
+      if (p1 == std::string::npos) break;
+      p0 = p1 + 1;
+    }
+    if (!pass_caps.empty() && pass_caps[0]) first_ops = pass_caps[0];
+  }
   if (const char* e = std::getenv("HQ_FIRST_PASS_OPS")) first_ops = std::max<size_t>(8, std::min<size_t>(max_ops, std::atoll(e)));
   const char* pla = std::getenv("HQ_PASS_LOOKAHEAD");
   const bool lookahead = !(pla && pla[0] == '0');
@@ -420,7 +433,11 @@ std::vector<hq::Pass> schedule_passes(const std::vector<hq_op>& ops, int n, int 
         const uint64_t qs = op_mask(ops[k]);
         if (qs & blocked) { blocked |= qs; continue; }
         const uint64_t ex = exch_mask(ops[k]);
-        if (ps.op_ids.size() >= (passes.empty() ? first_ops : max_ops)) { blocked |= qs; continue; }
+        if (ps.op_ids.size() >= (passes.empty() ? first_ops : (passes.size() < pass_caps.size() && pass_caps[passes.size()]
+                                                                   ? pass_caps[passes.size()] : max_ops))) {
+          blocked |= qs;
+          continue;
+        }
         const uint64_t excl = passes.empty() ? excl0 : 0;
         if (!(ex & excl) && ((ex & ~L) == 0 || popc(L | ex) <= q)) {
           L |= ex;
@@ -1265,6 +1282,13 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
     if (hq::jit_build(pl, why) != HQ_OK) pl->jit.small = nullptr;
   }
   if (!pl->onchip && std::getenv("HQ_PLAN_WINDOWS")) {
+    if (std::getenv("HQ_PLAN_ONLY")) {   // planner experiments: print and stop before the JIT
+      std::fprintf(stderr, "hq windows:");
+      for (const auto& ps2 : pl->passes) std::fprintf(stderr, " %d/%zu", ps2.n_dops, ps2.wins.size());
+      std::fprintf(stderr, "\n");
+      delete pl;
+      return fail(HQ_E_CONFIG, "plan-only");
+    }
     std::fprintf(stderr, "hq windows:");
     for (const auto& ps : pl->passes) std::fprintf(stderr, " %d/%zu", ps.n_dops, ps.wins.size());
     std::fprintf(stderr, "\n");
