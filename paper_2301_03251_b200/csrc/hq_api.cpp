@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -478,7 +479,8 @@ uint16_t swz_host(uint32_t j) { return (uint16_t)(j ^ (((j >> 4) ^ (j >> 8)) & 1
 // Split one pass's ops (tile-bit operands) into register windows (see
 // hq_window.cuh): same greedy as the pass scheduler, capacity kRegBits, over
 // the exchange qubits; controls / diagonal qubits may be thread bits.
-void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, int fixed, bool rollout = true) {
+void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, int fixed, bool rollout = true,
+                  bool warp_local = false) {
   auto exch = [](const hq::DOp& o) -> uint32_t {
     switch (o.kind) {
       case HQ_GATE_H: case HQ_GATE_X: case HQ_GATE_Y: case HQ_GATE_RX: case HQ_GATE_RY:
@@ -515,6 +517,10 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
   // The lookahead prefers such register sets by kShflBonus score points
   // (= half an admitted op each).
   const bool shfl = hq::shfl_enabled();
+  // (complex128 default: its kernels use the warp-local transitions; complex64
+  // keeps CTA barriers, measured faster there -- profiles/r02_warpsync.log)
+  bool keep_warps = warp_local;
+  if (const char* e = std::getenv("HQ_KEEP_WARPS")) keep_warps = std::atoi(e) != 0;
   int shfl_bonus = 3;
   if (const char* e = std::getenv("HQ_SHFL_BONUS")) shfl_bonus = std::atoi(e);
   std::vector<int> pR, pS;            // previous window's register / thread bits
@@ -632,6 +638,46 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
   int n_roll = 0;
   if (const char* e = std::getenv("HQ_WIN_ROLLOUT")) n_roll = std::atoi(e);
   if (!rollout || shfl) n_roll = 0;
+  struct WinTmp {
+    uint32_t Rm = 0, ctl = 0;
+    std::vector<int> R, S;
+    std::vector<size_t> exec;
+    bool shuffled = false;
+  };
+  std::vector<WinTmp> wins;
+  // thread bits of a window: lanes first (one per bank class, the fixed bits
+  // in their own slots, CNOT controls kept for the warp bits), then the warp
+  // bits -- the set W when given (ascending, so equal sets get equal slots)
+  auto thread_bits = [&](const WinTmp& wt, const std::vector<int>& W) {
+    uint32_t Wm = 0;
+    for (int b : W) Wm |= 1u << b;
+    std::vector<int> S, rest;
+    for (int b = 0; b < q; ++b)
+      if (!(wt.Rm >> b & 1u)) rest.push_back(b);
+    std::vector<char> used(rest.size(), 0);
+    for (size_t i = 0; i < rest.size(); ++i) used[i] = (Wm >> rest[i] & 1u) ? 1 : 0;
+    auto pick = [&](int cls) {   // lane bit of bank class cls (-1: any class)
+      int best = -1;
+      for (size_t i = 0; i < rest.size(); ++i) {
+        if (used[i] || (cls >= 0 && (rest[i] & 3) != cls)) continue;
+        if (rest[i] < fixed) { best = (int)i; break; }
+        const bool c = wt.ctl >> rest[i] & 1u;
+        if (best < 0 || (!c && (wt.ctl >> rest[best] & 1u))) best = (int)i;
+        if (!c) break;
+      }
+      if (best >= 0) { S.push_back(rest[best]); used[best] = 1; }
+    };
+    for (int cls = 0; cls < 4 && (int)S.size() < 5; ++cls) pick(cls);
+    while ((int)S.size() < 5 && S.size() < rest.size()) {
+      const size_t before = S.size();
+      pick(-1);
+      if (S.size() == before) break;
+    }
+    for (size_t i = 0; i < rest.size(); ++i)
+      if (!used[i]) S.push_back(rest[i]);
+    S.insert(S.end(), W.begin(), W.end());
+    return S;
+  };
   do {
     uint32_t Rm = 0;
     if (lookahead && n_roll > 1) {
@@ -717,24 +763,13 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
     // classes.  Controls of CNOTs whose control is not a register bit go to
     // warp bits where possible (warp-uniform branch instead of FSEL swaps);
     // bits below `fixed` keep their lane slots (direct HBM windows).
-    uint32_t ctl = 0;
+    WinTmp wt;
+    wt.Rm = Rm;
+    wt.exec = exec;
     for (size_t k : exec)
-      if (ops[k].kind == HQ_GATE_CNOT && ops[k].a >= 0 && !(Rm >> ops[k].a & 1u)) ctl |= 1u << ops[k].a;
-    std::vector<int> R, S, rest;
-    for (int b = 0; b < q; ++b) (Rm >> b & 1u ? R : rest).push_back(b);
-    std::vector<char> used(rest.size(), 0);
-    auto pick = [&](int cls) {   // lane bit of bank class cls (-1: any class)
-      int best = -1;
-      for (size_t i = 0; i < rest.size(); ++i) {
-        if (used[i] || (cls >= 0 && (rest[i] & 3) != cls)) continue;
-        if (rest[i] < fixed) { best = (int)i; break; }
-        const bool c = ctl >> rest[i] & 1u;
-        if (best < 0 || (!c && (ctl >> rest[best] & 1u))) best = (int)i;
-        if (!c) break;
-      }
-      if (best >= 0) { S.push_back(rest[best]); used[best] = 1; }
-    };
-    bool shuffled = false;
+      if (ops[k].kind == HQ_GATE_CNOT && ops[k].a >= 0 && !(Rm >> ops[k].a & 1u)) wt.ctl |= 1u << ops[k].a;
+    for (int b = 0; b < q; ++b)
+      if (Rm >> b & 1u) wt.R.push_back(b);
     if (shfl_able(Rm)) {
       // keep the previous thread-bit slots; each qubit entering the registers
       // from lane slot s hands that slot to a qubit leaving the registers
@@ -747,27 +782,109 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
       int cls = 0;
       for (int s2 = 0; s2 < n_lanes; ++s2) cls |= 1 << (S2[s2] & 3);
       if (oi == out.size() && (cls == 15 || q - RB < 5)) {
-        S = S2;
-        shuffled = true;
+        wt.S = S2;
+        wt.shuffled = true;
       }
     }
-    if (!shuffled) {
-      for (int cls = 0; cls < 4 && (int)S.size() < 5; ++cls) pick(cls);
-      while ((int)S.size() < 5 && S.size() < rest.size()) pick(-1);
-      for (size_t i = 0; i < rest.size(); ++i)
-        if (!used[i]) S.push_back(rest[i]);
+    if (!wt.shuffled && (shfl || !keep_warps)) wt.S = thread_bits(wt, {});
+    pR = wt.R;
+    pS = wt.S;
+    have_prev = true;
+    wins.push_back(wt);
+  } while (left > 0);
+
+  // Warp-local transitions (complex128 default; HQ_KEEP_WARPS=0/1 overrides):
+  // the warp-index bits of each window are chosen over the whole pass so that
+  // consecutive windows keep as many of them as possible in the same warp-bit
+  // slots.  The shared-memory exchange between two windows then only crosses
+  // warps that differ in the changed slots: all kept -> inside each warp
+  // (__syncwarp), some kept -> within groups of 2 or 4 warps (named barriers),
+  // none -> the whole CTA (hq_jit.cpp, post_store_sync).  DP over the window
+  // sequence: state = the ordered warp-bit tuple W (disjoint from the window's
+  // register bits and the fixed bits, leaving lanes that still cover every
+  // bank class); score per transition 16·kept/nwarp + the CNOT controls W
+  // covers (warp-uniform branches).
+  if (!shfl && keep_warps && !wins.empty() && q - RB > n_lanes) {
+    const int nwarp = q - RB - n_lanes;
+    std::vector<int> free_bits;
+    for (int b = 0; b < q; ++b)
+      if (!(fmask_all >> b & 1u)) free_bits.push_back(b);
+    // ordered tuples (sorted sets only when there would be too many)
+    size_t n_ord = 1;
+    for (int i = 0; i < nwarp; ++i) n_ord *= (free_bits.size() > (size_t)i ? free_bits.size() - i : 0);
+    const bool ordered = n_ord <= 1500;
+    std::vector<std::vector<int>> cand;
+    std::vector<int> cur;
+    std::function<void(uint32_t)> gen = [&](uint32_t usedm) {
+      if ((int)cur.size() == nwarp) { cand.push_back(cur); return; }
+      for (int b : free_bits) {
+        if (usedm >> b & 1u) continue;
+        if (!ordered && !cur.empty() && b < cur.back()) continue;
+        cur.push_back(b);
+        gen(usedm | 1u << b);
+        cur.pop_back();
+      }
+    };
+    gen(0u);
+    auto classes = [&](uint32_t m) {
+      int c = 0;
+      for (int b = 0; b < q; ++b)
+        if (m >> b & 1u) c |= 1 << (b & 3);
+      return c;
+    };
+    const size_t K = wins.size(), C = cand.size();
+    std::vector<uint32_t> cmask(C, 0u);
+    for (size_t c = 0; c < C; ++c)
+      for (int b : cand[c]) cmask[c] |= 1u << b;
+    const int NEG = -(1 << 28);
+    std::vector<std::vector<int>> dp(K, std::vector<int>(C, NEG)), from(K, std::vector<int>(C, -1));
+    for (size_t k = 0; k < K; ++k) {
+      const uint32_t restm = all & ~wins[k].Rm;
+      std::vector<int> prev_ok;
+      if (k > 0)
+        for (size_t c2 = 0; c2 < C; ++c2)
+          if (dp[k - 1][c2] > NEG) prev_ok.push_back((int)c2);
+      for (size_t c = 0; c < C; ++c) {
+        if ((cmask[c] & wins[k].Rm) || classes(restm & ~cmask[c]) != classes(restm)) continue;
+        const int own = popc(cmask[c] & wins[k].ctl);
+        if (k == 0) { dp[k][c] = own; continue; }
+        int v = NEG, f = -1;
+        for (int c2 : prev_ok) {
+          int kept = 0;
+          uint32_t km = 0;
+          for (int i = 0; i < nwarp; ++i)
+            if (cand[c][i] == cand[c2][i]) { ++kept; km |= 1u << i; }
+          if (kept < nwarp && !hq::group_barrier_base(nwarp, km)) kept = 0;   // no ids: CTA barrier
+          const int sc = dp[k - 1][c2] + 16 * kept / nwarp;
+          if (sc > v) { v = sc; f = c2; }
+        }
+        if (f < 0) continue;
+        dp[k][c] = v + own;
+        from[k][c] = f;
+      }
     }
+    int c = -1, bv = NEG;
+    for (size_t i = 0; i < C; ++i)
+      if (dp[K - 1][i] > bv) { bv = dp[K - 1][i]; c = (int)i; }
+    std::vector<std::vector<int>> Wsel(K);
+    bool ok = c >= 0;
+    for (size_t k = K; ok && k-- > 0;) {
+      Wsel[k] = cand[c];
+      if (k > 0) { c = from[k][c]; ok = c >= 0; }
+    }
+    for (size_t k = 0; k < K; ++k) wins[k].S = thread_bits(wins[k], ok ? Wsel[k] : std::vector<int>{});
+  }
+
+  for (const WinTmp& wt : wins) {
+    const std::vector<int>& R = wt.R;
+    const std::vector<int>& S = wt.S;
     if (std::getenv("HQ_WIN_DEBUG")) {
-      std::fprintf(stderr, "win ops=%zu %s R=", exec.size(), shuffled ? "shfl" : "smem");
+      std::fprintf(stderr, "win ops=%zu %s R=", wt.exec.size(), wt.shuffled ? "shfl" : "smem");
       for (int b : R) std::fprintf(stderr, "%d,", b);
       std::fprintf(stderr, " S=");
       for (int b : S) std::fprintf(stderr, "%d,", b);
       std::fprintf(stderr, "\n");
     }
-    pR = R;
-    pS = S;
-    have_prev = true;
-    (void)all;
     hq::WinDev w{};
     w.op0 = (int16_t)ps.wops.size();
     for (int i = 0; i < RB; ++i) w.pr[i] = swz_host(1u << R[i]);
@@ -778,7 +895,7 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
       for (size_t i = 0; i < S.size(); ++i) if (S[i] == x) return (int8_t)(16 + i);
       return (int8_t)-1;
     };
-    for (size_t k : exec) {
+    for (size_t k : wt.exec) {
       const hq::DOp& o = ops[k];
       hq::WOp wo{};
       wo.kind = (int8_t)o.kind;
@@ -791,7 +908,7 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
     }
     w.op1 = (int16_t)ps.wops.size();
     ps.wins.push_back(w);
-  } while (left > 0);
+  }
 }
 
 template <typename T>
@@ -1253,7 +1370,7 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
         pl->dops.push_back(o);
         pops.push_back(o);
       }
-      plan_windows(ps, pops, pl->tile_bits, RB, f);
+      plan_windows(ps, pops, pl->tile_bits, RB, f, true, pl->precision == HQ_C128);
       ps.n_dops = (int32_t)ps.op_ids.size();
       ps.n_dslots_pass = (int32_t)pass_dlist.size() - ps.first_dlist;
       ps.first_slotlist = (int32_t)pass_slots.size();

@@ -99,6 +99,27 @@ inline bool shfl_enabled() {
   const char* e = std::getenv("HQ_SHFL");
   return e && e[0] == '1';
 }
+// Named-barrier ids of the warp-group window transitions (hq_jit.cpp
+// post_store_sync; chosen for by plan_windows).  A transition that keeps the
+// warp-index slots in `kept` (bit j = slot 5 + j of nwarp) synchronises each
+// group of warps agreeing on those slots with barrier base + (their values).
+// Every id always belongs to the SAME group of warps with the same count --
+// otherwise a warp running ahead could join a barrier another group still
+// uses.  Ids 1..15 are handed to kept-slot patterns, most slots kept first;
+// returns the base id, or 0 when the pattern has no ids (full CTA barrier).
+inline int group_barrier_base(int nwarp, uint32_t kept) {
+  const uint32_t full = (1u << nwarp) - 1u;
+  if (kept == 0 || kept == full || nwarp > 5) return 0;
+  int next = 1;
+  for (int sz = nwarp - 1; sz >= 1; --sz)
+    for (uint32_t m = full; m >= 1; --m) {   // fixed order: high slots first
+      if (__builtin_popcount(m) != sz) continue;
+      if (next + (1 << sz) > 16) return 0;
+      if (m == kept) return next;
+      next += 1 << sz;
+    }
+  return 0;
+}
 }  // namespace hq
 
 struct hq_plan_s {

@@ -29,6 +29,7 @@
 #include <fstream>
 #include <functional>
 #include <map>
+#include <set>
 #include <mutex>
 #include <thread>
 #include <atomic>
@@ -164,6 +165,7 @@ struct Gen {
   // multiply per variable by a precomputed product e^{iΣ kθ} (ptab, per CTA in
   // shared memory) instead of one per RZ.
   bool defer = false;
+  bool no_csel = false;   // HQ_ABLATE & 8 (timing only): runtime-controlled CNOTs skipped
   // phase-table cap (shared memory: ≤ ~16 KB complex128); past it new RZs
   // apply immediately (they commute with the pending records)
   static constexpr size_t kMaxPtab = 1024;
@@ -441,7 +443,7 @@ struct Gen {
         if (is_reg(a)) {
           for (int i = 0; i < N; ++i)
             if ((i >> a & 1) && !(i >> kt & 1)) std::swap(map[i], map[i | 1 << kt]);
-        } else {
+        } else if (!no_csel) {
           o << "{ const bool c_ = " << cond(a) << ";\n";
           sets([&](bool lam) {
             for (int i = 0; i < N; ++i) {
@@ -602,6 +604,73 @@ struct Gen {
     }
     if (!cnd.empty()) o << "if (!(" << cnd << ")) acc_ = (R)0;\n";
     if (neg2) o << "acc_ *= (R)-2;\n";
+    dot_store(op, per_thread, group, nw, reg_acc);
+  }
+
+  // Diagonal-rotation dots sharing one evaluation point.  d/dθ of RZ / CR on
+  // the bit set M is −2 Σ_{i ⊇ M} Im(λ_i* ψ_i) at the gate, and that sum is the
+  // same at every point reached through gates commuting with the rotation's
+  // generator (diagonal gates, gates on other qubits, CNOT controls; the
+  // emitter checks this while grouping).  So a run of such derivatives shares
+  // the per-amplitude products m_v = Im(λ_v* ψ_v) (2 FMA per amplitude, once)
+  // and each derivative is a sum of them (adds) instead of 2 FMA per amplitude.
+  // Deferred phases multiply ψ_v and λ_v alike and leave m_v unchanged.
+  static int diag_mask_cost(const WOp& op, int N, int& M, std::string& cnd) {
+    M = 0;
+    cnd.clear();
+    std::vector<int> codes = {op.a};
+    if (op.kind == HQ_GATE_CR) codes.push_back(op.b);
+    for (int code : codes) {
+      if (is_reg(code)) M |= 1 << code;
+      else cnd += (cnd.empty() ? "" : " && ") + cond(code);
+    }
+    int n = 0;
+    for (int i = 0; i < N; ++i) n += (i & M) == M;
+    return n;
+  }
+  void dot_diag_group(const std::vector<WOp>& ops, bool per_thread, int group, int nw, int reg_acc) {
+    o << "{ // shared diagonal dots\n";
+    for (int v = 0; v < N; ++v) {
+      const std::string l = "l" + std::to_string(v), p = "p" + std::to_string(v);
+      if (packed) o << "const C m" << v << "_ = mul2(" << l << ", swp2(" << p << "));\n";
+      else o << "const R m" << v << "_ = fmaf_r(" << l << ".x, " << p << ".y, -" << l << ".y * " << p << ".x);\n";
+    }
+    std::map<int, std::string> sums;
+    for (const WOp& op : ops) {
+      int M;
+      std::string cnd;
+      diag_mask_cost(op, N, M, cnd);
+      if (!sums.count(M)) {
+        std::vector<std::string> t;
+        for (int i = 0; i < N; ++i)
+          if ((i & M) == M) t.push_back("m" + std::to_string(map[i]) + "_");
+        // pairwise tree (short dependency chains)
+        int lv = 0;
+        while (t.size() > 1) {
+          std::vector<std::string> nt;
+          for (size_t j = 0; j + 1 < t.size(); j += 2) {
+            const std::string nm = "s" + std::to_string(M) + "_" + std::to_string(lv) + "_" + std::to_string(j / 2);
+            o << "const " << (packed ? "C " : "R ") << nm << " = " << (packed ? "add2(" + t[j] + ", " + t[j + 1] + ")"
+                                                                                : t[j] + " + " + t[j + 1]) << ";\n";
+            nt.push_back(nm);
+          }
+          if (t.size() & 1) nt.push_back(t.back());
+          t = nt;
+          ++lv;
+        }
+        const std::string nm = "sm" + std::to_string(M) + "_";
+        o << "const R " << nm << " = " << (packed ? t[0] + ".x - " + t[0] + ".y" : t[0]) << ";\n";
+        sums[M] = nm;
+      }
+      o << "{ R acc_ = " << sums[M] << ";\n";
+      if (!cnd.empty()) o << "if (!(" << cnd << ")) acc_ = (R)0;\n";
+      o << "acc_ *= (R)-2;\n";
+      dot_store(op, per_thread, group, nw, reg_acc);
+    }
+    o << "}\n";
+  }
+
+  void dot_store(const WOp& op, bool per_thread, int group, int nw, int reg_acc) {
     if (op.dl < reg_acc) {
       o << "da" << op.dl << " += acc_; }\n";
     } else if (per_thread) {
@@ -1125,6 +1194,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   // HQ_ABLATE (timing experiments only, results are wrong): backward kernels
   // without window transitions (1), gate math (2), derivative dots (4)
   const int ablate = std::getenv("HQ_ABLATE") ? std::atoi(std::getenv("HQ_ABLATE")) : 0;
+  g.no_csel = bwd && (ablate & 8);
   // complex128 backward passes: the branch copies cost more than the FSEL swaps
   // they save (2 CTAs/SM, latency bound; profiles/r01_ncu_c128_summary.md)
   int ubudget = (bwd && !c64) ? 0 : 2;
@@ -1144,6 +1214,37 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   };
   // tile-loop barrier outside any branch (the whole CTA, or one tile group)
   auto gsync = [&]() { o << (pp ? "bar_id(1 + grp, T);\n" : "__syncthreads();\n"); };
+  // Window transitions: each thread stores its registers to the same shared
+  // addresses it loaded them from (load_regs / store_regs of one window), so
+  // no barrier is needed before the store; after it, the next window's loads
+  // read data written by other threads -- only by threads of the same warp
+  // when both windows map the same tile qubits to the warp-index bits (then a
+  // __syncwarp suffices and the CTA's warps drift apart, overlapping one
+  // warp's transition with another's FP64 math: complex128 fwd / bwd -5% / -4%
+  // on cfg4).  complex64 keeps the barriers (its huge straight-line kernels run
+  // 8% slower when the warps drift apart; profiles/r02_warpsync.log).
+  // HQ_WARP_SYNC=0/1 overrides.
+  bool wsync_on = !g.c64;
+  if (const char* e = std::getenv("HQ_WARP_SYNC")) wsync_on = std::atoi(e) != 0;
+  wsync_on = wsync_on && !pp && tbits >= 5;
+  auto pre_store_sync = [&]() { if (!wsync_on) sync(); };
+  auto post_store_sync = [&](const WinDev& A, const WinDev& B) {
+    if (!wsync_on) { sync(); return; }
+    // warp-index slots keeping their qubit: only warps differing in the other
+    // slots exchange data -> one named barrier per group of such warps
+    std::vector<int> kept, moved;
+    uint32_t km = 0;
+    for (int s2 = 5; s2 < tbits; ++s2) {
+      (A.ps[s2] == B.ps[s2] ? kept : moved).push_back(s2);
+      if (A.ps[s2] == B.ps[s2]) km |= 1u << (s2 - 5);
+    }
+    if (moved.empty()) { o << "__syncwarp();\n"; return; }
+    const int base = hq::group_barrier_base(tbits - 5, km);
+    if (!base) { sync(); return; }
+    std::string id = std::to_string(base);
+    for (size_t j = 0; j < kept.size(); ++j) id += " + (((tid >> " + std::to_string(kept[j]) + ") & 1) << " + std::to_string(j) + ")";
+    o << (na ? "bar_id_na(" : "bar_id(") << id << ", " << (32 << moved.size()) << ");\n";
+  };
   // ping-pong token: before a window's gate math wait for the other group's
   // math to end (the first window of group 0 starts at once); after it, hand
   // the token over (the last window of group 1 has nobody left to hand to)
@@ -1156,20 +1257,58 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     if (last_window) o << " && !(grp == 1 && tt + 2 >= ps.tpc)";
     o << ") bar_arrive_na(3 + grp, " << L.block << ");\n";
   };
+  // shared diagonal derivative dots (Gen::dot_diag_group); HQ_DIAG_DOTS=0 turns them off
+  std::set<int> dot_done;
+  const bool diag_share = !std::getenv("HQ_DIAG_DOTS") || std::atoi(std::getenv("HQ_DIAG_DOTS")) != 0;
+  auto is_diag_dot = [](const WOp& op) { return op.dl >= 0 && (op.kind == HQ_GATE_RZ || op.kind == HQ_GATE_CR); };
   std::function<void(const std::vector<int>&, size_t, bool, const std::function<void()>&, int)> emit_steps;
   emit_steps = [&](const std::vector<int>& ks, size_t i, bool adj, const std::function<void()>& tail, int budget) {
     for (; i < ks.size(); ++i) {
       const int k = ks[i];
       const WOp& op = P.wops[k];
+      if (adj && !(ablate & 4) && diag_share && is_diag_dot(op) && !dot_done.count(k)) {
+        // gather the diagonal derivatives evaluable here: later ops (in this
+        // backward order) reached only through gates commuting with Z on their bits
+        std::vector<WOp> grp;
+        std::vector<int> grp_k;
+        std::set<int> blocked;
+        int single = 0;
+        for (size_t j = i; j < ks.size(); ++j) {
+          const WOp& oj = P.wops[ks[j]];
+          if (is_diag_dot(oj) && !dot_done.count(ks[j]) && !blocked.count(oj.a) &&
+              !(oj.kind == HQ_GATE_CR && blocked.count(oj.b))) {
+            int M;
+            std::string cnd;
+            single += 2 * Gen::diag_mask_cost(oj, g.N, M, cnd);
+            grp.push_back(oj);
+            grp_k.push_back(ks[j]);
+          }
+          bool stop = false;
+          switch (oj.kind) {
+            case HQ_GATE_Z: case HQ_GATE_RZ: case HQ_GATE_CZ: case HQ_GATE_CR: break;
+            case HQ_GATE_H: case HQ_GATE_X: case HQ_GATE_Y: case HQ_GATE_RX: case HQ_GATE_RY: blocked.insert(oj.a); break;
+            case HQ_GATE_CNOT: blocked.insert(oj.b); break;
+            case HQ_GATE_SWAP: blocked.insert(oj.a); blocked.insert(oj.b); break;
+            default: stop = true;
+          }
+          if (stop) break;
+        }
+        // shared products cost 2 per amplitude plus the adds
+        if (grp.size() >= 2 && single > 2 * g.N + 2 * (int)grp.size()) {
+          g.dot_diag_group(grp, L.per_thread, L.group, nwt, reg_acc);
+          for (int kk : grp_k) dot_done.insert(kk);
+        }
+      }
       g.prepare(op, adj);
       if (adj) {
-        if (!(ablate & 4)) g.dot(op, L.per_thread, L.group, nwt, reg_acc);
+        if (!(ablate & 4) && !dot_done.count(k)) g.dot(op, L.per_thread, L.group, nwt, reg_acc);
         if (first && !fold_end && k == stop_op && op.dl >= 0) continue;
       }
       const bool uni = op.kind == HQ_GATE_CNOT && !Gen::is_reg(op.a) && (op.a >= 64 || op.a - 16 >= 5);
       if (budget > 0 && uni) {
         const std::vector<int> map0 = g.map, bq0 = g.bq;
         const auto vph0 = g.vph;
+        const std::set<int> done0 = dot_done;
         const bool pend0 = g.pending, na0 = na, decl0 = g.ph_decl;
         if (op.a < 64) na = true;
         WOp x{};
@@ -1185,6 +1324,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         g.map = map0;
         g.vph = vph0;
         g.bq = bq0;
+        dot_done = done0;
         g.pending = pend0;
         g.ph_decl = decl0;
         emit_steps(ks, i + 1, adj, tail, budget - 1);
@@ -1301,14 +1441,14 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         identity_map();   // every branch path ended canonical
         fwd_shfl_in = true;
       } else if (w < nwin - 1) {
-        emit_steps(ks, 0, false, [&] { g.flush_vph(false); g.flush_pending(false); sync(); g.store_regs(W, "p", "tp"); sync(); }, ubudget);
+        emit_steps(ks, 0, false, [&] { g.flush_vph(false); g.flush_pending(false); pre_store_sync(); g.store_regs(W, "p", "tp"); post_store_sync(W, P.wins[w + 1]); }, ubudget);
         o << "}\n";
       } else if (fused) {
         for (int k : ks) g.apply(P.wops[k], false, false);
         g.flush_vph(false);
         g.flush_pending(false);
       } else if (last || !direct_ok(W)) {
-        emit_steps(ks, 0, false, [&] { g.flush_vph(false); g.flush_pending(false); sync(); g.store_regs(W, "p", "tp"); sync(); }, ubudget);
+        emit_steps(ks, 0, false, [&] { g.flush_vph(false); g.flush_pending(false); pre_store_sync(); g.store_regs(W, "p", "tp"); sync(); }, ubudget);
         o << "}\n";
       } else {
         emit_steps(ks, 0, false, [&] { g.flush_vph(false); g.flush_pending(false); direct_store(W, false); }, ubudget);
@@ -1430,6 +1570,17 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       std::vector<int> ks;
       for (int k = W.op1 - 1; k >= lo; --k) ks.push_back(k);
       hoist(ks);
+      if (std::getenv("HQ_JIT_OPS")) {
+        std::fprintf(stderr, "bwd win %d:", w);
+        // gate letter (H X Y Z, x y z = RX RY RZ, C = CNOT, c = CZ, R = CR, S = SWAP), codes, ' = derivative
+        for (int k : ks) {
+          const WOp& q = P.wops[k];
+          std::fprintf(stderr, " %c%d", "HXYZxyzCcRS"[q.kind], q.a);
+          if (q.b >= 0) std::fprintf(stderr, ",%d", q.b);
+          if (q.dl >= 0) std::fprintf(stderr, "'");
+        }
+        std::fprintf(stderr, "\n");
+      }
       const bool end = first ? (wi == nwin - 1 || w == stop_win) : (w == 0);
       pp_acquire();
       if (end) {
@@ -1525,7 +1676,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
           if (direct_ok(W)) {
             direct_store(W, true);
           } else {
-            sync();
+            pre_store_sync();
             g.store_regs(W, "p", "tp");
             g.store_regs(W, "l", "tl");
             sync();
@@ -1552,10 +1703,10 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
           emit_shfl(sw, perm, true);
           return;
         }
-        sync();
+        pre_store_sync();
         g.store_regs(W, "p", "tp");
         g.store_regs(W, "l", "tl");
-        sync();
+        post_store_sync(W, P.wins[w - 1]);
       }, ubudget);
       o << "}\n";
       if (to_shfl) identity_map();   // every branch path ended canonical

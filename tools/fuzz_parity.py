@@ -7,6 +7,8 @@ from oracle import hq_oracle as O
 from paper_2301_03251_b200 import engine, Circuit
 
 KINDS = ["H", "X", "Y", "Z", "RX", "RY", "RZ", "CNOT", "CZ", "CR", "SWAP"]
+if os.environ.get("FUZZ_KINDS"):   # e.g. a diagonal-heavy mix: RZ,RZ,RZ,CR,CR,RY,CNOT,CZ
+    KINDS = os.environ["FUZZ_KINDS"].split(",")
 
 
 def builder_for(n, depth, rng):
