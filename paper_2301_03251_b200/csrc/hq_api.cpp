@@ -28,6 +28,7 @@
 #include <map>
 #include <sstream>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "hq_internal.h"
@@ -838,25 +839,41 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
       for (int b : cand[c]) cmask[c] |= 1u << b;
     const int NEG = -(1 << 28);
     std::vector<std::vector<int>> dp(K, std::vector<int>(C, NEG)), from(K, std::vector<int>(C, -1));
+    // transition score by the exactly-kept slot pattern (via the barrier group
+    // it can use); the previous windows' best per (pattern, kept qubits) makes
+    // each step O(C · 2^nwarp) instead of O(C²)
+    const uint32_t nmask = 1u << nwarp;
+    std::vector<int> score(nmask, 0);
+    for (uint32_t m = 0; m < nmask; ++m) score[m] = 16 * popc(hq::group_barrier_mask(nwarp, m)) / nwarp;
+    auto key = [&](size_t c, uint32_t m) {
+      uint32_t k2 = 0;
+      for (int i = 0; i < nwarp; ++i)
+        if (m >> i & 1u) k2 = k2 * 32u + (uint32_t)cand[c][i] + 1u;
+      return k2;
+    };
     for (size_t k = 0; k < K; ++k) {
       const uint32_t restm = all & ~wins[k].Rm;
-      std::vector<int> prev_ok;
+      // best previous value per (sub-pattern m, its qubits): a previous tuple
+      // agreeing with c on at least m's slots scores at least score[m], and
+      // score is monotone over sub-patterns, so the max over m is exact
+      std::vector<std::unordered_map<uint32_t, std::pair<int, int>>> best(nmask);
       if (k > 0)
-        for (size_t c2 = 0; c2 < C; ++c2)
-          if (dp[k - 1][c2] > NEG) prev_ok.push_back((int)c2);
+        for (size_t c2 = 0; c2 < C; ++c2) {
+          if (dp[k - 1][c2] <= NEG) continue;
+          for (uint32_t m = 0; m < nmask; ++m) {
+            auto& e = best[m].try_emplace(key(c2, m), NEG, -1).first->second;
+            if (dp[k - 1][c2] > e.first) e = {dp[k - 1][c2], (int)c2};
+          }
+        }
       for (size_t c = 0; c < C; ++c) {
         if ((cmask[c] & wins[k].Rm) || classes(restm & ~cmask[c]) != classes(restm)) continue;
         const int own = popc(cmask[c] & wins[k].ctl);
         if (k == 0) { dp[k][c] = own; continue; }
         int v = NEG, f = -1;
-        for (int c2 : prev_ok) {
-          int kept = 0;
-          uint32_t km = 0;
-          for (int i = 0; i < nwarp; ++i)
-            if (cand[c][i] == cand[c2][i]) { ++kept; km |= 1u << i; }
-          if (kept < nwarp && !hq::group_barrier_base(nwarp, km)) kept = 0;   // no ids: CTA barrier
-          const int sc = dp[k - 1][c2] + 16 * kept / nwarp;
-          if (sc > v) { v = sc; f = c2; }
+        for (uint32_t m = 0; m < nmask; ++m) {
+          auto it = best[m].find(key(c, m));
+          if (it == best[m].end() || it->second.second < 0) continue;
+          if (it->second.first + score[m] > v) { v = it->second.first + score[m]; f = it->second.second; }
         }
         if (f < 0) continue;
         dp[k][c] = v + own;
@@ -1257,7 +1274,9 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
         if (capped.size() < best.size()) best.swap(capped);
       }
       const size_t first = best.empty() ? 0 : best[0].op_ids.size();
-      if (!search || best.size() < 4 || first < 64) return best;   // small plans: nothing to gain
+      // small plans: nothing to gain; long ones (cfg5: 59 passes) gain nothing
+      // measurable from the first pass's cap and pay ~10 s of window counting
+      if (!search || best.size() < 4 || best.size() > 24 || first < 64) return best;
       size_t best_cost = count_windows(best) + pass_w * best.size();
       const size_t oc = (try_cap && best[0].op_ids.size() <= kC128PassOps) ? kC128PassOps : op_cap;
       for (int pct : {95, 91, 87, 83, 79, 75}) {

@@ -120,6 +120,18 @@ inline int group_barrier_base(int nwarp, uint32_t kept) {
     }
   return 0;
 }
+// The warp slots a transition keeping `kept` synchronises on: all of them
+// (warp-local) when every slot is kept, else the largest sub-pattern that owns
+// barrier ids (a coarser group -- a superset of the warps that exchange data
+// -- is still correct), else 0 (CTA barrier).
+inline uint32_t group_barrier_mask(int nwarp, uint32_t kept) {
+  const uint32_t full = (1u << nwarp) - 1u;
+  if (kept == full) return full;
+  uint32_t best = 0;
+  for (uint32_t m = kept; m; m = (m - 1) & kept)
+    if (group_barrier_base(nwarp, m) && __builtin_popcount(m) > __builtin_popcount(best)) best = m;
+  return best;
+}
 }  // namespace hq
 
 struct hq_plan_s {

@@ -1232,15 +1232,16 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     if (!wsync_on) { sync(); return; }
     // warp-index slots keeping their qubit: only warps differing in the other
     // slots exchange data -> one named barrier per group of such warps
-    std::vector<int> kept, moved;
     uint32_t km = 0;
-    for (int s2 = 5; s2 < tbits; ++s2) {
-      (A.ps[s2] == B.ps[s2] ? kept : moved).push_back(s2);
+    for (int s2 = 5; s2 < tbits; ++s2)
       if (A.ps[s2] == B.ps[s2]) km |= 1u << (s2 - 5);
-    }
-    if (moved.empty()) { o << "__syncwarp();\n"; return; }
-    const int base = hq::group_barrier_base(tbits - 5, km);
+    const int nwarp = tbits - 5;
+    if (km == (1u << nwarp) - 1u) { o << "__syncwarp();\n"; return; }
+    km = hq::group_barrier_mask(nwarp, km);
+    const int base = hq::group_barrier_base(nwarp, km);
     if (!base) { sync(); return; }
+    std::vector<int> kept, moved;
+    for (int s2 = 5; s2 < tbits; ++s2) (km >> (s2 - 5) & 1u ? kept : moved).push_back(s2);
     std::string id = std::to_string(base);
     for (size_t j = 0; j < kept.size(); ++j) id += " + (((tid >> " + std::to_string(kept[j]) + ") & 1) << " + std::to_string(j) + ")";
     o << (na ? "bar_id_na(" : "bar_id(") << id << ", " << (32 << moved.size()) << ");\n";
