@@ -891,6 +891,9 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
     }
     for (size_t k = 0; k < K; ++k) wins[k].S = thread_bits(wins[k], ok ? Wsel[k] : std::vector<int>{});
   }
+  // no warp-index bits (one warp per tile): the default placement
+  for (WinTmp& wt : wins)
+    if (wt.S.empty()) wt.S = thread_bits(wt, {});
 
   for (const WinTmp& wt : wins) {
     const std::vector<int>& R = wt.R;
@@ -1390,6 +1393,18 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
         pops.push_back(o);
       }
       plan_windows(ps, pops, pl->tile_bits, RB, f, true, pl->precision == HQ_C128);
+      // complex128 forward kernels: one more register bit (HQ_FWD_RB=0: off)
+      {
+        bool split = pl->precision == HQ_C128 && pl->tile_bits - (RB + 1) >= 5;
+        if (const char* e = std::getenv("HQ_FWD_RB")) split = split && std::atoi(e) != 0;
+        if (split) {
+          hq::Pass tmp;
+          plan_windows(tmp, pops, pl->tile_bits, RB + 1, f, true, true);
+          ps.f_rb = RB + 1;
+          ps.fwins = std::move(tmp.wins);
+          ps.fwops = std::move(tmp.wops);
+        }
+      }
       ps.n_dops = (int32_t)ps.op_ids.size();
       ps.n_dslots_pass = (int32_t)pass_dlist.size() - ps.first_dlist;
       ps.first_slotlist = (int32_t)pass_slots.size();

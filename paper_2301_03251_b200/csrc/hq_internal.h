@@ -63,6 +63,12 @@ struct Pass {
   std::vector<WinDev> wins;        // register windows of this pass
   std::vector<WOp> wops;           // ops in window order
   int32_t first_win = 0, first_wop = 0;
+  // forward-only kernels of complex128 plans: windows of f_rb (= reg_bits + 1)
+  // register bits (ψ alone fits 16 amplitudes per thread; fewer windows, less
+  // shared-memory traffic); 0 = the kernels share wins / wops
+  int32_t f_rb = 0;
+  std::vector<WinDev> fwins;
+  std::vector<WOp> fwops;
 };
 
 struct ProfRec {

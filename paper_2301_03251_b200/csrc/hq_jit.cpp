@@ -847,7 +847,7 @@ bool pingpong_for(const hq_plan_s* pl, int i, bool bwd, bool fused) {
 
 JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd, bool fused) {
   const Pass& P = pl->passes[i];
-  const int RB = pl->reg_bits;
+  const int RB = (!bwd && !fused && P.f_rb > 0) ? P.f_rb : pl->reg_bits;
   const int T = 1 << (pl->tile_bits - RB);
   const size_t amp = pl->precision == HQ_C64 ? 8 : 16, rsz = amp / 2;
   JitLayout L{};
@@ -897,10 +897,18 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   const bool fused = mode == 2;
   const bool bwd = mode != 0;
   const bool fwd = mode != 1;
-  const Pass& P = pl->passes[pi];
+  // forward-only kernels of a split plan use their own (wider) register windows
+  const bool fsplit = mode == 0 && pl->passes[pi].f_rb > 0;
+  Pass Pf;
+  if (fsplit) {
+    Pf = pl->passes[pi];
+    Pf.wins = Pf.fwins;
+    Pf.wops = Pf.fwops;
+  }
+  const Pass& P = fsplit ? Pf : pl->passes[pi];
   const bool c64 = pl->precision == HQ_C64;
   Gen g;
-  g.RB = pl->reg_bits;
+  g.RB = fsplit ? P.f_rb : pl->reg_bits;
   g.N = 1 << g.RB;
   g.Q = pl->tile_bits;
   g.T = 1 << (g.Q - g.RB);
@@ -1086,7 +1094,8 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   // occupancy hint: ~128 registers per thread for ψ+λ kernels, 64 for forward
   // (4 CTAs/SM at 256 threads: cfg4 forward 95.8 -> 94.4 ms c128, 39.3 -> 38.1
   // ms c64 vs 80 registers / 3 CTAs, profiles/r02_fwdminb.log)
-  int minb = std::max(1, 65536 / (g.T * (bwd ? 128 : 64)));
+  // (16 complex128 amplitudes per thread in split forward kernels: 128)
+  int minb = std::max(1, 65536 / (g.T * (bwd || (!c64 && g.N == 16) ? 128 : 64)));
   if (const char* e = std::getenv(bwd ? "HQ_BWD_MINB" : "HQ_FWD_MINB")) minb = std::max(1, std::atoi(e));
   if (pp) minb = 1;
   o << "extern \"C\" __global__ void __launch_bounds__(" << L.block << ", " << minb << ") "

@@ -834,3 +834,42 @@ def test_device_probabilities_match_host():
         np.testing.assert_allclose(both[0], host, atol=1e-15)
         np.testing.assert_allclose(both[1], qsim.probabilities(qsim.StateVector.from_amplitudes(z[::-1].copy()), meas),
                                    atol=1e-15)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("flip", [False, True])
+@pytest.mark.parametrize("tile", [11, 12])
+def test_window_transition_barriers_vs_oracle(prec, flip, tile, monkeypatch):
+    """Barrier-light window transitions (no pre-store barrier; __syncwarp /
+    warp-group named barriers / CTA barrier after the store) with the DP
+    warp-slot placement, and the shared diagonal derivative dots -- in each
+    precision's default setting and flipped (complex64 runs them on,
+    complex128 off) -- against the oracle on an RZ/CR-heavy layered circuit
+    with 2-3 warp-index bits."""
+    monkeypatch.setenv("HQ_FORCE_STREAM", "1")
+    monkeypatch.setenv("HQ_TILE_BITS", str(tile))
+    if flip:
+        on = "1" if prec == "c64" else "0"
+        monkeypatch.setenv("HQ_WARP_SYNC", on)
+        monkeypatch.setenv("HQ_KEEP_WARPS", on)
+        monkeypatch.setenv("HQ_DIAG_DOTS", "0")
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "fuzz_parity_diag", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools",
+                                         "fuzz_parity.py"))
+    fz = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(fz)
+    fz.KINDS = ["RZ", "RZ", "RZ", "CR", "CR", "RY", "RX", "CNOT", "CZ", "H"]   # runs of diagonal derivatives
+    rng = np.random.default_rng(91)
+    hea, P = _hea_rz_builder(14, 4, seed=9)
+    cases = [(hea, P), (fz.builder_for(14, 90, rng), 4)]
+    for b, P in cases:
+        x = rng.uniform(-3, 3, (2, 2))
+        th = rng.uniform(0, 6, P)
+        res, jac, info = engine.run_batch(b, x, th, True, True, prec, cache=engine.PlanCache(2))
+        assert "path=stream" in info["plan"].description
+        out, jx, jp, _, _ = O.layer(lambda i, p: b(i, p, Circ=O.Circuit), x, th)
+        check_vals(res, out, prec, floor=1.0)
+        j = jac.cpu().numpy()
+        check_vals(j[:, :2], jx, prec, grad=True, floor=1.0)
+        check_vals(j[:, 2:], jp, prec, grad=True, floor=1.0)
