@@ -1395,8 +1395,9 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
       plan_windows(ps, pops, pl->tile_bits, RB, f, true, pl->precision == HQ_C128);
       // complex128 forward kernels: one more register bit (HQ_FWD_RB=0: off)
       {
-        bool split = pl->precision == HQ_C128 && pl->tile_bits - (RB + 1) >= 5;
-        if (const char* e = std::getenv("HQ_FWD_RB")) split = split && std::atoi(e) != 0;
+        bool split = pl->precision == HQ_C128;
+        if (const char* e = std::getenv("HQ_FWD_RB")) split = std::atoi(e) != 0;
+        split = split && pl->tile_bits - (RB + 1) >= 5 && RB + 1 <= 4;   // WinDev::pr holds 4 bits
         if (split) {
           hq::Pass tmp;
           plan_windows(tmp, pops, pl->tile_bits, RB + 1, f, true, true);
