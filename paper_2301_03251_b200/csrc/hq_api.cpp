@@ -875,21 +875,26 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
           if (it == best[m].end() || it->second.second < 0) continue;
           if (it->second.first + score[m] > v) { v = it->second.first + score[m]; f = it->second.second; }
         }
-        if (f < 0) continue;
+        if (f < 0) { dp[k][c] = own; continue; }   // previous window had no valid tuple: restart
         dp[k][c] = v + own;
         from[k][c] = f;
       }
     }
-    int c = -1, bv = NEG;
-    for (size_t i = 0; i < C; ++i)
-      if (dp[K - 1][i] > bv) { bv = dp[K - 1][i]; c = (int)i; }
+    // backtrack; a chain break (a window without any valid tuple) falls back
+    // to the default placement there and restarts from the best earlier state
     std::vector<std::vector<int>> Wsel(K);
-    bool ok = c >= 0;
-    for (size_t k = K; ok && k-- > 0;) {
+    int c = -1;
+    for (size_t k = K; k-- > 0;) {
+      if (c < 0) {
+        int bv = NEG;
+        for (size_t i = 0; i < C; ++i)
+          if (dp[k][i] > bv) { bv = dp[k][i]; c = (int)i; }
+      }
+      if (c < 0) continue;
       Wsel[k] = cand[c];
-      if (k > 0) { c = from[k][c]; ok = c >= 0; }
+      c = from[k][c];
     }
-    for (size_t k = 0; k < K; ++k) wins[k].S = thread_bits(wins[k], ok ? Wsel[k] : std::vector<int>{});
+    for (size_t k = 0; k < K; ++k) wins[k].S = thread_bits(wins[k], Wsel[k]);
   }
   // no warp-index bits (one warp per tile): the default placement
   for (WinTmp& wt : wins)
