@@ -513,7 +513,7 @@ struct Gen {
   // FMA latency chain is N/kChains long instead of N; dl < reg_acc adds into
   // the register accumulator da<dl> (kept across the tile loop), otherwise
   // into the shared-memory partials.
-  static constexpr int kChains = 4;
+  int kChains = std::getenv("HQ_DOT_CHAINS") ? std::max(1, std::atoi(std::getenv("HQ_DOT_CHAINS"))) : 4;
   void dot(const WOp& op, bool per_thread, int group, int nw, int reg_acc) {
     if (op.dl < 0) return;
     const int a = op.a;
