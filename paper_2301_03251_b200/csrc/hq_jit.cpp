@@ -1235,6 +1235,8 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   // HQ_WARP_SYNC=0/1 overrides.
   bool wsync_on = !g.c64;
   if (const char* e = std::getenv("HQ_WARP_SYNC")) wsync_on = std::atoi(e) != 0;
+  if (!bwd)
+    if (const char* e = std::getenv("HQ_WARP_SYNC_FWD")) wsync_on = std::atoi(e) != 0;
   wsync_on = wsync_on && !pp && tbits >= 5;
   auto pre_store_sync = [&]() { if (!wsync_on) sync(); };
   auto post_store_sync = [&](const WinDev& A, const WinDev& B) {
