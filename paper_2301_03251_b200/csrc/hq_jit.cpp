@@ -1240,6 +1240,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   wsync_on = wsync_on && !pp && tbits >= 5;
   auto pre_store_sync = [&]() { if (!wsync_on) sync(); };
   auto post_store_sync = [&](const WinDev& A, const WinDev& B) {
+    if (ablate & 16) return;   // timing study only: no barrier (races; wrong results)
     if (!wsync_on) { sync(); return; }
     // warp-index slots keeping their qubit: only warps differing in the other
     // slots exchange data -> one named barrier per group of such warps
