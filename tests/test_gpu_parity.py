@@ -873,3 +873,41 @@ def test_window_transition_barriers_vs_oracle(prec, flip, tile, monkeypatch):
         j = jac.cpu().numpy()
         check_vals(j[:, :2], jx, prec, grad=True, floor=1.0)
         check_vals(j[:, 2:], jp, prec, grad=True, floor=1.0)
+
+
+@pytest.mark.parametrize("tile", [10, 11, 12])
+@pytest.mark.parametrize("split", ["1", "0"])
+def test_forward_window_split_states_vs_oracle(tile, split, monkeypatch):
+    """complex128 forward kernels on their own 4-register-bit windows
+    (HQ_FWD_RB=1, the default) vs the backward's 3-bit windows: final
+    amplitudes (exact phases, hq_state's last pass), the expectation and the
+    adjoint gradient of a layered multi-pass circuit against the oracle."""
+    monkeypatch.setenv("HQ_FORCE_STREAM", "1")
+    monkeypatch.setenv("HQ_TILE_BITS", str(tile))
+    monkeypatch.setenv("HQ_FWD_RB", split)
+    n = 15
+    rng = np.random.default_rng(tile * 3 + int(split))
+    c, oc = Circuit(n), O.Circuit(n)
+    for layer in range(3):
+        for q in range(n):
+            a, b = (float(v) for v in rng.uniform(-3, 3, 2))
+            c.ry(q, a); oc.add(O.Op("RY", (q,), a))
+            c.rz(q, b); oc.add(O.Op("RZ", (q,), b))
+        for q in range(n - 1):
+            c.cnot(q, q + 1); oc.add(O.Op("CNOT", (q, q + 1)))
+        q0, q1 = (int(v) for v in rng.choice(n, 2, replace=False))
+        c.cz(q0, q1); oc.add(O.Op("CZ", (q0, q1)))
+        c.h(q1); oc.add(O.Op("H", (q1,)))
+    c.measure(0, 7, 14); oc.measure(0, 7, 14)
+    st = engine.final_states([c], "c128")[0]
+    np.testing.assert_allclose(st, O.simulate(oc), atol=1e-12)
+    assert engine.evaluate_circuits([c], "c128")[0] == pytest.approx(O.expectation(oc), abs=1e-11)
+    b, P = _hea_rz_builder(n, 3, seed=tile)
+    x = rng.uniform(-3, 3, (2, 2))
+    th = rng.uniform(0, 6, P)
+    res, jac, info = engine.run_batch(b, x, th, True, True, "c128", cache=engine.PlanCache(2))
+    out, jx, jp, _, _ = O.layer(lambda i, p: b(i, p, Circ=O.Circuit), x, th)
+    check_vals(res, out, "c128", floor=1.0)
+    j = jac.cpu().numpy()
+    check_vals(j[:, :2], jx, "c128", grad=True, floor=1.0)
+    check_vals(j[:, 2:], jp, "c128", grad=True, floor=1.0)
