@@ -61,14 +61,23 @@ struct Nvrtc {
   nvrtcResult (*log)(nvrtcProgram, char*) = nullptr;
   nvrtcResult (*destroy)(nvrtcProgram*) = nullptr;
   nvrtcResult (*version)(int*, int*) = nullptr;
+  int major = 0, minor = 0;
 };
 
+// The toolkit's NVRTC first ($HQ_NVRTC overrides): a bare "libnvrtc.so.12"
+// resolves to whatever copy is already loaded -- in a process that imported
+// torch that is the wheel's (12.8), elsewhere the toolkit's (12.9) -- and the
+// two generate different code for the same source (complex64 pass kernels
+// 12-18% slower with 12.8).  Pinning one compiler keeps the cubins built on
+// the build host (tools/precompile.py) and on the GPU box identical.
 Nvrtc load_nvrtc() {
   Nvrtc n;
-  const char* cands[] = {"libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"};
+  const char* env = std::getenv("HQ_NVRTC");
+  const char* cands[] = {env && *env ? env : "/usr/local/cuda/lib64/libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12",
+                         "libnvrtc.so.12", "libnvrtc.so"};
   void* h = nullptr;
   for (const char* c : cands)
-    if ((h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
+    if ((h = dlopen(c, RTLD_NOW | RTLD_LOCAL))) break;
   if (!h) { n.why = "libnvrtc.so.12 not found"; return n; }
   n.create = (decltype(n.create))dlsym(h, "nvrtcCreateProgram");
   n.compile = (decltype(n.compile))dlsym(h, "nvrtcCompileProgram");
@@ -80,6 +89,7 @@ Nvrtc load_nvrtc() {
   n.version = (decltype(n.version))dlsym(h, "nvrtcVersion");
   n.ok = n.create && n.compile && n.cubin_size && n.cubin && n.log_size && n.log && n.destroy;
   if (!n.ok) n.why = "libnvrtc lacks the expected symbols";
+  if (n.ok && n.version) n.version(&n.major, &n.minor);
   return n;
 }
 
@@ -866,7 +876,13 @@ JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd, bool fused) {
     L.group = 32;
     while (L.group > 1 && (size_t)P.n_dslots_pass * nwt * L.group * rsz > 40 * 1024) L.group >>= 1;
     L.per_thread = L.group == 32;
-    if (!L.per_thread) L.group = std::min(L.group, 4);   // batched reduction keeps 4 partials per warp
+    // batched reduction keeps 4 partials per warp (complex128: 2, one transposed
+    // level more per batch and half the shared partials: backward -1%,
+    // profiles/r02_knobs3.log); HQ_DOT_GROUP overrides (read here at JIT and launch)
+    if (!L.per_thread) {
+      L.group = std::min(L.group, pl->precision == HQ_C64 ? 4 : 2);
+      if (const char* e = std::getenv("HQ_DOT_GROUP")) L.group = std::max(1, std::min(L.group, std::atoi(e)));
+    }
     // group mode: a batch updates 8 slots at once; a stride of nw·G + 4 puts
     // consecutive slots on different banks.  Ping-pong per-thread mode keeps
     // every partial in registers and reduces per warp at the end.
@@ -1937,7 +1953,8 @@ hq_status jit_build(hq_plan_s* pl, std::string& err) {
     const bool fused_i = i == np - 1 && !pl->seg;
     units[i].src = small ? head + gen_small(pl)
                          : head + gen_pass(pl, i, 0) + gen_pass(pl, i, 1) + (fused_i ? gen_pass(pl, i, 2) : "");
-    units[i].hash = fnv1a(units[i].src);
+    // keyed by source AND compiler version (different NVRTCs -> different code)
+    units[i].hash = fnv1a(units[i].src + "\n// nvrtc " + std::to_string(nv.major) + "." + std::to_string(nv.minor));
     if (std::getenv("HQ_JIT_DUMP")) dump += units[i].src;
   }
   if (const char* path = std::getenv("HQ_JIT_DUMP")) {
