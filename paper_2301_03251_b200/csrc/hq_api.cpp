@@ -518,8 +518,8 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
   // The lookahead prefers such register sets by kShflBonus score points
   // (= half an admitted op each).
   const bool shfl = hq::shfl_enabled();
-  // (complex128 default: its kernels use the warp-local transitions; complex64
-  // keeps CTA barriers, measured faster there -- profiles/r02_warpsync.log)
+  // (default for both precisions: complex64 -2.8% with the warp-group
+  // transitions, measured with one compiler -- profiles/r02_compiler_ab.log)
   bool keep_warps = warp_local;
   if (const char* e = std::getenv("HQ_KEEP_WARPS")) keep_warps = std::atoi(e) != 0;
   int shfl_bonus = 3;
@@ -1397,7 +1397,7 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
         pl->dops.push_back(o);
         pops.push_back(o);
       }
-      plan_windows(ps, pops, pl->tile_bits, RB, f, true, pl->precision == HQ_C128);
+      plan_windows(ps, pops, pl->tile_bits, RB, f, true, true);
       // complex128 forward kernels: one more register bit (HQ_FWD_RB=0: off)
       {
         bool split = pl->precision == HQ_C128;

@@ -523,7 +523,9 @@ struct Gen {
   // FMA latency chain is N/kChains long instead of N; dl < reg_acc adds into
   // the register accumulator da<dl> (kept across the tile loop), otherwise
   // into the shared-memory partials.
-  int kChains = std::getenv("HQ_DOT_CHAINS") ? std::max(1, std::atoi(std::getenv("HQ_DOT_CHAINS"))) : 4;
+  // independent FMA chains per derivative dot (2: -0.4% / -0.5% vs 4 for
+  // complex128 / complex64, profiles/r02_compiler_ab.log); HQ_DOT_CHAINS overrides
+  int kChains = std::getenv("HQ_DOT_CHAINS") ? std::max(1, std::atoi(std::getenv("HQ_DOT_CHAINS"))) : 2;
   void dot(const WOp& op, bool per_thread, int group, int nw, int reg_acc) {
     if (op.dl < 0) return;
     const int a = op.a;
@@ -876,11 +878,11 @@ JitLayout jit_layout(const hq_plan_s* pl, int i, bool bwd, bool fused) {
     L.group = 32;
     while (L.group > 1 && (size_t)P.n_dslots_pass * nwt * L.group * rsz > 40 * 1024) L.group >>= 1;
     L.per_thread = L.group == 32;
-    // batched reduction keeps 4 partials per warp (complex128: 2, one transposed
-    // level more per batch and half the shared partials: backward -1%,
-    // profiles/r02_knobs3.log); HQ_DOT_GROUP overrides (read here at JIT and launch)
+    // batched reduction keeps 4 partials per warp (2: no faster with one
+    // compiler, profiles/r02_compiler_ab.log); HQ_DOT_GROUP overrides (read
+    // here at JIT and launch)
     if (!L.per_thread) {
-      L.group = std::min(L.group, pl->precision == HQ_C64 ? 4 : 2);
+      L.group = std::min(L.group, 4);
       if (const char* e = std::getenv("HQ_DOT_GROUP")) L.group = std::max(1, std::min(L.group, std::atoi(e)));
     }
     // group mode: a batch updates 8 slots at once; a stride of nw·G + 4 puts
@@ -1245,11 +1247,10 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   // read data written by other threads -- only by threads of the same warp
   // when both windows map the same tile qubits to the warp-index bits (then a
   // __syncwarp suffices and the CTA's warps drift apart, overlapping one
-  // warp's transition with another's FP64 math: complex128 fwd / bwd -5% / -4%
-  // on cfg4).  complex64 keeps the barriers (its huge straight-line kernels run
-  // 8% slower when the warps drift apart; profiles/r02_warpsync.log).
-  // HQ_WARP_SYNC=0/1 overrides.
-  bool wsync_on = !g.c64;
+  // warp's transition with another's math: cfg4 forward + adjoint complex128
+  // -6.6%, complex64 -2.5%; profiles/r02_compiler_ab.log).  HQ_WARP_SYNC=0/1
+  // overrides.
+  bool wsync_on = true;
   if (const char* e = std::getenv("HQ_WARP_SYNC")) wsync_on = std::atoi(e) != 0;
   if (!bwd)
     if (const char* e = std::getenv("HQ_WARP_SYNC_FWD")) wsync_on = std::atoi(e) != 0;

@@ -842,16 +842,15 @@ def test_device_probabilities_match_host():
 def test_window_transition_barriers_vs_oracle(prec, flip, tile, monkeypatch):
     """Barrier-light window transitions (no pre-store barrier; __syncwarp /
     warp-group named barriers / CTA barrier after the store) with the DP
-    warp-slot placement, and the shared diagonal derivative dots -- in each
-    precision's default setting and flipped (complex64 runs them on,
-    complex128 off) -- against the oracle on an RZ/CR-heavy layered circuit
-    with 2-3 warp-index bits."""
+    warp-slot placement, and the shared diagonal derivative dots -- the
+    default, and flipped off (CTA barriers, round-1 thread-bit placement, one
+    dot per diagonal gate) -- against the oracle on an RZ/CR-heavy layered
+    circuit with 2-3 warp-index bits."""
     monkeypatch.setenv("HQ_FORCE_STREAM", "1")
     monkeypatch.setenv("HQ_TILE_BITS", str(tile))
     if flip:
-        on = "1" if prec == "c64" else "0"
-        monkeypatch.setenv("HQ_WARP_SYNC", on)
-        monkeypatch.setenv("HQ_KEEP_WARPS", on)
+        monkeypatch.setenv("HQ_WARP_SYNC", "0")
+        monkeypatch.setenv("HQ_KEEP_WARPS", "0")
         monkeypatch.setenv("HQ_DIAG_DOTS", "0")
     import importlib.util
     spec = importlib.util.spec_from_file_location(
