@@ -196,6 +196,12 @@ struct hq_plan_s {
     std::string why;                      // why the static kernels run instead
     std::vector<cudaKernel_t> fwd, bwd;   // per pass
     cudaKernel_t fused = nullptr;         // last forward pass + its backward
+    // launch geometry fixed when the kernels were generated (threads per CTA,
+    // dynamic shared memory), per pass and mode (0 fwd, 1 bwd, 2 fused): later
+    // changes of the environment knobs cannot desynchronise a launch from
+    // the code's shared-memory carve-up
+    std::vector<int> block[3];
+    std::vector<size_t> smem[3];
     cudaKernel_t small = nullptr;         // on-chip plans up to 4 qubits: one thread per sample
   } jit;
 };

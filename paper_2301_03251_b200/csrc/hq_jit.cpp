@@ -2019,6 +2019,10 @@ hq_status jit_build(hq_plan_s* pl, std::string& err) {
   }
   pl->jit.fwd.assign(np, nullptr);
   pl->jit.bwd.assign(np, nullptr);
+  for (int m = 0; m < 3; ++m) {
+    pl->jit.block[m].assign(np, 0);
+    pl->jit.smem[m].assign(np, 0);
+  }
   for (int i = 0; i < np; ++i) {
     cudaLibrary_t lib = nullptr;
     {
@@ -2044,6 +2048,8 @@ hq_status jit_build(hq_plan_s* pl, std::string& err) {
     }
     for (int mode = 0; mode < (i == np - 1 && !pl->seg ? 3 : 2); ++mode) {
       const JitLayout L = jit_layout(pl, i, mode != 0, mode == 2);
+      pl->jit.block[mode][i] = L.block;
+      pl->jit.smem[mode][i] = L.total;
       cudaKernel_t k = mode == 0 ? pl->jit.fwd[i] : (mode == 1 ? pl->jit.bwd[i] : pl->jit.fused);
       cudaError_t ce = cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
       if (ce != cudaSuccess) {
@@ -2065,18 +2071,18 @@ cudaError_t jit_launch_small(const hq_plan_s* pl, const KArgs& a, cudaStream_t s
 cudaError_t jit_launch_pass(const hq_plan_s* pl, int i, int mode, const KArgs& a, const JPass& ps,
                             unsigned grid, cudaStream_t st) {
   const bool bwd = mode != 0;
-  const JitLayout L = jit_layout(pl, i, bwd, mode == 2);
   cudaKernel_t k = mode == 0 ? pl->jit.fwd[i] : (mode == 1 ? pl->jit.bwd[i] : pl->jit.fused);
-  const int T = L.block;
+  const int T = pl->jit.block[mode][i];
+  const size_t smem = pl->jit.smem[mode][i];
   KArgs ac = a;
   JPass pc = ps;
   void* args[] = {&ac, &pc};
-  cudaError_t e = cudaLaunchKernel((const void*)k, dim3(grid), dim3(T), args, L.total, st);
+  cudaError_t e = cudaLaunchKernel((const void*)k, dim3(grid), dim3(T), args, smem, st);
   if (e != cudaSuccess && std::getenv("HQ_JIT_DEBUG")) {
     cudaFuncAttributes fa{};
     cudaError_t e2 = cudaFuncGetAttributes(&fa, (const void*)k);
     std::fprintf(stderr, "hq_jit launch %s%d grid=%u block=%d smem=%zu -> %s | attrs(%s): regs=%d maxthr=%d "
-                 "static_smem=%zu maxdyn=%d local=%zu\n", bwd ? "hq_b" : "hq_f", i, grid, T, L.total,
+                 "static_smem=%zu maxdyn=%d local=%zu\n", bwd ? "hq_b" : "hq_f", i, grid, T, smem,
                  cudaGetErrorString(e), cudaGetErrorString(e2), fa.numRegs, fa.maxThreadsPerBlock,
                  fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.localSizeBytes);
   }
