@@ -910,9 +910,9 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
       for (int b : S) std::fprintf(stderr, "%d,", b);
       std::fprintf(stderr, "\n");
     }
-    hq::WinDev w{};
+    hq::WinHost w{};
     w.op0 = (int16_t)ps.wops.size();
-    for (int i = 0; i < RB; ++i) w.pr[i] = swz_host(1u << R[i]);
+    for (int i = 0; i < RB && i < 6; ++i) w.pr[i] = swz_host(1u << R[i]);
     for (size_t s2 = 0; s2 < S.size() && s2 < 10; ++s2) w.ps[s2] = swz_host(1u << S[s2]);
     auto code = [&](int x) -> int8_t {
       if (x < 0) return (int8_t)(64 + ~x);
@@ -932,7 +932,15 @@ void plan_windows(hq::Pass& ps, const std::vector<hq::DOp>& ops, int q, int RB, 
       ps.wops.push_back(wo);
     }
     w.op1 = (int16_t)ps.wops.size();
-    ps.wins.push_back(w);
+    ps.hwins.push_back(w);
+    if (RB <= 4) {   // the device copy (generic kernels) holds 4 register bits
+      hq::WinDev d{};
+      d.op0 = w.op0;
+      d.op1 = w.op1;
+      for (int i = 0; i < 4; ++i) d.pr[i] = w.pr[i];
+      for (int i = 0; i < 10; ++i) d.ps[i] = w.ps[i];
+      ps.wins.push_back(d);
+    }
   }
 }
 
@@ -1260,7 +1268,7 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
         }
         hq::Pass tmp = ps;
         plan_windows(tmp, pops, pl->tile_bits, RB, f, false);
-        w += tmp.wins.size();
+        w += tmp.hwins.size();
       }
       return w;
     };
@@ -1402,12 +1410,12 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
       {
         bool split = pl->precision == HQ_C128;
         if (const char* e = std::getenv("HQ_FWD_RB")) split = std::atoi(e) != 0;
-        split = split && pl->tile_bits - (RB + 1) >= 5 && RB + 1 <= 4;   // WinDev::pr holds 4 bits
+        split = split && pl->tile_bits - (RB + 1) >= 5 && RB + 1 <= 5;
         if (split) {
           hq::Pass tmp;
           plan_windows(tmp, pops, pl->tile_bits, RB + 1, f, true, true);
           ps.f_rb = RB + 1;
-          ps.fwins = std::move(tmp.wins);
+          ps.fwins = std::move(tmp.hwins);
           ps.fwops = std::move(tmp.wops);
         }
       }

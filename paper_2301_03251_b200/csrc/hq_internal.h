@@ -49,6 +49,14 @@ struct WinDev {
   uint16_t ps[10];  // swz(1 << S[s]); thread-index bit s <-> tile qubit S[s]
 };
 
+// Host-side window (the JIT generator): up to 6 register bits (forward
+// kernels with one more register bit than the device struct carries).
+struct WinHost {
+  int16_t op0 = 0, op1 = 0;
+  uint16_t pr[6] = {};
+  uint16_t ps[10] = {};
+};
+
 // One HBM pass of the streaming path: tile = 2^q amplitudes gathered from the
 // global qubits local[0..q).
 struct Pass {
@@ -67,8 +75,9 @@ struct Pass {
   // register bits (ψ alone fits 16 amplitudes per thread; fewer windows, less
   // shared-memory traffic); 0 = the kernels share wins / wops
   int32_t f_rb = 0;
-  std::vector<WinDev> fwins;
+  std::vector<WinHost> fwins;
   std::vector<WOp> fwops;
+  std::vector<WinHost> hwins;      // wins as the generator reads them
 };
 
 struct ProfRec {

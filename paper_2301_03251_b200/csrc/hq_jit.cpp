@@ -753,22 +753,22 @@ struct Gen {
   // cover the four classes (plan_windows picks them that way).
   static uint32_t pad(uint32_t j) { return j + (j >> 4) + (j >> 8); }
   static int bit_of(uint16_t m) { return 31 - __builtin_clz((unsigned)m); }  // raw bit behind swz(1<<b)
-  void win_tb(const WinDev& w, int tbits) {
+  void win_tb(const WinHost& w, int tbits) {
     o << "const uint32_t tb = 0u";
     for (int s = 0; s < tbits; ++s)
       o << " + ((tid & " << (1 << s) << ") ? " << pad(1u << bit_of(w.ps[s])) << "u : 0u)";
     o << ";\n";
   }
-  uint32_t phys(const WinDev& w, int i) const {
+  uint32_t phys(const WinHost& w, int i) const {
     uint32_t j = 0;
     for (int b = 0; b < RB; ++b)
       if (i >> b & 1) j |= 1u << bit_of(w.pr[b]);
     return pad(j);
   }
-  void load_regs(const WinDev& w, const char* arr, const char* tile) {
+  void load_regs(const WinHost& w, const char* arr, const char* tile) {
     for (int i = 0; i < N; ++i) o << arr << map[i] << " = " << tile << "[tb + " << phys(w, i) << "u];\n";
   }
-  void store_regs(const WinDev& w, const char* arr, const char* tile) {
+  void store_regs(const WinHost& w, const char* arr, const char* tile) {
     for (int i = 0; i < N; ++i) o << tile << "[tb + " << phys(w, i) << "u] = " << arr << map[i] << ";\n";
   }
 };
@@ -920,7 +920,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   Pass Pf;
   if (fsplit) {
     Pf = pl->passes[pi];
-    Pf.wins = Pf.fwins;
+    Pf.hwins = Pf.fwins;
     Pf.wops = Pf.fwops;
   }
   const Pass& P = fsplit ? Pf : pl->passes[pi];
@@ -963,7 +963,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   const int nwt = L.block / 32;   // warps per CTA (both tile groups in ping-pong kernels)
   const size_t pp_buf = ((size_t)(bwd ? 2 : 1) * (c64 ? 8 : 16) *
                          (((size_t)1 << g.Q) + ((size_t)1 << g.Q) / 16 + ((size_t)1 << g.Q) / 256) + 15) & ~(size_t)15;
-  const int nwin = (int)P.wins.size();
+  const int nwin = (int)P.hwins.size();
   std::ostringstream& o = g.o;
 
   std::vector<uint64_t> gbit(g.Q);
@@ -982,37 +982,37 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     std::snprintf(b, sizeof b, "0x%llxull", (unsigned long long)v);
     return std::string(b);
   };
-  auto Sbits = [&](const WinDev& W) {
+  auto Sbits = [&](const WinHost& W) {
     std::vector<int> v;
     for (int s2 = 0; s2 < tbits; ++s2) v.push_back(Gen::bit_of(W.ps[s2]));
     return v;
   };
-  auto Rbits = [&](const WinDev& W) {
+  auto Rbits = [&](const WinHost& W) {
     std::vector<int> v;
     for (int r = 0; r < g.RB; ++r) v.push_back(Gen::bit_of(W.pr[r]));
     return v;
   };
-  auto direct_ok = [&](const WinDev& W) {
+  auto direct_ok = [&](const WinHost& W) {
     const std::vector<int> S = Sbits(W);
     for (int k = 0; k < f; ++k)
       if (std::find(S.begin(), S.begin() + f, k) == S.begin() + f) return false;
     return true;
   };
   // per-thread global offset of window W's thread bits
-  auto emit_tw = [&](const WinDev& W) {
+  auto emit_tw = [&](const WinHost& W) {
     const std::vector<int> S = Sbits(W);
     o << "const uint64_t tw = 0ull";
     for (int s2 = 0; s2 < tbits; ++s2) o << " | ((tid & " << (1 << s2) << ") ? " << hex64(gbit[S[s2]]) << " : 0ull)";
     o << ";\n";
   };
-  auto reg_goff = [&](const WinDev& W, int i) {
+  auto reg_goff = [&](const WinHost& W, int i) {
     const std::vector<int> R = Rbits(W);
     uint32_t m = 0;
     for (int r = 0; r < g.RB; ++r)
       if (i >> r & 1) m |= 1u << R[r];
     return goff(m);
   };
-  auto direct_load = [&](const WinDev& W, bool lam) {
+  auto direct_load = [&](const WinHost& W, bool lam) {
     o << "{\n";
     emit_tw(W);
     for (int i = 0; i < g.N; ++i) {
@@ -1023,7 +1023,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   };
   // ψ goes to gout (the next checkpoint, or in place); backward passes with
   // checkpoints have gout == null and store only λ
-  auto direct_store = [&](const WinDev& W, bool lam) {
+  auto direct_store = [&](const WinHost& W, bool lam) {
     o << "{\n";
     emit_tw(W);
     if (lam) o << "if (gout) {\n";
@@ -1046,7 +1046,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   // slot unchanged.  sw: (register bit r of A, lane s); perm[r2] = A-register
   // bit that holds B's register qubit r2 after the swaps.
   const bool use_shfl = shfl_enabled() && !std::getenv("HQ_ABLATE");
-  auto shfl_ok = [&](const WinDev& A, const WinDev& B, std::vector<std::pair<int, int>>& sw,
+  auto shfl_ok = [&](const WinHost& A, const WinHost& B, std::vector<std::pair<int, int>>& sw,
                      std::vector<int>& perm) -> bool {
     if (!use_shfl) return false;
     const std::vector<int> RA = Rbits(A), RB2 = Rbits(B), SA = Sbits(A), SB = Sbits(B);
@@ -1113,7 +1113,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   // (4 CTAs/SM at 256 threads: cfg4 forward 95.8 -> 94.4 ms c128, 39.3 -> 38.1
   // ms c64 vs 80 registers / 3 CTAs, profiles/r02_fwdminb.log)
   // (16 complex128 amplitudes per thread in split forward kernels: 128)
-  int minb = std::max(1, 65536 / (g.T * (bwd || (!c64 && g.N == 16) ? 128 : 64)));
+  int minb = std::max(1, 65536 / (g.T * (bwd || (!c64 && g.N == 16) || (c64 && g.N == 32) ? 128 : 64)));
   if (const char* e = std::getenv(bwd ? "HQ_BWD_MINB" : "HQ_FWD_MINB")) minb = std::max(1, std::atoi(e));
   if (pp) minb = 1;
   o << "extern \"C\" __global__ void __launch_bounds__(" << L.block << ", " << minb << ") "
@@ -1197,7 +1197,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     for (int k = 0; k < (int)P.wops.size(); ++k)
       if (P.wops[k].dl >= 0) { stop_op = k; break; }
     for (int w = 0; w < nwin; ++w)
-      if (P.wins[w].op1 > stop_op) { stop_win = w; break; }
+      if (P.hwins[w].op1 > stop_op) { stop_win = w; break; }
   }
 
   // derivative accumulators in registers across the tile loop when the pass
@@ -1256,7 +1256,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     if (const char* e = std::getenv("HQ_WARP_SYNC_FWD")) wsync_on = std::atoi(e) != 0;
   wsync_on = wsync_on && !pp && tbits >= 5;
   auto pre_store_sync = [&]() { if (!wsync_on) sync(); };
-  auto post_store_sync = [&](const WinDev& A, const WinDev& B) {
+  auto post_store_sync = [&](const WinHost& A, const WinHost& B) {
     if (ablate & 16) return;   // timing study only: no barrier (races; wrong results)
     if (!wsync_on) { sync(); return; }
     // warp-index slots keeping their qubit: only warps differing in the other
@@ -1414,7 +1414,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
   bool regs_live = false;  // registers hold the current window's data
   if (fwd) {
     // -- stage in ψ
-    const WinDev& W0 = P.wins[0];
+    const WinHost& W0 = P.hwins[0];
     identity_map();
     if (first) {
       o << "{ auto goff_j = [&](uint32_t j) { uint64_t r = 0; for (int b = 0; b < Q; ++b) if ((j >> b) & 1u) "
@@ -1449,7 +1449,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     // -- forward windows
     bool fwd_shfl_in = false;   // this window's registers arrive by shuffles
     for (int w = 0; w < nwin; ++w) {
-      const WinDev& W = P.wins[w];
+      const WinHost& W = P.hwins[w];
       o << "{ // window " << w << "\n";
       g.ph_decl = false;
       g.win_tb(W, tbits);
@@ -1464,14 +1464,14 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       hoist(ks);
       std::vector<std::pair<int, int>> sw;
       std::vector<int> perm;
-      if (w < nwin - 1 && shfl_ok(W, P.wins[w + 1], sw, perm)) {
+      if (w < nwin - 1 && shfl_ok(W, P.hwins[w + 1], sw, perm)) {
         // registers stay live across the transition: declared outside the window block
         emit_steps(ks, 0, false, [&] { g.flush_vph(false); g.flush_pending(false); emit_shfl(sw, perm, false); }, ubudget);
         o << "}\n";
         identity_map();   // every branch path ended canonical
         fwd_shfl_in = true;
       } else if (w < nwin - 1) {
-        emit_steps(ks, 0, false, [&] { g.flush_vph(false); g.flush_pending(false); pre_store_sync(); g.store_regs(W, "p", "tp"); post_store_sync(W, P.wins[w + 1]); }, ubudget);
+        emit_steps(ks, 0, false, [&] { g.flush_vph(false); g.flush_pending(false); pre_store_sync(); g.store_regs(W, "p", "tp"); post_store_sync(W, P.hwins[w + 1]); }, ubudget);
         o << "}\n";
       } else if (fused) {
         for (int k : ks) g.apply(P.wops[k], false, false);
@@ -1486,7 +1486,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       }
     }
     // fused: the last window's block is still open here
-    const WinDev& WL = P.wins[nwin - 1];
+    const WinHost& WL = P.hwins[nwin - 1];
     if (fused && pl->perm) {
       // readout through the folded trailing permutation: w(P g), P's output bit
       // for measured qubit m = parity(g & mask_m) ^ c_m, g = global index
@@ -1558,7 +1558,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     }
   }
   if (bwd) {
-    const WinDev& WL = P.wins[nwin - 1];
+    const WinHost& WL = P.hwins[nwin - 1];
     if (!fused) {
       identity_map();
       if (direct_ok(WL)) {
@@ -1580,7 +1580,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
     for (int wi = 0; wi < nwin; ++wi) {
       const int w = nwin - 1 - wi;
       if (first && w < stop_win) break;
-      const WinDev& W = P.wins[w];
+      const WinHost& W = P.hwins[w];
       const bool cont = wi == 0 && regs_live;  // block already open, registers hold window w
       if (!cont) {
         o << "{ // window " << w << " (adjoint)\n";
@@ -1722,7 +1722,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
       }
       std::vector<std::pair<int, int>> sw;
       std::vector<int> perm;
-      const bool to_shfl = w > 0 && shfl_ok(W, P.wins[w - 1], sw, perm);
+      const bool to_shfl = w > 0 && shfl_ok(W, P.hwins[w - 1], sw, perm);
       emit_steps(ks, 0, true, [&] {
         g.flush_batch();
         g.flush_vph(true);
@@ -1736,7 +1736,7 @@ static std::string gen_pass(const hq_plan_s* pl, int pi, int mode) {
         pre_store_sync();
         g.store_regs(W, "p", "tp");
         g.store_regs(W, "l", "tl");
-        post_store_sync(W, P.wins[w - 1]);
+        post_store_sync(W, P.hwins[w - 1]);
       }, ubudget);
       o << "}\n";
       if (to_shfl) identity_map();   // every branch path ended canonical
