@@ -1292,7 +1292,8 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
       const size_t first = best.empty() ? 0 : best[0].op_ids.size();
       // small plans: nothing to gain; long ones (cfg5: 59 passes) gain nothing
       // measurable from the first pass's cap and pay ~10 s of window counting
-      if (!search || best.size() < 4 || best.size() > 24 || first < 64) return best;
+      const bool force = ps_env && ps_env[0] == '2';   // HQ_PLAN_SEARCH=2: also long plans
+      if (!search || best.size() < 4 || (best.size() > 24 && !force) || first < 64) return best;
       size_t best_cost = count_windows(best) + pass_w * best.size();
       const size_t oc = (try_cap && best[0].op_ids.size() <= kC128PassOps) ? kC128PassOps : op_cap;
       for (int pct : {95, 91, 87, 83, 79, 75}) {
