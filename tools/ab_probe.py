@@ -2,6 +2,8 @@
 process: every variant's plan is built first (its env applied while the
 kernels are generated), then forward+adjoint steps alternate A, B, A, B, ...
 so clock / power drift hits all variants alike; medians of the device times.
+Each plan's kernels keep the launch geometry they were generated with, so
+knobs read at launch time (HQ_PINGPONG, HQ_DOT_GROUP) vary per plan too.
 
   python tools/ab_probe.py cfg4 1024 c64 "HQ_WARP_SYNC=0" "HQ_WARP_SYNC=1" [rounds]
 """
