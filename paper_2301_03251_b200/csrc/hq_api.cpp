@@ -90,7 +90,8 @@ int tile_bits_for(int precision) { return precision == HQ_C64 ? 12 : 11; }
 int fixed_bits_for(int precision) {
   if (const char* e = std::getenv("HQ_FIXED_BITS")) return std::atoi(e);   // test hook
   // 128-byte runs: whole L2 lines per tile visit (measured: forward passes
-  // 4.6 -> 5.3 TB/s on cfg4 despite 17 instead of 15 passes)
+  // 4.6 -> 5.3 TB/s on cfg4 despite 17 instead of 15 passes).  complex128
+  // plans with dense passes drop to 2 fixed bits at schedule time (below).
   return precision == HQ_C64 ? 4 : 3;
 }
 
@@ -1194,7 +1195,7 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
       delete pl;
       return fail(HQ_E_CONFIG, "circuit too small for the streaming path");
     }
-    const int f = std::min(fixed_bits_for(d->precision), pl->tile_bits - 2);
+    int f = std::min(fixed_bits_for(d->precision), pl->tile_bits - 2);
     pl->fixed_bits = f;
     // SWAP(a,b) = CNOT(a,b) CNOT(b,a) CNOT(a,b): register windows only permute along one bit
     std::vector<hq_op> g2;
@@ -1303,6 +1304,21 @@ static hq_status plan_create_impl(const hq_plan_desc* d, hq_plan* out, int opts)
       }
       return best;
     };
+    // complex128 with dense passes: 64-byte runs (2 fixed bits).  Its pass
+    // kernels are FP64-bound when a pass carries many gates, and the freer
+    // tile choice needs fewer passes (cfg4: 8 -> 6, 336.9 -> 335.9 ms forward
+    // + adjoint at B=1024; bench 3,019 -> 3,052 samples/s), while sparse
+    // passes stay HBM-bound and want whole 128-byte lines (cfg5, ~32 gates
+    // per pass: forward 1.86 s with 3 fixed bits, 2.09 s with 2;
+    // profiles/r02_compiler_ab.log).  Rule: >= 4 passes of >= 48 gates each
+    // on average with 3 fixed bits.  HQ_FIXED_BITS overrides.
+    if (d->precision == HQ_C128 && !std::getenv("HQ_FIXED_BITS") && f == 3 && !(opts & kSmallPasses)) {
+      const auto probe = schedule_passes(gates, n, pl->tile_bits, f, 0, op_cap);
+      if (probe.size() >= 4 && gates.size() >= 48 * probe.size()) {
+        f = 2;
+        pl->fixed_bits = f;
+      }
+    }
     pl->passes = schedule(0);
 
     // ---- fold leading single-qubit gates into the initial product state ----
